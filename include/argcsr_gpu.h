@@ -1,0 +1,188 @@
+/*
+ * argcsr_gpu.h — C-ABI of the B200-native ARG-CSR hot path.
+ *
+ * Drop-in boundary for the reference library `argcsr` (arxiv/paper_1203_5737,
+ * /root/reference/proj).  Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference).  Plain pointers and sizes only:
+ * no C++ or torch types cross this boundary, so the reference's C++ API
+ * (include/argcsr_gpu.hpp), its pybind11 module (paper_1203_5737_b200) and any
+ * other FFI (ctypes, cgo, JNI, ...) bind the same symbols.
+ *
+ * Conventions
+ *   - Every function returns an argcsr_status; on failure a thread-local
+ *     message is available from argcsr_last_error().  The C++ shim rethrows the
+ *     status as the matching proj/include/argcsr/errors.hpp class.
+ *   - Validation order and messages follow the reference: threads_per_group /
+ *     desired_chunk_size first (argcsr.cpp:20-23), then an empty matrix
+ *     (argcsr.cpp:24-26), then vector lengths (argcsr.cpp:220-223).
+ *   - A handle owns device memory on one device and is immutable after
+ *     argcsr_dev_convert; calls on different handles/streams may run
+ *     concurrently.  `stream` is a cudaStream_t passed as void* (NULL = the
+ *     legacy default stream).
+ *   - argcsr_dev_spmv* on device pointers are stream-ordered and never
+ *     synchronise except to report an error.  Calls with host pointers are
+ *     synchronous, like the reference's value-returning functions.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point fails with ARGCSR_E_CUDA.
+ */
+#ifndef ARGCSR_GPU_H
+#define ARGCSR_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ARGCSR_GPU_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ARGCSR_API __attribute__((visibility("default")))
+#else
+#define ARGCSR_API
+#endif
+
+typedef enum {
+    ARGCSR_OK = 0,
+    ARGCSR_E_PARAMETER = 1,   /* argcsr::ParameterError   (errors.hpp:27) */
+    ARGCSR_E_DIMENSION = 2,   /* argcsr::DimensionError   (errors.hpp:21) */
+    ARGCSR_E_BOUNDS = 3,      /* argcsr::BoundsError      (errors.hpp:15) */
+    ARGCSR_E_INTERNAL = 4,    /* argcsr::InternalError    (errors.hpp:33) */
+    ARGCSR_E_CUDA = 5,        /* CUDA runtime/driver failure -> InternalError subclass */
+    ARGCSR_E_NCCL = 6,        /* collective failure          -> InternalError subclass */
+    ARGCSR_E_OOM = 7,         /* device or pinned-host allocation failed */
+    ARGCSR_E_FORMAT = 8,      /* argcsr::FormatError      (errors.hpp:51) */
+    ARGCSR_E_IO = 9,          /* argcsr::IoError          (errors.hpp:57) */
+    ARGCSR_E_PARSE = 10,      /* argcsr::ParseError       (errors.hpp:39) */
+    ARGCSR_E_UNSUPPORTED = 11 /* argcsr::UnsupportedError (errors.hpp:45) */
+} argcsr_status;
+
+typedef enum { ARGCSR_F64 = 0, ARGCSR_F32 = 1 } argcsr_dtype;
+
+typedef enum { ARGCSR_HOST = 0, ARGCSR_DEVICE = 1 } argcsr_memspace;
+
+/* A CSR matrix (proj/include/argcsr/core.hpp:31-41): row i owns
+ * [row_pointers[i], row_pointers[i+1]) of columns/values.  Pointers are host
+ * or device memory according to `space`.  Like the reference converter, the
+ * device converter neither validates nor re-sorts entries (argcsr.cpp:107-117). */
+typedef struct {
+    uint64_t num_rows;
+    uint64_t num_cols;
+    uint64_t nnz;
+    const uint64_t* row_pointers; /* [num_rows + 1] */
+    const int32_t* columns;       /* [nnz] */
+    const void* values;           /* [nnz] of dtype */
+    argcsr_dtype dtype;
+    argcsr_memspace space;
+} argcsr_csr_view;
+
+/* Opaque device-resident ARG-CSR matrix (proj/include/argcsr/argcsr.hpp:52-63). */
+typedef struct argcsr_dev argcsr_dev;
+
+typedef struct {
+    uint64_t num_rows;
+    uint64_t num_cols;
+    uint64_t threads_per_group;
+    uint64_t desired_chunk_size;
+    uint64_t num_groups;       /* ArgCsrMatrix::groups.size() */
+    uint64_t total_slots;      /* ArgCsrMatrix::total_slots() (argcsr.hpp:61) */
+    uint64_t nnz;              /* explicit entries */
+    uint64_t heavy_groups;     /* groups scheduled on the long-chunk path */
+    uint64_t light_tiles;      /* CTA tiles of the short-chunk path */
+    uint64_t max_chunk_size;
+    uint64_t device_bytes;     /* device memory held by the handle */
+    int32_t device;
+    argcsr_dtype dtype;
+} argcsr_dev_info_t;
+
+/* ---------------------------------------------------------------- conversion */
+
+/* Replaces argcsr::argcsr_from_csr(const CsrMatrix&, tpg = 128, dcs = 1)
+ * (argcsr.hpp:101-104, argcsr.cpp:123-155).  Runs row_nnz, partition_groups,
+ * assign_threads, the inclusive threads_mapping scan and layout_group as GPU
+ * kernels on `device`; the result is bit-exact with the reference arrays
+ * (see argcsr_dev_export).  Host-space inputs are copied to the device.
+ * Synchronises `stream` (group and slot counts size the allocations). */
+ARGCSR_API argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t threads_per_group,
+                                 uint64_t desired_chunk_size, int device, void* stream,
+                                 argcsr_dev** out);
+
+ARGCSR_API argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info);
+
+/* Copies the reference layout to HOST memory, widened to the reference field
+ * types (argcsr.hpp:23-30, 52-63).  Any pointer may be NULL to skip it.
+ *   groups4          [num_groups * 4] u64: first_row, size, offset, chunk_size
+ *   threads_mapping  [num_rows] u64 (per-group inclusive scan)
+ *   values           [total_slots] f64 (or f32 for an F32 handle); padding +0.0
+ *   columns          [total_slots] i32; padding -1 (core.hpp:15)           */
+ARGCSR_API argcsr_status argcsr_dev_export(const argcsr_dev* m, uint64_t* groups4, uint64_t* threads_mapping,
+                                void* values, int32_t* columns);
+
+/* --------------------------------------------------------------------- SpMV */
+
+/* y = A x on device pointers, stream-ordered: x[num_cols], y[num_rows] of the
+ * handle's dtype.  Replaces spmv_argcsr / spmv_argcsr_parallel
+ * (argcsr.cpp:219-227, bench.cpp:109-116).  fp64 results are bit-identical to
+ * the reference (same per-chunk and per-row summation order, no FMA). */
+ARGCSR_API argcsr_status argcsr_dev_spmv(const argcsr_dev* m, const void* x, void* y, void* stream);
+
+/* Group-range kernel (argcsr.hpp:114-116, argcsr.cpp:185-217): writes only the
+ * rows of groups [group_begin, group_end); no length check, like the reference. */
+ARGCSR_API argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_t group_begin,
+                                     uint64_t group_end, void* y, void* stream);
+
+/* Host-buffer form of spmv_argcsr (argcsr.cpp:219-227): checks x_len ==
+ * num_cols (DimensionError, same message shape), copies x in, multiplies,
+ * copies y (num_rows entries) out, synchronises. */
+ARGCSR_API argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x, uint64_t x_len, void* y);
+
+/* Same, with caller-pinned host buffers and caller-owned device staging
+ * (x_dev/y_dev), on `stream`: H2D x, SpMV, D2H y, then synchronise.  The
+ * end-to-end path bench.py times. */
+ARGCSR_API argcsr_status argcsr_dev_spmv_host_staged(const argcsr_dev* m, const void* x_host, void* x_dev,
+                                          void* y_dev, void* y_host, void* stream);
+
+/* ----------------------------------------------------------- accessors / next */
+
+/* csr_from_argcsr (argcsr.cpp:157-183) on the device: writes the lossless CSR
+ * back into HOST arrays row_pointers[num_rows+1], columns[nnz], values[nnz]. */
+ARGCSR_API argcsr_status argcsr_dev_to_csr(const argcsr_dev* m, uint64_t* row_pointers, int32_t* columns,
+                                void* values);
+
+/* chunk_entries (argcsr.cpp:229-249): non-sentinel entries of chunk (g, c) in
+ * storage order into host arrays of capacity `cap`; *n gets the count.
+ * BoundsError on a bad group or chunk index. */
+ARGCSR_API argcsr_status argcsr_dev_chunk_entries(const argcsr_dev* m, uint64_t group_index,
+                                       uint64_t chunk_index, void* values, int32_t* columns,
+                                       uint64_t cap, uint64_t* n);
+
+/* padding_stats(const ArgCsrMatrix&) (analysis.cpp:167-184) reduced on the device. */
+typedef struct {
+    uint64_t explicit_nnz;
+    uint64_t assigned_padded_slots;
+    uint64_t total_allocated_slots;
+    double padding_ratio;
+    uint64_t estimated_bytes;
+} argcsr_format_stats;
+ARGCSR_API argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_format_stats* out);
+
+ARGCSR_API void argcsr_dev_free(argcsr_dev* m);
+
+/* ------------------------------------------------------ multi-GPU row slices */
+
+/* nnz-balanced contiguous row split: row_begin[p] =
+ * lower_bound(row_pointers, p*nnz/parts), row_begin[parts] = num_rows; rows of
+ * each part >= 1 when num_rows >= parts.  row_pointers is host memory. */
+ARGCSR_API argcsr_status argcsr_partition_rows(const uint64_t* row_pointers, uint64_t num_rows,
+                                    uint32_t parts, uint64_t* row_begin);
+
+/* ------------------------------------------------------------------- errors */
+ARGCSR_API const char* argcsr_last_error(void);
+ARGCSR_API const char* argcsr_status_name(argcsr_status s);
+ARGCSR_API int argcsr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARGCSR_GPU_H */

@@ -1,0 +1,444 @@
+// pybind11 module `_argcsr_gpu`: the reference's Python bindings
+// (proj/python/bindings.cpp:13-173) re-pointed at the C-ABI.  Names, argument
+// names and defaults follow the reference module; every error surfaces as
+// `Error` or one of its subclasses (bindings.cpp:15).  Large arrays cross as
+// numpy buffers instead of Python lists.
+#include <pybind11/numpy.h>
+#include <pybind11/operators.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <tuple>
+
+#include "argcsr_gpu.hpp"
+
+namespace py = pybind11;
+using namespace argcsr_b200;
+
+namespace {
+
+// csr_from_triplets (core.hpp:48-49, core.cpp:7-48 semantics): bounds checks,
+// (row, col) sort, duplicates summed in sorted order, explicit zeros kept.
+struct Triplet {
+    std::size_t row, col;
+    double value;
+};
+
+CsrMatrix csr_from_triplets(std::size_t num_rows, std::size_t num_cols, std::vector<Triplet> entries) {
+    if (num_rows == 0 || num_cols == 0)
+        throw DimensionError("csr_from_triplets: matrix dimensions must be at least 1x1");
+    for (const Triplet& t : entries)
+        if (t.row >= num_rows || t.col >= num_cols)
+            throw BoundsError("csr_from_triplets: entry (" + std::to_string(t.row) + ", " + std::to_string(t.col) +
+                              ") outside " + std::to_string(num_rows) + "x" + std::to_string(num_cols));
+    std::sort(entries.begin(), entries.end(), [](const Triplet& a, const Triplet& b) {
+        return a.row != b.row ? a.row < b.row : a.col < b.col;
+    });
+    CsrMatrix A;
+    A.num_rows = num_rows;
+    A.num_cols = num_cols;
+    A.row_pointers.assign(num_rows + 1, 0);
+    for (std::size_t i = 0; i < entries.size();) {
+        double sum = entries[i].value;
+        std::size_t j = i + 1;
+        while (j < entries.size() && entries[j].row == entries[i].row && entries[j].col == entries[i].col)
+            sum += entries[j++].value;
+        A.values.push_back(sum);
+        A.columns.push_back(static_cast<index_t>(entries[i].col));
+        A.row_pointers[entries[i].row + 1] += 1;
+        i = j;
+    }
+    for (std::size_t r = 0; r < num_rows; ++r) A.row_pointers[r + 1] += A.row_pointers[r];
+    return A;
+}
+
+template <typename T>
+py::array_t<T> view_of(const std::vector<T>& v, py::handle base) {
+    return py::array_t<T>({v.size()}, {sizeof(T)}, v.data(), base);
+}
+
+template <typename T>
+std::vector<T> vec_from(const py::array_t<T, py::array::c_style | py::array::forcecast>& a) {
+    return std::vector<T>(a.data(), a.data() + a.size());
+}
+
+// Python-side ARG-CSR matrix: the device handle plus a lazily exported
+// reference-layout host copy (argcsr.hpp:52-63 fields).
+struct PyArgCsr {
+    std::shared_ptr<DeviceArgCsr> dev;
+    mutable std::optional<std::vector<uint64_t>> groups4, tm;
+    mutable std::optional<py::array> values;
+    mutable std::optional<std::vector<int32_t>> columns;
+
+    const argcsr_dev_info_t& info() const { return dev->info(); }
+    void need_meta() const {
+        if (groups4) return;
+        std::vector<uint64_t> g(4 * info().num_groups), t(info().num_rows);
+        check(argcsr_dev_export(dev->handle(), g.data(), t.data(), nullptr, nullptr));
+        groups4 = std::move(g);
+        tm = std::move(t);
+    }
+    void need_slots() const {
+        if (columns) return;
+        const std::size_t S = info().total_slots;
+        py::array v = info().dtype == ARGCSR_F64 ? py::array(py::dtype::of<double>(), {S})
+                                                 : py::array(py::dtype::of<float>(), {S});
+        std::vector<int32_t> c(S);
+        check(argcsr_dev_export(dev->handle(), nullptr, nullptr, v.mutable_data(), c.data()));
+        values = v;
+        columns = std::move(c);
+    }
+};
+
+PyArgCsr make_handle(argcsr_dev* h) {
+    PyArgCsr p;
+    p.dev = std::make_shared<DeviceArgCsr>(h);
+    return p;
+}
+
+PyArgCsr convert_arrays(std::size_t num_rows, std::size_t num_cols, py::array row_pointers, py::array columns,
+                        py::array values, std::size_t tpg, std::size_t dcs, int device) {
+    auto rp = py::array_t<uint64_t, py::array::c_style | py::array::forcecast>(row_pointers);
+    auto cl = py::array_t<int32_t, py::array::c_style | py::array::forcecast>(columns);
+    argcsr_csr_view v{};
+    v.num_rows = num_rows;
+    v.num_cols = num_cols;
+    v.space = ARGCSR_HOST;
+    v.row_pointers = rp.data();
+    v.columns = cl.data();
+    if (rp.size() != py::ssize_t(num_rows + 1) && num_rows != 0)
+        throw DimensionError("argcsr_from_csr: row_pointers length does not match num_rows + 1");
+    py::array vals;
+    if (py::dtype(values.dtype()).is(py::dtype::of<float>())) {
+        vals = py::array_t<float, py::array::c_style | py::array::forcecast>(values);
+        v.dtype = ARGCSR_F32;
+    } else {
+        vals = py::array_t<double, py::array::c_style | py::array::forcecast>(values);
+        v.dtype = ARGCSR_F64;
+    }
+    if (vals.size() != cl.size()) throw DimensionError("argcsr_from_csr: values and columns lengths differ");
+    v.nnz = uint64_t(cl.size());
+    v.values = vals.data();
+    argcsr_dev* h = nullptr;
+    {
+        py::gil_scoped_release nogil;
+        check(argcsr_dev_convert(&v, tpg, dcs, device, nullptr, &h));
+    }
+    return make_handle(h);
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_argcsr_gpu, m) {
+    m.doc() = "B200-native adaptive row-grouped CSR (ARG-CSR): GPU conversion and SpMV behind the argcsr API";
+
+    py::register_exception_translator([](std::exception_ptr p) {
+        if (!p) return;
+        try {
+            std::rethrow_exception(p);
+        } catch (const Error& e) {
+            const char* name = "Error";
+            if (dynamic_cast<const ParameterError*>(&e)) name = "ParameterError";
+            else if (dynamic_cast<const DimensionError*>(&e)) name = "DimensionError";
+            else if (dynamic_cast<const BoundsError*>(&e)) name = "BoundsError";
+            else if (dynamic_cast<const CudaError*>(&e)) name = "CudaError";
+            else if (dynamic_cast<const NcclError*>(&e)) name = "NcclError";
+            else if (dynamic_cast<const OutOfMemoryError*>(&e)) name = "OutOfMemoryError";
+            else if (dynamic_cast<const InternalError*>(&e)) name = "InternalError";
+            else if (dynamic_cast<const UnsupportedError*>(&e)) name = "UnsupportedError";
+            else if (dynamic_cast<const FormatError*>(&e)) name = "FormatError";
+            else if (dynamic_cast<const IoError*>(&e)) name = "IoError";
+            else if (dynamic_cast<const ParseError*>(&e)) name = "ParseError";
+            else if (dynamic_cast<const CorrectnessError*>(&e)) name = "CorrectnessError";
+            py::object cls = py::module_::import("paper_1203_5737_b200._errors").attr(name);
+            PyErr_SetString(cls.ptr(), e.what());
+        }
+    });
+
+    m.attr("kDefaultThreadsPerGroup") = kDefaultThreadsPerGroup;
+    m.attr("kDefaultDesiredChunkSize") = kDefaultDesiredChunkSize;
+    m.attr("kPaddingColumn") = kPaddingColumn;
+    m.def("abi_version", &argcsr_abi_version);
+
+    py::class_<CsrMatrix>(m, "CsrMatrix")
+        .def(py::init<>())
+        .def_readonly("num_rows", &CsrMatrix::num_rows)
+        .def_readonly("num_cols", &CsrMatrix::num_cols)
+        .def_property_readonly("values", [](py::object self) { return view_of(self.cast<const CsrMatrix&>().values, self); })
+        .def_property_readonly("columns", [](py::object self) { return view_of(self.cast<const CsrMatrix&>().columns, self); })
+        .def_property_readonly("row_pointers", [](py::object self) {
+            const auto& rp = self.cast<const CsrMatrix&>().row_pointers;
+            return py::array_t<uint64_t>({rp.size()}, {sizeof(uint64_t)}, reinterpret_cast<const uint64_t*>(rp.data()), self);
+        })
+        .def_property_readonly("nnz", &CsrMatrix::nnz)
+        .def_static(
+            "from_arrays",
+            [](std::size_t num_rows, std::size_t num_cols, py::array_t<uint64_t, py::array::c_style | py::array::forcecast> rp,
+               py::array_t<int32_t, py::array::c_style | py::array::forcecast> cols,
+               py::array_t<double, py::array::c_style | py::array::forcecast> vals) {
+                if (rp.size() != py::ssize_t(num_rows + 1)) throw DimensionError("from_arrays: row_pointers length");
+                if (cols.size() != vals.size()) throw DimensionError("from_arrays: columns/values length");
+                CsrMatrix A;
+                A.num_rows = num_rows;
+                A.num_cols = num_cols;
+                A.row_pointers.assign(rp.data(), rp.data() + rp.size());
+                A.columns = vec_from<int32_t>(cols);
+                A.values = vec_from<double>(vals);
+                return A;
+            },
+            py::arg("num_rows"), py::arg("num_cols"), py::arg("row_pointers"), py::arg("columns"), py::arg("values"))
+        .def(py::self == py::self)
+        .def("__repr__", [](const CsrMatrix& A) {
+            return "CsrMatrix(" + std::to_string(A.num_rows) + "x" + std::to_string(A.num_cols) +
+                   ", nnz=" + std::to_string(A.nnz()) + ")";
+        });
+
+    py::class_<GroupInfo>(m, "GroupInfo")
+        .def(py::init([](std::size_t f, std::size_t s, std::size_t o, std::size_t c) { return GroupInfo{f, s, o, c}; }),
+             py::arg("first_row") = 0, py::arg("size") = 0, py::arg("offset") = 0, py::arg("chunk_size") = 0)
+        .def_readonly("first_row", &GroupInfo::first_row)
+        .def_readonly("size", &GroupInfo::size)
+        .def_readonly("offset", &GroupInfo::offset)
+        .def_readonly("chunk_size", &GroupInfo::chunk_size)
+        .def(py::self == py::self)
+        .def("__repr__", [](const GroupInfo& g) {
+            return "GroupInfo(" + std::to_string(g.first_row) + ", " + std::to_string(g.size) + ", " +
+                   std::to_string(g.offset) + ", " + std::to_string(g.chunk_size) + ")";
+        });
+
+    py::class_<FormatStats>(m, "FormatStats")
+        .def_readonly("explicit_nnz", &FormatStats::explicit_nnz)
+        .def_readonly("assigned_padded_slots", &FormatStats::assigned_padded_slots)
+        .def_readonly("total_allocated_slots", &FormatStats::total_allocated_slots)
+        .def_readonly("padding_ratio", &FormatStats::padding_ratio)
+        .def_readonly("estimated_bytes", &FormatStats::estimated_bytes);
+
+    py::class_<PyArgCsr>(m, "ArgCsrMatrix")
+        .def_property_readonly("num_rows", [](const PyArgCsr& p) { return p.info().num_rows; })
+        .def_property_readonly("num_cols", [](const PyArgCsr& p) { return p.info().num_cols; })
+        .def_property_readonly("threads_per_group", [](const PyArgCsr& p) { return p.info().threads_per_group; })
+        .def_property_readonly("desired_chunk_size", [](const PyArgCsr& p) { return p.info().desired_chunk_size; })
+        .def_property_readonly("total_slots", [](const PyArgCsr& p) { return p.info().total_slots; })
+        .def_property_readonly("num_groups", [](const PyArgCsr& p) { return p.info().num_groups; })
+        .def_property_readonly("nnz", [](const PyArgCsr& p) { return p.info().nnz; })
+        .def_property_readonly("heavy_groups", [](const PyArgCsr& p) { return p.info().heavy_groups; })
+        .def_property_readonly("light_tiles", [](const PyArgCsr& p) { return p.info().light_tiles; })
+        .def_property_readonly("max_chunk_size", [](const PyArgCsr& p) { return p.info().max_chunk_size; })
+        .def_property_readonly("device_bytes", [](const PyArgCsr& p) { return p.info().device_bytes; })
+        .def_property_readonly("device", [](const PyArgCsr& p) { return p.info().device; })
+        .def_property_readonly("dtype", [](const PyArgCsr& p) { return p.info().dtype == ARGCSR_F64 ? "float64" : "float32"; })
+        .def_property_readonly("groups", [](const PyArgCsr& p) {
+            p.need_meta();
+            std::vector<GroupInfo> out(p.info().num_groups);
+            const auto& g = *p.groups4;
+            for (std::size_t i = 0; i < out.size(); ++i) out[i] = {g[4 * i], g[4 * i + 1], g[4 * i + 2], g[4 * i + 3]};
+            return out;
+        })
+        .def_property_readonly("groups_array", [](py::object self) {
+            const auto& p = self.cast<const PyArgCsr&>();
+            p.need_meta();
+            return py::array_t<uint64_t>({p.groups4->size() / 4, std::size_t(4)}, {4 * sizeof(uint64_t), sizeof(uint64_t)},
+                                         p.groups4->data(), self);
+        })
+        .def_property_readonly("threads_mapping", [](py::object self) {
+            const auto& p = self.cast<const PyArgCsr&>();
+            p.need_meta();
+            return view_of(*p.tm, self);
+        })
+        .def_property_readonly("values", [](const PyArgCsr& p) {
+            p.need_slots();
+            return *p.values;
+        })
+        .def_property_readonly("columns", [](py::object self) {
+            const auto& p = self.cast<const PyArgCsr&>();
+            p.need_slots();
+            return view_of(*p.columns, self);
+        })
+        .def("spmv_device",
+             [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t y, std::uintptr_t stream) {
+                 check(argcsr_dev_spmv(p.dev->handle(), reinterpret_cast<const void*>(x), reinterpret_cast<void*>(y),
+                                       reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
+        .def("spmv_groups_device",
+             [](const PyArgCsr& p, std::uintptr_t x, std::uint64_t gb, std::uint64_t ge, std::uintptr_t y,
+                std::uintptr_t stream) {
+                 check(argcsr_dev_spmv_groups(p.dev->handle(), reinterpret_cast<const void*>(x), gb, ge,
+                                              reinterpret_cast<void*>(y), reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_ptr"), py::arg("group_begin"), py::arg("group_end"), py::arg("y_ptr"), py::arg("stream") = 0)
+        .def("spmv_host_staged",
+             [](const PyArgCsr& p, std::uintptr_t xh, std::uintptr_t xd, std::uintptr_t yd, std::uintptr_t yh,
+                std::uintptr_t stream) {
+                 py::gil_scoped_release nogil;
+                 check(argcsr_dev_spmv_host_staged(p.dev->handle(), reinterpret_cast<const void*>(xh),
+                                                   reinterpret_cast<void*>(xd), reinterpret_cast<void*>(yd),
+                                                   reinterpret_cast<void*>(yh), reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_host_ptr"), py::arg("x_dev_ptr"), py::arg("y_dev_ptr"), py::arg("y_host_ptr"), py::arg("stream") = 0)
+        .def("free", [](PyArgCsr& p) { p.dev->reset(); })
+        .def("__eq__", [](const PyArgCsr& a, const PyArgCsr& b) {
+            if (a.info().num_rows != b.info().num_rows || a.info().num_cols != b.info().num_cols ||
+                a.info().threads_per_group != b.info().threads_per_group || a.info().dtype != b.info().dtype)
+                return false;
+            a.need_meta(), b.need_meta(), a.need_slots(), b.need_slots();
+            if (*a.groups4 != *b.groups4 || *a.tm != *b.tm || *a.columns != *b.columns) return false;
+            return std::memcmp(a.values->data(), b.values->data(), a.values->nbytes()) == 0;
+        })
+        .def("__repr__", [](const PyArgCsr& p) {
+            return "ArgCsrMatrix(" + std::to_string(p.info().num_rows) + "x" + std::to_string(p.info().num_cols) +
+                   ", tpg=" + std::to_string(p.info().threads_per_group) + ", groups=" +
+                   std::to_string(p.info().num_groups) + ", slots=" + std::to_string(p.info().total_slots) +
+                   ", device=" + std::to_string(p.info().device) + ")";
+        });
+
+    m.def(
+        "csr_from_triplets",
+        [](std::size_t num_rows, std::size_t num_cols,
+           const std::vector<std::tuple<std::size_t, std::size_t, double>>& entries) {
+            std::vector<Triplet> ts;
+            ts.reserve(entries.size());
+            for (const auto& [r, c, v] : entries) ts.push_back({r, c, v});
+            return csr_from_triplets(num_rows, num_cols, std::move(ts));
+        },
+        py::arg("num_rows"), py::arg("num_cols"), py::arg("entries"),
+        "Builds CSR from (row, col, value) tuples; duplicates are summed.");
+
+    m.def(
+        "triplets_from_csr",
+        [](const CsrMatrix& A) {
+            std::vector<std::tuple<std::size_t, std::size_t, double>> out;
+            out.reserve(A.nnz());
+            for (std::size_t r = 0; r < A.num_rows; ++r)
+                for (std::size_t k = A.row_pointers[r]; k < A.row_pointers[r + 1]; ++k)
+                    out.emplace_back(r, std::size_t(A.columns[k]), A.values[k]);
+            return out;
+        },
+        py::arg("matrix"));
+
+    m.def(
+        "argcsr_from_csr",
+        [](const CsrMatrix& A, std::size_t tpg, std::size_t dcs, int device) {
+            argcsr_csr_view v{};
+            v.num_rows = A.num_rows;
+            v.num_cols = A.num_cols;
+            v.nnz = A.nnz();
+            v.row_pointers = reinterpret_cast<const uint64_t*>(A.row_pointers.data());
+            v.columns = A.columns.data();
+            v.values = A.values.data();
+            v.dtype = ARGCSR_F64;
+            v.space = ARGCSR_HOST;
+            argcsr_dev* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_dev_convert(&v, tpg, dcs, device, nullptr, &h));
+            }
+            return make_handle(h);
+        },
+        py::arg("matrix"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
+        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0);
+
+    m.def("argcsr_from_csr_arrays", &convert_arrays, py::arg("num_rows"), py::arg("num_cols"), py::arg("row_pointers"),
+          py::arg("columns"), py::arg("values"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
+          py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0);
+
+    m.def(
+        "argcsr_from_device_csr",
+        [](std::uint64_t num_rows, std::uint64_t num_cols, std::uint64_t nnz, std::uintptr_t rp, std::uintptr_t cols,
+           std::uintptr_t vals, const std::string& dtype, std::size_t tpg, std::size_t dcs, int device,
+           std::uintptr_t stream) {
+            argcsr_csr_view v{};
+            v.num_rows = num_rows;
+            v.num_cols = num_cols;
+            v.nnz = nnz;
+            v.row_pointers = reinterpret_cast<const uint64_t*>(rp);
+            v.columns = reinterpret_cast<const int32_t*>(cols);
+            v.values = reinterpret_cast<const void*>(vals);
+            if (dtype == "float64") v.dtype = ARGCSR_F64;
+            else if (dtype == "float32") v.dtype = ARGCSR_F32;
+            else throw ParameterError("argcsr_from_device_csr: dtype must be float64 or float32");
+            v.space = ARGCSR_DEVICE;
+            argcsr_dev* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_dev_convert(&v, tpg, dcs, device, reinterpret_cast<void*>(stream), &h));
+            }
+            return make_handle(h);
+        },
+        py::arg("num_rows"), py::arg("num_cols"), py::arg("nnz"), py::arg("row_pointers_ptr"), py::arg("columns_ptr"),
+        py::arg("values_ptr"), py::arg("dtype") = "float64", py::arg("threads_per_group") = kDefaultThreadsPerGroup,
+        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("stream") = 0);
+
+    m.def(
+        "csr_from_argcsr",
+        [](const PyArgCsr& p) {
+            if (p.info().dtype != ARGCSR_F64) throw UnsupportedError("csr_from_argcsr: fp32 handle");
+            return argcsr_b200::csr_from_argcsr(*p.dev);
+        },
+        py::arg("matrix"));
+
+    m.def(
+        "csr_arrays_from_argcsr",
+        [](const PyArgCsr& p) {
+            const std::size_t N = p.info().num_rows, nnz = p.info().nnz;
+            py::array_t<uint64_t> rp(N + 1);
+            py::array_t<int32_t> cols(nnz);
+            py::array vals = p.info().dtype == ARGCSR_F64 ? py::array(py::dtype::of<double>(), {nnz})
+                                                          : py::array(py::dtype::of<float>(), {nnz});
+            check(argcsr_dev_to_csr(p.dev->handle(), rp.mutable_data(), cols.mutable_data(), vals.mutable_data()));
+            return py::make_tuple(rp, cols, vals);
+        },
+        py::arg("matrix"));
+
+    m.def(
+        "spmv_host",
+        [](const PyArgCsr& p, py::array x) {
+            const bool f64 = p.info().dtype == ARGCSR_F64;
+            py::array xc = f64 ? py::array(py::array_t<double, py::array::c_style | py::array::forcecast>(x))
+                               : py::array(py::array_t<float, py::array::c_style | py::array::forcecast>(x));
+            py::array y = f64 ? py::array(py::dtype::of<double>(), {p.info().num_rows})
+                              : py::array(py::dtype::of<float>(), {p.info().num_rows});
+            const void* xp = xc.data();
+            void* yp = y.mutable_data();
+            const uint64_t n = uint64_t(xc.size());
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_dev_spmv_host(p.dev->handle(), xp, n, yp));
+            }
+            return y;
+        },
+        py::arg("matrix"), py::arg("x"));
+
+    m.def(
+        "chunk_entries",
+        [](const PyArgCsr& p, std::size_t g, std::size_t c) {
+            const std::size_t cap = p.info().max_chunk_size + 1;
+            std::vector<double> v(cap);
+            std::vector<float> vf(cap);
+            std::vector<int32_t> cl(cap);
+            uint64_t n = 0;
+            const bool f64 = p.info().dtype == ARGCSR_F64;
+            check(argcsr_dev_chunk_entries(p.dev->handle(), g, c, f64 ? static_cast<void*>(v.data()) : vf.data(),
+                                           cl.data(), cap, &n));
+            std::vector<std::pair<double, int32_t>> out;
+            for (uint64_t i = 0; i < n; ++i) out.emplace_back(f64 ? v[i] : double(vf[i]), cl[i]);
+            return out;
+        },
+        py::arg("matrix"), py::arg("group_index"), py::arg("chunk_index"));
+
+    m.def(
+        "padding_stats", [](const PyArgCsr& p) { return argcsr_b200::padding_stats(*p.dev); }, py::arg("matrix"));
+
+    m.def(
+        "partition_rows",
+        [](py::array_t<uint64_t, py::array::c_style | py::array::forcecast> rp, uint32_t parts) {
+            py::array_t<uint64_t> out(parts + 1);
+            check(argcsr_partition_rows(rp.data(), uint64_t(rp.size()) - 1, parts, out.mutable_data()));
+            return out;
+        },
+        py::arg("row_pointers"), py::arg("parts"));
+}

@@ -1,0 +1,378 @@
+// The C-ABI (include/argcsr_gpu.h).  Validation order and messages follow the
+// reference (proj/src/argcsr.cpp:20-26, 220-223, 235-242); every failure is a
+// status code plus a thread-local message, never an exception across the ABI.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "argcsr_gpu.h"
+#include "common.cuh"
+#include "convert.cuh"
+#include "inverse.cuh"
+#include "spmv.cuh"
+
+using argcsr_gpu::fail;
+using argcsr_gpu::Failure;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+argcsr_status guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return ARGCSR_OK;
+    } catch (const Failure& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return ARGCSR_E_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return ARGCSR_E_INTERNAL;
+    }
+}
+
+// Binds the handle's device for the duration of a call and restores the
+// caller's current device afterwards.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(ARGCSR_E_CUDA, "no CUDA device available (the ARG-CSR path has no CPU fallback)");
+        }
+        if (dev < 0 || dev >= n) fail(ARGCSR_E_PARAMETER, "device ordinal " + std::to_string(dev) + " out of range");
+        CUDA_OK(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_OK(cudaSetDevice(dev));
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void free_handle(argcsr_dev* m) {
+    if (!m) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    cudaFree(m->values);
+    cudaFree(m->columns);
+    cudaFree(m->groups);
+    cudaFree(m->tm);
+    cudaFree(m->assigned);
+    cudaFree(m->unit_base);
+    cudaFree(m->tiles);
+    cudaFree(m->heavy);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete m;
+}
+
+size_t elem_size(argcsr_dtype d) { return d == ARGCSR_F64 ? sizeof(double) : sizeof(float); }
+
+void check_handle(const argcsr_dev* m) {
+    if (!m) fail(ARGCSR_E_PARAMETER, "null ARG-CSR handle");
+}
+
+// Persisting-L2 carve-out for the x window (SpMV), set once per device.
+size_t ensure_l2_persist(int device) {
+    static std::mutex mu;
+    static std::vector<long long> done(64, -1);
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 64 && done[device] >= 0) return size_t(done[device]);
+    int persist_max = 0;
+    CUDA_OK(cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, device));
+    size_t granted = 0;
+    if (persist_max > 0) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(persist_max)) == cudaSuccess) {
+            CUDA_OK(cudaDeviceGetLimit(&granted, cudaLimitPersistingL2CacheSize));
+        } else {
+            cudaGetLastError();
+        }
+    }
+    if (device < 64) done[device] = (long long)granted;
+    return granted;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* argcsr_last_error(void) { return g_last_error.c_str(); }
+
+int argcsr_abi_version(void) { return ARGCSR_GPU_ABI_VERSION; }
+
+const char* argcsr_status_name(argcsr_status s) {
+    switch (s) {
+        case ARGCSR_OK: return "ok";
+        case ARGCSR_E_PARAMETER: return "ParameterError";
+        case ARGCSR_E_DIMENSION: return "DimensionError";
+        case ARGCSR_E_BOUNDS: return "BoundsError";
+        case ARGCSR_E_INTERNAL: return "InternalError";
+        case ARGCSR_E_CUDA: return "CudaError";
+        case ARGCSR_E_NCCL: return "NcclError";
+        case ARGCSR_E_OOM: return "OutOfMemory";
+        case ARGCSR_E_FORMAT: return "FormatError";
+        case ARGCSR_E_IO: return "IoError";
+        case ARGCSR_E_PARSE: return "ParseError";
+        case ARGCSR_E_UNSUPPORTED: return "UnsupportedError";
+    }
+    return "unknown";
+}
+
+argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t tpg, uint64_t dcs, int device,
+                                 void* stream, argcsr_dev** out) {
+    return guarded([&] {
+        if (!csr || !out) fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert: null argument");
+        *out = nullptr;
+        // argcsr.cpp:20-26 order: parameters, then an empty row set.
+        if (tpg == 0 || dcs == 0)
+            fail(ARGCSR_E_PARAMETER,
+                 "partition_groups: threads_per_group and desired_chunk_size must be at least 1");
+        if (csr->num_rows == 0) fail(ARGCSR_E_PARAMETER, "partition_groups: row_nnz must be nonempty");
+        if (tpg > argcsr_gpu::kMaxThreadsPerGroup)
+            fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: threads_per_group " + std::to_string(tpg) +
+                                           " exceeds the device limit " +
+                                           std::to_string(argcsr_gpu::kMaxThreadsPerGroup));
+        if (csr->num_rows >= 0xFFFFFFFFull)
+            fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: num_rows exceeds the device limit 2^32-2");
+        if (csr->dtype != ARGCSR_F64 && csr->dtype != ARGCSR_F32)
+            fail(ARGCSR_E_PARAMETER, "argcsr_from_csr: unknown dtype");
+        if (!csr->row_pointers || (csr->nnz && (!csr->columns || !csr->values)))
+            fail(ARGCSR_E_PARAMETER, "argcsr_from_csr: null CSR array");
+
+        DeviceScope scope(device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto* m = new argcsr_dev;
+        m->device = device;
+        m->dtype = csr->dtype;
+        m->num_rows = csr->num_rows;
+        m->num_cols = csr->num_cols;
+        m->tpg = tpg;
+        m->dcs = dcs;
+        m->tm16 = true;
+        try {
+            m->l2_persist_max = ensure_l2_persist(device);
+            const uint64_t N = csr->num_rows, nnz = csr->nnz;
+            const size_t es = elem_size(csr->dtype);
+            const uint64_t* rp = csr->row_pointers;
+            const int32_t* cols = csr->columns;
+            const void* vals = csr->values;
+            void* staged[3] = {nullptr, nullptr, nullptr};
+            struct Release {
+                void** p;
+                cudaStream_t s;
+                ~Release() {
+                    for (int i = 0; i < 3; ++i)
+                        if (p[i]) cudaFreeAsync(p[i], s);
+                }
+            } release{staged, s};
+            if (csr->space == ARGCSR_HOST) {
+                CUDA_OK(cudaMallocAsync(&staged[0], (N + 1) * sizeof(uint64_t), s));
+                CUDA_OK(cudaMallocAsync(&staged[1], std::max<uint64_t>(nnz, 1) * sizeof(int32_t), s));
+                CUDA_OK(cudaMallocAsync(&staged[2], std::max<uint64_t>(nnz, 1) * es, s));
+                CUDA_OK(cudaMemcpyAsync(staged[0], rp, (N + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+                if (nnz) {
+                    CUDA_OK(cudaMemcpyAsync(staged[1], cols, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+                    CUDA_OK(cudaMemcpyAsync(staged[2], vals, nnz * es, cudaMemcpyHostToDevice, s));
+                }
+                rp = static_cast<const uint64_t*>(staged[0]);
+                cols = static_cast<const int32_t*>(staged[1]);
+                vals = staged[2];
+            }
+            uint64_t ends[2] = {0, 0};
+            CUDA_OK(cudaMemcpyAsync(&ends[0], rp, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpyAsync(&ends[1], rp + N, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+            argcsr_gpu::convert_device_csr(m, rp, cols, vals, s);
+            m->nnz = ends[1] - ends[0];
+            CUDA_OK(cudaStreamSynchronize(s));
+        } catch (...) {
+            free_handle(m);
+            throw;
+        }
+        *out = m;
+    });
+}
+
+argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info) {
+    return guarded([&] {
+        check_handle(m);
+        if (!info) fail(ARGCSR_E_PARAMETER, "argcsr_dev_info: null output");
+        info->num_rows = m->num_rows;
+        info->num_cols = m->num_cols;
+        info->threads_per_group = m->tpg;
+        info->desired_chunk_size = m->dcs;
+        info->num_groups = m->num_groups;
+        info->total_slots = m->total_slots;
+        info->nnz = m->nnz;
+        info->heavy_groups = m->num_heavy;
+        info->light_tiles = m->num_tiles;
+        info->max_chunk_size = m->max_chunk;
+        info->device_bytes = m->device_bytes;
+        info->device = m->device;
+        info->dtype = m->dtype;
+    });
+}
+
+argcsr_status argcsr_dev_export(const argcsr_dev* m, uint64_t* groups4, uint64_t* threads_mapping, void* values,
+                                int32_t* columns) {
+    return guarded([&] {
+        check_handle(m);
+        DeviceScope scope(m->device);
+        argcsr_gpu::export_arrays(m, groups4, threads_mapping, values, columns, cudaStreamPerThread);
+    });
+}
+
+argcsr_status argcsr_dev_spmv(const argcsr_dev* m, const void* x, void* y, void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv: null vector");
+        DeviceScope scope(m->device);
+        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, static_cast<cudaStream_t>(stream));
+    });
+}
+
+argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_t group_begin, uint64_t group_end,
+                                     void* y, void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_groups: null vector");
+        DeviceScope scope(m->device);
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream));
+    });
+}
+
+argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x, uint64_t x_len, void* y) {
+    return guarded([&] {
+        check_handle(m);
+        // argcsr.cpp:220-223
+        if (x_len != m->num_cols)
+            fail(ARGCSR_E_DIMENSION, "spmv_argcsr: vector length " + std::to_string(x_len) + " does not match " +
+                                         std::to_string(m->num_cols) + " columns");
+        if ((!x && x_len) || (!y && m->num_rows)) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_host: null vector");
+        DeviceScope scope(m->device);
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t es = elem_size(m->dtype);
+        void *dx = nullptr, *dy = nullptr;
+        CUDA_OK(cudaMallocAsync(&dx, std::max<uint64_t>(m->num_cols, 1) * es, s));
+        struct Free {
+            void** a;
+            void** b;
+            cudaStream_t s;
+            ~Free() {
+                if (*a) cudaFreeAsync(*a, s);
+                if (*b) cudaFreeAsync(*b, s);
+                cudaStreamSynchronize(s);
+            }
+        } fr{&dx, &dy, s};
+        CUDA_OK(cudaMallocAsync(&dy, m->num_rows * es, s));
+        if (x_len) CUDA_OK(cudaMemcpyAsync(dx, x, x_len * es, cudaMemcpyHostToDevice, s));
+        argcsr_gpu::spmv_launch(m, dx, dy, 0, m->num_groups, s);
+        CUDA_OK(cudaMemcpyAsync(y, dy, m->num_rows * es, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    });
+}
+
+argcsr_status argcsr_dev_spmv_host_staged(const argcsr_dev* m, const void* x_host, void* x_dev, void* y_dev,
+                                          void* y_host, void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if (!x_host || !x_dev || !y_dev || !y_host) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_host_staged: null buffer");
+        DeviceScope scope(m->device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t es = elem_size(m->dtype);
+        CUDA_OK(cudaMemcpyAsync(x_dev, x_host, m->num_cols * es, cudaMemcpyHostToDevice, s));
+        argcsr_gpu::spmv_launch(m, x_dev, y_dev, 0, m->num_groups, s);
+        CUDA_OK(cudaMemcpyAsync(y_host, y_dev, m->num_rows * es, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    });
+}
+
+argcsr_status argcsr_dev_to_csr(const argcsr_dev* m, uint64_t* row_pointers, int32_t* columns, void* values) {
+    return guarded([&] {
+        check_handle(m);
+        if (!row_pointers || (m->nnz && (!columns || !values))) fail(ARGCSR_E_PARAMETER, "argcsr_dev_to_csr: null output");
+        DeviceScope scope(m->device);
+        argcsr_gpu::to_csr(m, row_pointers, columns, values, cudaStreamPerThread);
+    });
+}
+
+argcsr_status argcsr_dev_chunk_entries(const argcsr_dev* m, uint64_t group_index, uint64_t chunk_index, void* values,
+                                       int32_t* columns, uint64_t cap, uint64_t* n) {
+    return guarded([&] {
+        check_handle(m);
+        // argcsr.cpp:231-238
+        if (group_index >= m->num_groups)
+            fail(ARGCSR_E_BOUNDS, "chunk_entries: group " + std::to_string(group_index) + " out of range");
+        if (chunk_index >= m->tpg)
+            fail(ARGCSR_E_BOUNDS, "chunk_entries: chunk " + std::to_string(chunk_index) + " out of range");
+        if (!n) fail(ARGCSR_E_PARAMETER, "argcsr_dev_chunk_entries: null count");
+        DeviceScope scope(m->device);
+        cudaStream_t s = cudaStreamPerThread;
+        argcsr_gpu::GroupDesc d;
+        CUDA_OK(cudaMemcpyAsync(&d, m->groups + group_index, sizeof d, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        const size_t es = elem_size(m->dtype);
+        std::vector<int32_t> c(d.chunk);
+        std::vector<unsigned char> v(size_t(d.chunk) * es);
+        if (d.chunk) {
+            const uint64_t slot = d.offset + chunk_index;
+            CUDA_OK(cudaMemcpy2DAsync(c.data(), sizeof(int32_t), m->columns + slot, m->tpg * sizeof(int32_t),
+                                      sizeof(int32_t), d.chunk, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpy2DAsync(v.data(), es, static_cast<const unsigned char*>(m->values) + slot * es,
+                                      m->tpg * es, es, d.chunk, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaStreamSynchronize(s));
+        }
+        uint64_t k = 0;
+        while (k < d.chunk && c[k] != -1) ++k;
+        *n = k;
+        if (k > cap) fail(ARGCSR_E_BOUNDS, "chunk_entries: output capacity too small");
+        if (k) {
+            if (!columns || !values) fail(ARGCSR_E_PARAMETER, "argcsr_dev_chunk_entries: null output");
+            std::memcpy(columns, c.data(), k * sizeof(int32_t));
+            std::memcpy(values, v.data(), k * es);
+        }
+    });
+}
+
+argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_format_stats* out) {
+    return guarded([&] {
+        check_handle(m);
+        if (!out) fail(ARGCSR_E_PARAMETER, "argcsr_dev_padding_stats: null output");
+        DeviceScope scope(m->device);
+        argcsr_gpu::padding_stats(m, out, cudaStreamPerThread);
+    });
+}
+
+void argcsr_dev_free(argcsr_dev* m) { free_handle(m); }
+
+argcsr_status argcsr_partition_rows(const uint64_t* row_pointers, uint64_t num_rows, uint32_t parts,
+                                    uint64_t* row_begin) {
+    return guarded([&] {
+        if (parts == 0) fail(ARGCSR_E_PARAMETER, "partition_rows: parts must be at least 1");
+        if (!row_pointers || !row_begin) fail(ARGCSR_E_PARAMETER, "partition_rows: null argument");
+        const uint64_t nnz = row_pointers[num_rows] - row_pointers[0];
+        row_begin[0] = 0;
+        for (uint32_t p = 1; p < parts; ++p) {
+            const unsigned __int128 target128 = (unsigned __int128)nnz * p / parts;
+            const uint64_t target = row_pointers[0] + uint64_t(target128);
+            uint64_t r = uint64_t(std::lower_bound(row_pointers, row_pointers + num_rows + 1, target) - row_pointers);
+            // keep parts non-empty and ordered when rows allow it
+            const uint64_t lo = row_begin[p - 1] + (num_rows >= parts ? 1 : 0);
+            const uint64_t hi = num_rows >= parts ? num_rows - (parts - p) : num_rows;
+            r = std::min(std::max(r, lo), hi);
+            row_begin[p] = r;
+        }
+        row_begin[parts] = num_rows;
+    });
+}
+
+}  // extern "C"

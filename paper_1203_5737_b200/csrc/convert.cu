@@ -1,0 +1,593 @@
+// CSR -> ARG-CSR conversion on the GPU, bit-exact with the reference
+// argcsr_from_csr (proj/src/argcsr.cpp:123-155).  The two sequential greedies
+// of the reference are restated data-parallel:
+//
+//   K1 k1_next          budget boundary next(r) per row        (argcsr.cpp:30-45 admission test)
+//   K2 k2_*             group starts = orbit of row 0 under next, resolved with
+//                       exact per-tile transfer tables           (argcsr.cpp:17-46)
+//   K3 k3_assign        threads per row by threshold search on event keys,
+//                       inclusive scan into threads_mapping      (argcsr.cpp:48-89, 141-145)
+//   K4 exclusive scans  slot offsets, SpMV work units            (argcsr.cpp:151-152)
+//   K5 k5_layout        per-slot gather into the columnwise block (argcsr.cpp:91-121)
+//
+// plus the SpMV schedule (light tiles, heavy groups in LPT order).
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "convert.cuh"
+#include "scan.cuh"
+
+namespace argcsr_gpu {
+
+namespace {
+
+constexpr uint32_t kTileRows = 8192;       // K2 tile length (rows)
+constexpr uint32_t kMaxTiledTpg = 1024;    // K2 tile path bound (one thread per entry)
+constexpr uint16_t kEnd = 0xFFFF;          // K2: chain reached num_rows
+constexpr uint32_t kResolveBatch = 12000;  // K2 resolve: table entries per smem batch (< 48 KB)
+
+__device__ __forceinline__ uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+// chunk_filling, argcsr.cpp:11-13
+__device__ __forceinline__ uint64_t filling(uint64_t n, uint64_t t) { return n == 0 ? 0 : cdiv(n, t); }
+
+// ------------------------------------------------------------------- K1
+// next(r) = max(r+1, max{e <= min(r+tpg, N) : P[e]-P[r] <= budget}).  A group
+// opened at r admits row e-1 iff (e-r <= tpg) and (P[e]-P[r] <= budget), the
+// reference's `count + 1 > tpg || elements + cnt > budget` test; P is
+// monotone, so the admissible ends form a prefix and a binary search finds it.
+__global__ void k1_next(const uint64_t* __restrict__ rp, uint64_t N, uint64_t tpg, uint64_t budget,
+                        uint32_t* __restrict__ next) {
+    for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < N;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t base = rp[r];
+        uint64_t e;
+        if (rp[r + 1] - base > budget) {
+            e = r + 1;  // oversized row: singleton group (argcsr.hpp:75-76)
+        } else {
+            uint64_t lo = r + 1, hi = (tpg >= N - r) ? N : r + tpg;
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo + 1) / 2;
+                if (rp[mid] - base <= budget) lo = mid; else hi = mid - 1;
+            }
+            e = lo;
+        }
+        next[r] = uint32_t(e);
+    }
+}
+
+// ------------------------------------------------------------------- K2
+// Any chain entering tile [T, T+L) first lands in [T, T+tpg) (a jump is at
+// most tpg rows), so each tile is summarised by a table over its <= tpg entry
+// offsets: exit offset into the next tile and number of group starts.
+__global__ void __launch_bounds__(1024) k2_tile_tables(const uint32_t* __restrict__ next, uint32_t N, uint32_t E,
+                                                       uint16_t* __restrict__ exit_tab,
+                                                       uint16_t* __restrict__ cnt_tab) {
+    __shared__ uint32_t s_next[kTileRows];
+    const uint32_t T = blockIdx.x * kTileRows;
+    const uint32_t Lk = min(kTileRows, N - T);
+    for (uint32_t i = threadIdx.x; i < Lk; i += blockDim.x) s_next[i] = next[T + i];
+    __syncthreads();
+    const uint32_t tile_end = T + Lk;
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+        uint32_t s = T + e, c = 0;
+        uint16_t ex = kEnd;
+        if (s < N) {
+            while (s < tile_end) {
+                ++c;
+                s = s_next[s - T];
+            }
+            ex = s >= N ? kEnd : uint16_t(s - tile_end);
+        }
+        exit_tab[size_t(blockIdx.x) * E + e] = ex;
+        cnt_tab[size_t(blockIdx.x) * E + e] = uint16_t(c);
+    }
+}
+
+// One CTA composes the tile tables in order: entry/base group of every tile.
+__global__ void __launch_bounds__(1024) k2_resolve(const uint16_t* __restrict__ exit_tab,
+                                                   const uint16_t* __restrict__ cnt_tab, uint32_t ntiles,
+                                                   uint32_t E, uint32_t* __restrict__ tile_entry,
+                                                   uint32_t* __restrict__ tile_gbase,
+                                                   uint32_t* __restrict__ total_groups) {
+    extern __shared__ uint16_t s_tab[];  // [2][TB*E]
+    const uint32_t TB = max(1u, kResolveBatch / E);
+    uint16_t* s_exit = s_tab;
+    uint16_t* s_cnt = s_tab + size_t(TB) * E;
+    __shared__ uint32_t s_entry, s_gbase;
+    if (threadIdx.x == 0) s_entry = 0, s_gbase = 0;
+    for (uint32_t k0 = 0; k0 < ntiles; k0 += TB) {
+        const uint32_t nb = min(TB, ntiles - k0);
+        const size_t n = size_t(nb) * E;
+        __syncthreads();
+        for (size_t i = threadIdx.x; i < n; i += blockDim.x) {
+            s_exit[i] = exit_tab[size_t(k0) * E + i];
+            s_cnt[i] = cnt_tab[size_t(k0) * E + i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t entry = s_entry, gb = s_gbase;
+            for (uint32_t k = 0; k < nb; ++k) {
+                tile_entry[k0 + k] = entry;
+                tile_gbase[k0 + k] = gb;
+                if (entry == kEnd) continue;
+                gb += s_cnt[size_t(k) * E + entry];
+                entry = s_exit[size_t(k) * E + entry];
+            }
+            s_entry = entry;
+            s_gbase = gb;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *total_groups = s_gbase;
+}
+
+// Re-walk each tile's true chain and emit its group starts.
+__global__ void __launch_bounds__(256) k2_emit(const uint32_t* __restrict__ next, uint32_t N,
+                                               const uint32_t* __restrict__ tile_entry,
+                                               const uint32_t* __restrict__ tile_gbase,
+                                               uint32_t* __restrict__ first_row) {
+    __shared__ uint32_t s_next[kTileRows];
+    const uint32_t T = blockIdx.x * kTileRows;
+    const uint32_t Lk = min(kTileRows, N - T);
+    const uint32_t entry = tile_entry[blockIdx.x];
+    if (entry == kEnd) return;
+    for (uint32_t i = threadIdx.x; i < Lk; i += blockDim.x) s_next[i] = next[T + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = T + entry, g = tile_gbase[blockIdx.x];
+        const uint32_t tile_end = T + Lk;
+        while (s < tile_end) {
+            first_row[g++] = s;
+            s = s_next[s - T];
+        }
+    }
+}
+
+// threads_per_group > kMaxTiledTpg: few, large groups -> one sequential walk.
+__global__ void k2_sequential(const uint32_t* __restrict__ next, uint32_t N, uint32_t* __restrict__ first_row,
+                              uint32_t* __restrict__ total_groups) {
+    uint32_t s = 0, g = 0;
+    while (s < N) {
+        first_row[g++] = s;
+        s = next[s];
+    }
+    *total_groups = g;
+}
+
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+// ------------------------------------------------------------------- K3
+// Row r can take threads t = 1 .. T_max(n_r) where T_max is the first plateau
+// of ceil(n/t) (the strict-improvement test, argcsr.cpp:71).  Each grant
+// (r, t -> t+1) has key ceil(n_r/t), strictly decreasing per row, so the
+// greedy grants events in (key desc, row asc) order: all events with key > K*
+// for the smallest K* with A(K*) <= spare, then the remaining spare to the
+// rows owning a key == K* event, ascending.  T_max is capped at spare+1.
+__device__ __forceinline__ uint64_t plateau_capped(uint64_t n, uint64_t spare) {
+    uint64_t t = 1;
+    while (t <= spare && filling(n, t + 1) < filling(n, t)) ++t;
+    return t;
+}
+// a_r(K): events of row r with key > K (K = 0: all of them).
+__device__ __forceinline__ uint64_t events_above(uint64_t n, uint64_t tcap, uint64_t K) {
+    if (K == 0) return tcap - 1;
+    if (n <= K) return 0;
+    const uint64_t a = cdiv(n, K) - 1;
+    return a < tcap - 1 ? a : tcap - 1;
+}
+
+template <typename TM>
+__global__ void __launch_bounds__(256) k3_assign(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ first_row,
+                                                 uint32_t G, uint64_t tpg, uint32_t* __restrict__ tcap_buf,
+                                                 TM* __restrict__ tm, uint32_t* __restrict__ chunk_out,
+                                                 TM* __restrict__ assigned_out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < G; g += nwarps) {
+        const uint32_t f = first_row[g];
+        const uint32_t k = first_row[g + 1] - f;
+        const uint64_t spare = tpg - k;
+        uint64_t E = 0, maxn = 0;
+        for (uint32_t i = lane; i < k; i += 32) {
+            const uint64_t n = rp[f + i + 1] - rp[f + i];
+            const uint64_t tc = plateau_capped(n, spare);
+            tcap_buf[f + i] = uint32_t(tc);
+            E += tc - 1;
+            maxn = n > maxn ? n : maxn;
+        }
+        E = warp_sum_u64(E);
+        maxn = warp_max_u64(maxn);
+        uint64_t K = 0, left = 0;
+        if (E > spare) {
+            uint64_t lo = 1, hi = maxn;  // A(maxn) = 0 <= spare
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                uint64_t A = 0;
+                for (uint32_t i = lane; i < k; i += 32)
+                    A += events_above(rp[f + i + 1] - rp[f + i], tcap_buf[f + i], mid);
+                A = warp_sum_u64(A);
+                if (A <= spare) hi = mid; else lo = mid + 1;
+            }
+            K = lo;
+            uint64_t A = 0;
+            for (uint32_t i = lane; i < k; i += 32)
+                A += events_above(rp[f + i + 1] - rp[f + i], tcap_buf[f + i], K);
+            left = spare - warp_sum_u64(A);
+        }
+        uint64_t carry = 0, chunk = 0, ties_before = 0;
+        const unsigned lt_mask = (1u << lane) - 1u;
+        for (uint32_t base = 0; base < k; base += 32) {
+            const uint32_t i = base + lane;
+            const bool valid = i < k;
+            uint64_t n = 0, tc = 1, t = 0;
+            if (valid) {
+                n = rp[f + i + 1] - rp[f + i];
+                tc = tcap_buf[f + i];
+                t = 1 + events_above(n, tc, K);
+            }
+            if (K > 0) {
+                const bool tie = valid && events_above(n, tc, K - 1) > events_above(n, tc, K);
+                const unsigned bal = __ballot_sync(0xffffffffu, tie);
+                const uint64_t rank = ties_before + __popc(bal & lt_mask);
+                if (tie && rank < left) t += 1;
+                ties_before += __popc(bal);
+            }
+            const uint64_t incl = warp_incl_scan_u64(t, lane) + carry;
+            if (valid) {
+                tm[f + i] = TM(incl);  // inclusive per-group scan, argcsr.cpp:141-145
+                const uint64_t fl = filling(n, t);
+                chunk = fl > chunk ? fl : chunk;
+            }
+            carry = __shfl_sync(0xffffffffu, incl, 31);
+        }
+        chunk = warp_max_u64(chunk);
+        if (lane == 0) {
+            chunk_out[g] = uint32_t(chunk);
+            assigned_out[g] = TM(carry);
+        }
+    }
+}
+
+// ------------------------------------------------------------------- K4
+template <typename TM>
+__global__ void k4_fill_desc(const uint32_t* __restrict__ first_row, const uint32_t* __restrict__ chunk,
+                             const uint64_t* __restrict__ offset, uint32_t G, uint32_t N,
+                             GroupDesc* __restrict__ desc) {
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g <= G;
+         g += uint64_t(gridDim.x) * blockDim.x) {
+        GroupDesc d;
+        d.offset = offset[g];
+        d.first_row = g < G ? first_row[g] : N;
+        d.chunk = g < G ? chunk[g] : 0;
+        desc[g] = d;
+    }
+}
+
+struct SlotsOf {  // chunk_size * threads_per_group (argcsr.cpp:151-152)
+    const uint32_t* chunk;
+    uint64_t tpg;
+    __device__ uint64_t operator()(uint64_t g) const { return uint64_t(chunk[g]) * tpg; }
+};
+
+template <typename TM>
+struct UnitsOf {  // SpMV work units: ceil(assigned / V), heavy groups count 1
+    const uint32_t* chunk;
+    const TM* assigned;
+    uint32_t V;
+    __device__ uint64_t operator()(uint64_t g) const {
+        return chunk[g] > kHeavyChunk ? 1 : (uint64_t(assigned[g]) + V - 1) / V;
+    }
+};
+
+struct HeavyFlag {
+    const uint32_t* chunk;
+    __device__ uint64_t operator()(uint64_t g) const { return chunk[g] > kHeavyChunk ? 1 : 0; }
+};
+
+__global__ void k4_scatter_heavy(const uint32_t* __restrict__ chunk, const uint64_t* __restrict__ pos,
+                                 uint32_t G, uint32_t* __restrict__ ids, uint32_t* __restrict__ chunks) {
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G;
+         g += uint64_t(gridDim.x) * blockDim.x) {
+        if (chunk[g] > kHeavyChunk) {
+            ids[pos[g]] = uint32_t(g);
+            chunks[pos[g]] = chunk[g];
+        }
+    }
+}
+
+// Light tile k starts at the first group whose unit base is >= k * B.
+__global__ void k4_tiles(const uint64_t* __restrict__ unit_base, uint32_t G, uint32_t ntiles,
+                         uint32_t* __restrict__ tiles) {
+    for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k <= ntiles;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        if (k == ntiles) {
+            tiles[k] = G;
+            continue;
+        }
+        const uint64_t key = k * uint64_t(kTileThreads);
+        uint64_t lo = 0, hi = G;  // lower_bound over unit_base[0..G)
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (unit_base[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        tiles[k] = uint32_t(lo);
+    }
+}
+
+__global__ void k4_max_tile_groups(const uint32_t* __restrict__ tiles, uint32_t ntiles,
+                                   unsigned long long* __restrict__ out) {
+    uint64_t m = 0;
+    for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < ntiles;
+         k += uint64_t(gridDim.x) * blockDim.x)
+        m = max(m, uint64_t(tiles[k + 1] - tiles[k]));
+    m = warp_max_u64(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+}
+
+__global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, unsigned long long* __restrict__ out) {
+    uint64_t m = 0;
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G;
+         g += uint64_t(gridDim.x) * blockDim.x)
+        m = max(m, uint64_t(chunk[g]));
+    m = warp_max_u64(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+}
+
+// ------------------------------------------------------------------- K5
+// Gather form of layout_group: lane l of group g belongs to the row whose
+// threads_mapping range holds l; its chunk c holds the row's elements
+// [start, start+len) with the ceil/floor split, larger chunks first.  Slot
+// (j, l) = value j of that run, or (+0.0, -1) padding.  Writes are coalesced
+// along the lane dimension of each j-row.
+template <typename T, typename TM>
+__global__ void __launch_bounds__(256) k5_layout(const uint64_t* __restrict__ rp, const int32_t* __restrict__ cols_in,
+                                                 const T* __restrict__ vals_in, const GroupDesc* __restrict__ desc,
+                                                 const TM* __restrict__ tm, const TM* __restrict__ assigned,
+                                                 uint64_t tpg, uint32_t G, T* __restrict__ vals_out,
+                                                 int32_t* __restrict__ cols_out) {
+    constexpr uint32_t WL = 1024;
+    __shared__ uint64_t s_src[WL];
+    __shared__ uint32_t s_len[WL];
+    for (uint64_t g = blockIdx.x; g < G; g += gridDim.x) {
+        const GroupDesc d = desc[g];
+        const uint32_t f = d.first_row;
+        const uint32_t k = desc[g + 1].first_row - f;
+        const uint64_t chunk = d.chunk;
+        if (chunk == 0) continue;  // all-empty group: zero slots
+        const uint64_t asg = assigned[g];
+        for (uint64_t w0 = 0; w0 < tpg; w0 += WL) {
+            const uint32_t wl = uint32_t(min(uint64_t(WL), tpg - w0));
+            for (uint32_t l = threadIdx.x; l < wl; l += blockDim.x) {
+                const uint64_t lane = w0 + l;
+                uint64_t src = 0;
+                uint32_t len = 0;
+                if (lane < asg) {
+                    uint32_t lo = 0, hi = k - 1;  // first local row with tm > lane
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) / 2;
+                        if (uint64_t(tm[f + mid]) > lane) hi = mid; else lo = mid + 1;
+                    }
+                    const uint64_t b = lo ? uint64_t(tm[f + lo - 1]) : 0;
+                    const uint64_t t = uint64_t(tm[f + lo]) - b;
+                    const uint64_t c = lane - b;
+                    const uint64_t n = rp[f + lo + 1] - rp[f + lo];
+                    const uint64_t base = n / t, extra = n % t;
+                    const uint64_t start = c < extra ? c * (base + 1) : extra * (base + 1) + (c - extra) * base;
+                    len = uint32_t(base + (c < extra ? 1 : 0));
+                    src = rp[f + lo] + start;
+                }
+                s_src[l] = src;
+                s_len[l] = len;
+            }
+            __syncthreads();
+            uint64_t j = threadIdx.x / wl;
+            uint32_t l = threadIdx.x % wl;
+            const uint32_t step_j = blockDim.x / wl, step_l = blockDim.x % wl;
+            for (; j < chunk;) {
+                const uint64_t slot = d.offset + j * tpg + w0 + l;
+                if (j < s_len[l]) {
+                    const uint64_t src = s_src[l] + j;
+                    vals_out[slot] = vals_in[src];
+                    cols_out[slot] = cols_in[src];
+                } else {
+                    vals_out[slot] = T(0);
+                    cols_out[slot] = -1;
+                }
+                j += step_j;
+                l += step_l;
+                if (l >= wl) {
+                    l -= wl;
+                    ++j;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
+    const uint64_t b = (n + block - 1) / block;
+    return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, cap)));
+}
+
+template <typename P>
+struct DevPtr {  // stream-ordered scratch allocation
+    P* p = nullptr;
+    cudaStream_t s;
+    DevPtr(size_t n, cudaStream_t st) : s(st) { CUDA_OK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(P), s)); }
+    ~DevPtr() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    DevPtr(const DevPtr&) = delete;
+    DevPtr& operator=(const DevPtr&) = delete;
+};
+
+template <typename P>
+P* dev_alloc(argcsr_dev* m, size_t n) {
+    P* p = nullptr;
+    CUDA_OK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(P)));
+    m->device_bytes += std::max<size_t>(n, 1) * sizeof(P);
+    return p;
+}
+
+template <typename T, typename TM>
+void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const T* vals, cudaStream_t s) {
+    const uint64_t N = m->num_rows, tpg = m->tpg;
+    const uint64_t budget = m->dcs * tpg;  // size_t product, wraps like argcsr.cpp:28
+    const uint32_t N32 = uint32_t(N);
+
+    // K1
+    DevPtr<uint32_t> next(N, s);
+    k1_next<<<grid_for(N, 256), 256, 0, s>>>(rp, N, tpg, budget, next.p);
+    LAUNCH_OK("k1_next");
+
+    // K2
+    DevPtr<uint32_t> first_row(N + 1, s);
+    DevPtr<uint32_t> d_G(1, s);
+    if (tpg <= kMaxTiledTpg) {
+        const uint32_t ntiles = uint32_t((N + kTileRows - 1) / kTileRows);
+        const uint32_t E = uint32_t(tpg);
+        DevPtr<uint16_t> exit_tab(size_t(ntiles) * E, s), cnt_tab(size_t(ntiles) * E, s);
+        DevPtr<uint32_t> tile_entry(ntiles, s), tile_gbase(ntiles, s);
+        const unsigned thr = std::min<unsigned>(1024, (E + 31) / 32 * 32);
+        k2_tile_tables<<<ntiles, thr, 0, s>>>(next.p, N32, E, exit_tab.p, cnt_tab.p);
+        LAUNCH_OK("k2_tile_tables");
+        const uint32_t TB = std::max(1u, kResolveBatch / E);
+        const size_t smem = size_t(2) * TB * E * sizeof(uint16_t);
+        k2_resolve<<<1, 1024, smem, s>>>(exit_tab.p, cnt_tab.p, ntiles, E, tile_entry.p, tile_gbase.p, d_G.p);
+        LAUNCH_OK("k2_resolve");
+        k2_emit<<<ntiles, 256, 0, s>>>(next.p, N32, tile_entry.p, tile_gbase.p, first_row.p);
+        LAUNCH_OK("k2_emit");
+    } else {
+        k2_sequential<<<1, 1, 0, s>>>(next.p, N32, first_row.p, d_G.p);
+        LAUNCH_OK("k2_sequential");
+    }
+    uint32_t G = 0;
+    CUDA_OK(cudaMemcpyAsync(&G, d_G.p, sizeof G, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    m->num_groups = G;
+    k_set_u32<<<1, 1, 0, s>>>(first_row.p + G, N32);
+    LAUNCH_OK("k_set_u32");
+
+    // K3
+    TM* tm = dev_alloc<TM>(m, N);
+    TM* assigned = dev_alloc<TM>(m, G);
+    m->tm = tm;
+    m->assigned = assigned;
+    DevPtr<uint32_t> chunk(G, s), tcap(N, s);
+    {
+        const uint64_t threads = uint64_t(G) * 32;
+        k3_assign<TM><<<grid_for(threads, 256, 148u * 256u), 256, 0, s>>>(rp, first_row.p, G, tpg, tcap.p, tm,
+                                                                          chunk.p, assigned);
+        LAUNCH_OK("k3_assign");
+    }
+
+    // K4: offsets (+ total slots), descriptors
+    DevPtr<uint64_t> offset(uint64_t(G) + 1, s);
+    exclusive_scan(SlotsOf{chunk.p, tpg}, G, offset.p, s);
+    uint64_t total_slots = 0;
+    CUDA_OK(cudaMemcpyAsync(&total_slots, offset.p + G, sizeof total_slots, cudaMemcpyDeviceToHost, s));
+    m->groups = dev_alloc<GroupDesc>(m, uint64_t(G) + 1);
+    k4_fill_desc<TM><<<grid_for(uint64_t(G) + 1, 256), 256, 0, s>>>(first_row.p, chunk.p, offset.p, G, N32, m->groups);
+    LAUNCH_OK("k4_fill_desc");
+    {
+        DevPtr<unsigned long long> mx(1, s);
+        CUDA_OK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), s));
+        k4_max_chunk<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, G, mx.p);
+        LAUNCH_OK("k4_max_chunk");
+        unsigned long long mc = 0;
+        CUDA_OK(cudaMemcpyAsync(&mc, mx.p, sizeof mc, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        m->max_chunk = mc;
+    }
+    m->total_slots = total_slots;
+
+    // SpMV schedule: work units (V lanes), light tiles, heavy groups (LPT order).
+    const uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
+    m->lanes_per_unit = int(V);
+    m->unit_base = dev_alloc<uint64_t>(m, uint64_t(G) + 1);
+    exclusive_scan(UnitsOf<TM>{chunk.p, assigned, V}, G, m->unit_base, s);
+    uint64_t total_units = 0;
+    CUDA_OK(cudaMemcpyAsync(&total_units, m->unit_base + G, sizeof total_units, cudaMemcpyDeviceToHost, s));
+    {
+        DevPtr<uint64_t> hpos(uint64_t(G) + 1, s);
+        exclusive_scan(HeavyFlag{chunk.p}, G, hpos.p, s);
+        uint64_t nh = 0;
+        CUDA_OK(cudaMemcpyAsync(&nh, hpos.p + G, sizeof nh, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        m->num_heavy = uint32_t(nh);
+        m->heavy = dev_alloc<uint32_t>(m, nh);
+        if (nh) {
+            DevPtr<uint32_t> ids(nh, s), chs(nh, s);
+            k4_scatter_heavy<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, hpos.p, G, ids.p, chs.p);
+            LAUNCH_OK("k4_scatter_heavy");
+            std::vector<uint32_t> hid(nh), hch(nh);
+            CUDA_OK(cudaMemcpyAsync(hid.data(), ids.p, nh * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpyAsync(hch.data(), chs.p, nh * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaStreamSynchronize(s));
+            std::vector<uint32_t> order(nh);
+            std::iota(order.begin(), order.end(), 0u);
+            std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hch[a] > hch[b]; });
+            std::vector<uint32_t> sorted(nh);
+            for (uint64_t i = 0; i < nh; ++i) sorted[i] = hid[order[i]];
+            CUDA_OK(cudaMemcpyAsync(m->heavy, sorted.data(), nh * 4, cudaMemcpyHostToDevice, s));
+            CUDA_OK(cudaStreamSynchronize(s));
+        }
+    }
+    const uint64_t ntiles = (total_units + kTileThreads - 1) / kTileThreads;
+    if (ntiles > 0x7fffffffull) fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: matrix too large for the tile schedule");
+    m->num_tiles = uint32_t(ntiles);
+    m->tiles = dev_alloc<uint32_t>(m, ntiles + 1);
+    k4_tiles<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(m->unit_base, G, uint32_t(ntiles), m->tiles);
+    LAUNCH_OK("k4_tiles");
+    {
+        DevPtr<unsigned long long> mx(1, s);
+        CUDA_OK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), s));
+        if (ntiles) {
+            k4_max_tile_groups<<<grid_for(ntiles, 256), 256, 0, s>>>(m->tiles, uint32_t(ntiles), mx.p);
+            LAUNCH_OK("k4_max_tile_groups");
+        }
+        unsigned long long mg = 0;
+        CUDA_OK(cudaMemcpyAsync(&mg, mx.p, sizeof mg, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        m->max_tile_groups = uint32_t(mg);
+        m->max_tile_units = kTileThreads + (tpg + V - 1) / V;
+    }
+
+    // K5
+    m->values = dev_alloc<T>(m, total_slots);
+    m->columns = dev_alloc<int32_t>(m, total_slots);
+    if (G > 0 && total_slots > 0) {
+        const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
+        k5_layout<T, TM><<<grid, 256, 0, s>>>(rp, cols, vals, m->groups, tm, assigned, tpg, G,
+                                             static_cast<T*>(m->values), m->columns);
+        LAUNCH_OK("k5_layout");
+    }
+    CUDA_OK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(1024) scan_partials_kernel(uint64_t* partial, uint64_t nb, uint64_t* total) {
+    uint64_t carry = 0;
+    for (uint64_t base = 0; base < nb; base += blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        const uint64_t v = i < nb ? partial[i] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan_u64(v, &tot);
+        if (i < nb) partial[i] = ex + carry;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// threads_mapping and per-group assigned counts are u16 on the device
+// (threads_per_group <= kMaxThreadsPerGroup < 65536); export widens to u64.
+void convert_device_csr(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const void* vals, cudaStream_t s) {
+    if (m->dtype == ARGCSR_F64) convert_typed<double, uint16_t>(m, rp, cols, static_cast<const double*>(vals), s);
+    else convert_typed<float, uint16_t>(m, rp, cols, static_cast<const float*>(vals), s);
+}
+
+}  // namespace argcsr_gpu

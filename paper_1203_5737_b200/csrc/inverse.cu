@@ -1,0 +1,217 @@
+// Device-side accessors of the ARG-CSR handle:
+//   export_arrays  the reference layout, widened (argcsr.hpp:23-30, 52-63)
+//   to_csr         csr_from_argcsr (argcsr.cpp:157-183), lossless inverse
+//   padding_stats  padding_stats(const ArgCsrMatrix&) (analysis.cpp:167-184)
+#include <vector>
+
+#include "common.cuh"
+#include "inverse.cuh"
+#include "scan.cuh"
+
+namespace argcsr_gpu {
+
+namespace {
+
+unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
+    const uint64_t b = (n + block - 1) / block;
+    return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, cap)));
+}
+
+__global__ void k_export_groups(const GroupDesc* __restrict__ desc, uint64_t G, uint64_t* __restrict__ out4) {
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G;
+         g += uint64_t(gridDim.x) * blockDim.x) {
+        const GroupDesc d = desc[g];
+        out4[4 * g + 0] = d.first_row;
+        out4[4 * g + 1] = desc[g + 1].first_row - d.first_row;
+        out4[4 * g + 2] = d.offset;
+        out4[4 * g + 3] = d.chunk;
+    }
+}
+
+template <typename TM>
+__global__ void k_widen(const TM* __restrict__ in, uint64_t n, uint64_t* __restrict__ out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = in[i];
+}
+
+// Leading non-sentinel entries of lane `lane` of a group block.
+__device__ __forceinline__ uint64_t lane_len(const int32_t* cols, uint64_t off, uint64_t tpg, uint32_t chunk,
+                                             uint64_t lane) {
+    uint64_t n = 0;
+    for (uint32_t j = 0; j < chunk; ++j) {
+        if (cols[off + uint64_t(j) * tpg + lane] == -1) break;
+        ++n;
+    }
+    return n;
+}
+
+// Warp per group, lanes over its rows: per-row stored-element counts.
+template <typename TM>
+__global__ void k_row_counts(const GroupDesc* __restrict__ desc, const TM* __restrict__ tm,
+                             const int32_t* __restrict__ cols, uint64_t tpg, uint64_t G, uint64_t* __restrict__ cnt) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < G; g += nw) {
+        const GroupDesc d = desc[g];
+        const uint32_t f = d.first_row, k = desc[g + 1].first_row - f;
+        for (uint32_t r = lane; r < k; r += 32) {
+            const uint64_t b = r ? uint64_t(tm[f + r - 1]) : 0, e = tm[f + r];
+            uint64_t n = 0;
+            for (uint64_t c = b; c < e; ++c) n += lane_len(cols, d.offset, tpg, d.chunk, c);
+            cnt[f + r] = n;
+        }
+    }
+}
+
+template <typename T, typename TM>
+__global__ void k_fill_csr(const GroupDesc* __restrict__ desc, const TM* __restrict__ tm,
+                           const int32_t* __restrict__ cols, const T* __restrict__ vals, uint64_t tpg, uint64_t G,
+                           const uint64_t* __restrict__ rp, int32_t* __restrict__ out_cols, T* __restrict__ out_vals) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < G; g += nw) {
+        const GroupDesc d = desc[g];
+        const uint32_t f = d.first_row, k = desc[g + 1].first_row - f;
+        for (uint32_t r = lane; r < k; r += 32) {
+            const uint64_t b = r ? uint64_t(tm[f + r - 1]) : 0, e = tm[f + r];
+            uint64_t o = rp[f + r];
+            for (uint64_t c = b; c < e; ++c)
+                for (uint32_t j = 0; j < d.chunk; ++j) {
+                    const uint64_t slot = d.offset + uint64_t(j) * tpg + c;
+                    const int32_t col = cols[slot];
+                    if (col == -1) break;
+                    out_cols[o] = col;
+                    out_vals[o] = vals[slot];
+                    ++o;
+                }
+        }
+    }
+}
+
+__global__ void k_count_explicit(const int32_t* __restrict__ cols, uint64_t n, unsigned long long* __restrict__ out) {
+    uint64_t c = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        c += cols[i] != -1;
+    c = warp_sum_u64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+template <typename TM>
+__global__ void k_assigned_slots(const GroupDesc* __restrict__ desc, const TM* __restrict__ assigned, uint64_t G,
+                                 unsigned long long* __restrict__ out) {
+    uint64_t c = 0;
+    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G; g += uint64_t(gridDim.x) * blockDim.x)
+        c += uint64_t(assigned[g]) * desc[g].chunk;
+    c = warp_sum_u64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+struct FromArray {
+    const uint64_t* a;
+    __device__ uint64_t operator()(uint64_t i) const { return a[i]; }
+};
+
+template <typename P>
+struct Scratch {
+    P* p = nullptr;
+    cudaStream_t s;
+    Scratch(size_t n, cudaStream_t st) : s(st) { CUDA_OK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(P), s)); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+size_t elem_size(const argcsr_dev* m) { return m->dtype == ARGCSR_F64 ? sizeof(double) : sizeof(float); }
+
+}  // namespace
+
+void export_arrays(const argcsr_dev* m, uint64_t* groups4, uint64_t* tm, void* values, int32_t* columns,
+                   cudaStream_t s) {
+    const uint64_t G = m->num_groups, N = m->num_rows, S = m->total_slots;
+    if (groups4 && G) {
+        Scratch<uint64_t> tmp(4 * G, s);
+        k_export_groups<<<grid_for(G, 256), 256, 0, s>>>(m->groups, G, tmp.p);
+        LAUNCH_OK("k_export_groups");
+        CUDA_OK(cudaMemcpyAsync(groups4, tmp.p, 4 * G * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    }
+    if (tm && N) {
+        Scratch<uint64_t> tmp(N, s);
+        k_widen<uint16_t><<<grid_for(N, 256), 256, 0, s>>>(static_cast<const uint16_t*>(m->tm), N, tmp.p);
+        LAUNCH_OK("k_widen");
+        CUDA_OK(cudaMemcpyAsync(tm, tmp.p, N * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    }
+    if (values && S) CUDA_OK(cudaMemcpyAsync(values, m->values, S * elem_size(m), cudaMemcpyDeviceToHost, s));
+    if (columns && S) CUDA_OK(cudaMemcpyAsync(columns, m->columns, S * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+}
+
+void to_csr(const argcsr_dev* m, uint64_t* row_pointers, int32_t* columns, void* values, cudaStream_t s) {
+    const uint64_t G = m->num_groups, N = m->num_rows;
+    const auto* tm = static_cast<const uint16_t*>(m->tm);
+    Scratch<uint64_t> cnt(N, s), rp(N + 1, s);
+    k_row_counts<uint16_t><<<grid_for(G * 32, 256), 256, 0, s>>>(m->groups, tm, m->columns, m->tpg, G, cnt.p);
+    LAUNCH_OK("k_row_counts");
+    exclusive_scan(FromArray{cnt.p}, N, rp.p, s);
+    uint64_t nnz = 0;
+    CUDA_OK(cudaMemcpyAsync(&nnz, rp.p + N, sizeof nnz, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    Scratch<int32_t> oc(nnz, s);
+    Scratch<unsigned char> ov(nnz * elem_size(m), s);
+    if (m->dtype == ARGCSR_F64)
+        k_fill_csr<double, uint16_t><<<grid_for(G * 32, 256), 256, 0, s>>>(
+            m->groups, tm, m->columns, static_cast<const double*>(m->values), m->tpg, G, rp.p, oc.p,
+            reinterpret_cast<double*>(ov.p));
+    else
+        k_fill_csr<float, uint16_t><<<grid_for(G * 32, 256), 256, 0, s>>>(
+            m->groups, tm, m->columns, static_cast<const float*>(m->values), m->tpg, G, rp.p, oc.p,
+            reinterpret_cast<float*>(ov.p));
+    LAUNCH_OK("k_fill_csr");
+    CUDA_OK(cudaMemcpyAsync(row_pointers, rp.p, (N + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    if (nnz) {
+        CUDA_OK(cudaMemcpyAsync(columns, oc.p, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(values, ov.p, nnz * elem_size(m), cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_OK(cudaStreamSynchronize(s));
+}
+
+uint64_t to_csr_nnz(const argcsr_dev* m, cudaStream_t s) {
+    const uint64_t G = m->num_groups, N = m->num_rows;
+    Scratch<uint64_t> cnt(N, s), rp(N + 1, s);
+    k_row_counts<uint16_t><<<grid_for(G * 32, 256), 256, 0, s>>>(m->groups, static_cast<const uint16_t*>(m->tm),
+                                                                 m->columns, m->tpg, G, cnt.p);
+    LAUNCH_OK("k_row_counts");
+    exclusive_scan(FromArray{cnt.p}, N, rp.p, s);
+    uint64_t nnz = 0;
+    CUDA_OK(cudaMemcpyAsync(&nnz, rp.p + N, sizeof nnz, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    return nnz;
+}
+
+void padding_stats(const argcsr_dev* m, argcsr_format_stats* out, cudaStream_t s) {
+    Scratch<unsigned long long> acc(2, s);
+    CUDA_OK(cudaMemsetAsync(acc.p, 0, 2 * sizeof(unsigned long long), s));
+    if (m->total_slots) {
+        k_count_explicit<<<grid_for(m->total_slots, 256), 256, 0, s>>>(m->columns, m->total_slots, acc.p);
+        LAUNCH_OK("k_count_explicit");
+    }
+    if (m->num_groups) {
+        k_assigned_slots<uint16_t><<<grid_for(m->num_groups, 256), 256, 0, s>>>(
+            m->groups, static_cast<const uint16_t*>(m->assigned), m->num_groups, acc.p + 1);
+        LAUNCH_OK("k_assigned_slots");
+    }
+    unsigned long long h[2] = {0, 0};
+    CUDA_OK(cudaMemcpyAsync(h, acc.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    out->explicit_nnz = h[0];
+    out->total_allocated_slots = m->total_slots;
+    out->assigned_padded_slots = h[1] - h[0];
+    // ratio_of (analysis.cpp:14-19)
+    if (h[0] > 0) out->padding_ratio = double(m->total_slots) / double(h[0]);
+    else out->padding_ratio = m->total_slots == 0 ? 1.0 : __builtin_inf();
+    // kElementBytes = 8, kIndexBytes = 4 (analysis.cpp:11-12, 180-182)
+    out->estimated_bytes = m->total_slots * (8 + 4) + m->num_groups * 4 * 4 + m->num_rows * 4;
+}
+
+}  // namespace argcsr_gpu

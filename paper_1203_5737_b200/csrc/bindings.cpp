@@ -61,6 +61,12 @@ py::array_t<T> view_of(const std::vector<T>& v, py::handle base) {
     return py::array_t<T>({v.size()}, {sizeof(T)}, v.data(), base);
 }
 
+// A fresh, writeable 1-D float64 or float32 array of n elements.
+py::array new_array(bool f64, std::size_t n) {
+    if (f64) return py::array_t<double>(py::ssize_t(n));
+    return py::array_t<float>(py::ssize_t(n));
+}
+
 template <typename T>
 std::vector<T> vec_from(const py::array_t<T, py::array::c_style | py::array::forcecast>& a) {
     return std::vector<T>(a.data(), a.data() + a.size());
@@ -85,8 +91,7 @@ struct PyArgCsr {
     void need_slots() const {
         if (columns) return;
         const std::size_t S = info().total_slots;
-        py::array v = info().dtype == ARGCSR_F64 ? py::array(py::dtype::of<double>(), {S})
-                                                 : py::array(py::dtype::of<float>(), {S});
+        py::array v = new_array(info().dtype == ARGCSR_F64, S);
         std::vector<int32_t> c(S);
         check(argcsr_dev_export(dev->handle(), nullptr, nullptr, v.mutable_data(), c.data()));
         values = v;
@@ -387,8 +392,7 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
             const std::size_t N = p.info().num_rows, nnz = p.info().nnz;
             py::array_t<uint64_t> rp(N + 1);
             py::array_t<int32_t> cols(nnz);
-            py::array vals = p.info().dtype == ARGCSR_F64 ? py::array(py::dtype::of<double>(), {nnz})
-                                                          : py::array(py::dtype::of<float>(), {nnz});
+            py::array vals = new_array(p.info().dtype == ARGCSR_F64, nnz);
             check(argcsr_dev_to_csr(p.dev->handle(), rp.mutable_data(), cols.mutable_data(), vals.mutable_data()));
             return py::make_tuple(rp, cols, vals);
         },
@@ -400,8 +404,7 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
             const bool f64 = p.info().dtype == ARGCSR_F64;
             py::array xc = f64 ? py::array(py::array_t<double, py::array::c_style | py::array::forcecast>(x))
                                : py::array(py::array_t<float, py::array::c_style | py::array::forcecast>(x));
-            py::array y = f64 ? py::array(py::dtype::of<double>(), {p.info().num_rows})
-                              : py::array(py::dtype::of<float>(), {p.info().num_rows});
+            py::array y = new_array(f64, p.info().num_rows);
             const void* xp = xc.data();
             void* yp = y.mutable_data();
             const uint64_t n = uint64_t(xc.size());

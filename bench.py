@@ -365,7 +365,8 @@ def run_b200(args):
 
     peak, peak_src = measured_peak()
     info = {"groups": m.num_groups, "total_slots": m.total_slots, "heavy_groups": m.heavy_groups,
-            "light_tiles": m.light_tiles, "max_chunk": m.max_chunk_size, "device_bytes": m.device_bytes}
+            "light_tiles": m.light_tiles, "max_chunk": m.max_chunk_size, "device_bytes": m.device_bytes,
+            "heavy_ctas": m.heavy_ctas, "l2_persist_bytes": m.l2_persist_bytes}
     key = f"{args.config}_tpg{args.tpg}_dcs{args.dcs}"
     traffic = traffic_from_profiles(key)
     out = {

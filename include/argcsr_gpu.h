@@ -89,9 +89,11 @@ typedef struct {
     uint64_t total_slots;      /* ArgCsrMatrix::total_slots() (argcsr.hpp:61) */
     uint64_t nnz;              /* explicit entries */
     uint64_t heavy_groups;     /* groups scheduled on the long-chunk path */
+    uint64_t heavy_ctas;       /* CTAs the heavy groups are packed into */
     uint64_t light_tiles;      /* CTA tiles of the short-chunk path */
     uint64_t max_chunk_size;
     uint64_t device_bytes;     /* device memory held by the handle */
+    uint64_t l2_persist_bytes; /* persisting-L2 carve-out available to the x window */
     int32_t device;
     argcsr_dtype dtype;
 } argcsr_dev_info_t;

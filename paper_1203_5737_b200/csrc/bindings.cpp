@@ -231,9 +231,11 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         .def_property_readonly("num_groups", [](const PyArgCsr& p) { return p.info().num_groups; })
         .def_property_readonly("nnz", [](const PyArgCsr& p) { return p.info().nnz; })
         .def_property_readonly("heavy_groups", [](const PyArgCsr& p) { return p.info().heavy_groups; })
+        .def_property_readonly("heavy_ctas", [](const PyArgCsr& p) { return p.info().heavy_ctas; })
         .def_property_readonly("light_tiles", [](const PyArgCsr& p) { return p.info().light_tiles; })
         .def_property_readonly("max_chunk_size", [](const PyArgCsr& p) { return p.info().max_chunk_size; })
         .def_property_readonly("device_bytes", [](const PyArgCsr& p) { return p.info().device_bytes; })
+        .def_property_readonly("l2_persist_bytes", [](const PyArgCsr& p) { return p.info().l2_persist_bytes; })
         .def_property_readonly("device", [](const PyArgCsr& p) { return p.info().device; })
         .def_property_readonly("dtype", [](const PyArgCsr& p) { return p.info().dtype == ARGCSR_F64 ? "float64" : "float32"; })
         .def_property_readonly("groups", [](const PyArgCsr& p) {

@@ -72,6 +72,11 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->unit_base);
     cudaFree(m->tiles);
     cudaFree(m->heavy);
+    cudaFree(m->heavy_ptr);
+    cudaFree(m->sched);
+    if (m->aux) cudaStreamDestroy(m->aux);
+    if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+    if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (prev >= 0) cudaSetDevice(prev);
     delete m;
 }
@@ -161,6 +166,12 @@ argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t tpg, uint6
         m->tm16 = true;
         try {
             m->l2_persist_max = ensure_l2_persist(device);
+            CUDA_OK(cudaDeviceGetAttribute(&m->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize, device));
+            CUDA_OK(cudaStreamCreateWithFlags(&m->aux, cudaStreamNonBlocking));
+            CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+            CUDA_OK(cudaMalloc(&m->sched, 2 * sizeof(uint32_t)));
+            CUDA_OK(cudaMemset(m->sched, 0, 2 * sizeof(uint32_t)));
             const uint64_t N = csr->num_rows, nnz = csr->nnz;
             const size_t es = elem_size(csr->dtype);
             const uint64_t* rp = csr->row_pointers;
@@ -214,9 +225,11 @@ argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info) {
         info->total_slots = m->total_slots;
         info->nnz = m->nnz;
         info->heavy_groups = m->num_heavy;
+        info->heavy_ctas = m->heavy_ctas;
         info->light_tiles = m->num_tiles;
         info->max_chunk_size = m->max_chunk;
         info->device_bytes = m->device_bytes;
+        info->l2_persist_bytes = m->l2_persist_max;
         info->device = m->device;
         info->dtype = m->dtype;
     });

@@ -73,12 +73,21 @@ struct argcsr_dev {
     uint64_t* unit_base = nullptr;        // [num_groups + 1] exclusive scan of light units
     uint32_t* tiles = nullptr;            // [num_tiles + 1] first group of each light tile
     uint32_t* heavy = nullptr;            // [num_heavy] heavy groups, chunk descending (LPT)
-    uint32_t num_tiles = 0, num_heavy = 0;
+    uint32_t* heavy_ptr = nullptr;        // [heavy_ctas + 1] packing of `heavy` into CTAs
+    uint32_t num_tiles = 0, num_heavy = 0, heavy_ctas = 0;
+    uint64_t heavy_max_lanes = 0;         // lanes of the fullest heavy CTA
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
-    uint64_t max_tile_units = 0;
+    uint64_t tile_span = 0;               // units between consecutive tile keys
+    uint64_t max_tile_units = 0;          // tile_span + ceil(tpg / V) - 1
+
+    // Heavy groups run on an auxiliary stream forked from the caller's stream.
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    uint32_t* sched = nullptr;            // [2] dynamic tile counter + done counter (self-resetting)
 
     // x residency (L2 persisting window) — queried, not hard-coded.
     size_t l2_persist_max = 0;
+    int l2_window_max = 0;
 
     size_t device_bytes = 0;
 };

@@ -286,19 +286,22 @@ struct HeavyFlag {
     __device__ uint64_t operator()(uint64_t g) const { return chunk[g] > kHeavyChunk ? 1 : 0; }
 };
 
-__global__ void k4_scatter_heavy(const uint32_t* __restrict__ chunk, const uint64_t* __restrict__ pos,
-                                 uint32_t G, uint32_t* __restrict__ ids, uint32_t* __restrict__ chunks) {
+template <typename TM>
+__global__ void k4_scatter_heavy(const uint32_t* __restrict__ chunk, const TM* __restrict__ assigned,
+                                 const uint64_t* __restrict__ pos, uint32_t G, uint32_t* __restrict__ ids,
+                                 uint32_t* __restrict__ chunks, uint32_t* __restrict__ lanes) {
     for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G;
          g += uint64_t(gridDim.x) * blockDim.x) {
         if (chunk[g] > kHeavyChunk) {
             ids[pos[g]] = uint32_t(g);
             chunks[pos[g]] = chunk[g];
+            lanes[pos[g]] = assigned[g];
         }
     }
 }
 
 // Light tile k starts at the first group whose unit base is >= k * B.
-__global__ void k4_tiles(const uint64_t* __restrict__ unit_base, uint32_t G, uint32_t ntiles,
+__global__ void k4_tiles(const uint64_t* __restrict__ unit_base, uint32_t G, uint32_t ntiles, uint64_t span,
                          uint32_t* __restrict__ tiles) {
     for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k <= ntiles;
          k += uint64_t(gridDim.x) * blockDim.x) {
@@ -306,7 +309,7 @@ __global__ void k4_tiles(const uint64_t* __restrict__ unit_base, uint32_t G, uin
             tiles[k] = G;
             continue;
         }
-        const uint64_t key = k * uint64_t(kTileThreads);
+        const uint64_t key = k * span;
         uint64_t lo = 0, hi = G;  // lower_bound over unit_base[0..G)
         while (lo < hi) {
             const uint64_t mid = (lo + hi) / 2;
@@ -519,28 +522,54 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
         CUDA_OK(cudaStreamSynchronize(s));
         m->num_heavy = uint32_t(nh);
         m->heavy = dev_alloc<uint32_t>(m, nh);
+        std::vector<uint32_t> hptr{0};
+        uint64_t max_lanes = 0;
         if (nh) {
-            DevPtr<uint32_t> ids(nh, s), chs(nh, s);
-            k4_scatter_heavy<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, hpos.p, G, ids.p, chs.p);
+            DevPtr<uint32_t> ids(nh, s), chs(nh, s), lns(nh, s);
+            k4_scatter_heavy<TM><<<grid_for(G, 256), 256, 0, s>>>(chunk.p, assigned, hpos.p, G, ids.p, chs.p, lns.p);
             LAUNCH_OK("k4_scatter_heavy");
-            std::vector<uint32_t> hid(nh), hch(nh);
+            std::vector<uint32_t> hid(nh), hch(nh), hln(nh);
             CUDA_OK(cudaMemcpyAsync(hid.data(), ids.p, nh * 4, cudaMemcpyDeviceToHost, s));
             CUDA_OK(cudaMemcpyAsync(hch.data(), chs.p, nh * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpyAsync(hln.data(), lns.p, nh * 4, cudaMemcpyDeviceToHost, s));
             CUDA_OK(cudaStreamSynchronize(s));
             std::vector<uint32_t> order(nh);
             std::iota(order.begin(), order.end(), 0u);
+            // LPT: longest chunk first; ties by group index (deterministic)
             std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hch[a] > hch[b]; });
             std::vector<uint32_t> sorted(nh);
-            for (uint64_t i = 0; i < nh; ++i) sorted[i] = hid[order[i]];
+            // Pack consecutive (similar-chunk) heavy groups into CTAs of <= kTileThreads lanes.
+            uint64_t lanes = 0;
+            for (uint64_t i = 0; i < nh; ++i) {
+                sorted[i] = hid[order[i]];
+                const uint64_t l = hln[order[i]];
+                if (lanes > 0 && lanes + l > uint64_t(kTileThreads)) {
+                    hptr.push_back(uint32_t(i));
+                    max_lanes = std::max(max_lanes, lanes);
+                    lanes = 0;
+                }
+                lanes += l;
+            }
+            hptr.push_back(uint32_t(nh));
+            max_lanes = std::max(max_lanes, lanes);
             CUDA_OK(cudaMemcpyAsync(m->heavy, sorted.data(), nh * 4, cudaMemcpyHostToDevice, s));
-            CUDA_OK(cudaStreamSynchronize(s));
         }
+        m->heavy_ctas = uint32_t(hptr.size() - 1);
+        m->heavy_max_lanes = max_lanes;
+        m->heavy_ptr = dev_alloc<uint32_t>(m, hptr.size());
+        CUDA_OK(cudaMemcpyAsync(m->heavy_ptr, hptr.data(), hptr.size() * 4, cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaStreamSynchronize(s));
     }
-    const uint64_t ntiles = (total_units + kTileThreads - 1) / kTileThreads;
+    // Tile keys every `span` units so that a tile (span + at most one group's
+    // units - 1) fits one CTA pass when a group has at most half a CTA of units.
+    const uint64_t maxu = (tpg + V - 1) / V;
+    const uint64_t span = maxu <= uint64_t(kTileThreads) / 2 ? uint64_t(kTileThreads) - maxu + 1 : uint64_t(kTileThreads);
+    m->tile_span = span;
+    const uint64_t ntiles = (total_units + span - 1) / span;
     if (ntiles > 0x7fffffffull) fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: matrix too large for the tile schedule");
     m->num_tiles = uint32_t(ntiles);
     m->tiles = dev_alloc<uint32_t>(m, ntiles + 1);
-    k4_tiles<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(m->unit_base, G, uint32_t(ntiles), m->tiles);
+    k4_tiles<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(m->unit_base, G, uint32_t(ntiles), span, m->tiles);
     LAUNCH_OK("k4_tiles");
     {
         DevPtr<unsigned long long> mx(1, s);
@@ -553,7 +582,7 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
         CUDA_OK(cudaMemcpyAsync(&mg, mx.p, sizeof mg, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
         m->max_tile_groups = uint32_t(mg);
-        m->max_tile_units = kTileThreads + (tpg + V - 1) / V;
+        m->max_tile_units = span + maxu - 1;
     }
 
     // K5

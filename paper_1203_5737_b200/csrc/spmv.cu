@@ -1,28 +1,31 @@
 // ARG-CSR SpMV for sm_100a (replaces spmv_argcsr_groups, proj/src/argcsr.cpp:185-217).
 //
 // One launch, two CTA roles:
-//   * heavy CTAs (blockIdx < num_heavy): one long-chunk group each, in LPT
-//     order (largest chunk first), one lane per thread with a deep unroll so a
-//     1-3 MB group streams at full per-SM bandwidth;
+//   * heavy CTAs (blockIdx < heavy_ctas): long-chunk groups in LPT order
+//     (largest chunk first), packed so their assigned lanes fill the CTA, one
+//     lane per thread, deep unroll so a 1-3 MB group streams at per-SM speed;
 //   * light tiles: a run of consecutive short-chunk groups whose ASSIGNED lanes
 //     (free lanes are never read) are flattened into V-lane units, one unit per
-//     thread.  A unit's V adjacent lanes are one 128-bit column load and
-//     V*8 bytes of values per element step, so every warp access is a
-//     contiguous, coalesced segment of a group's j-row.
-// Group metadata of a tile is staged in shared memory; per-chunk partial sums
-// go to shared memory and each row sums its chunk range in ascending order
-// from +0.0.  Products and sums use __dmul_rn/__dadd_rn in the reference's
-// order (phase 1: per lane, j ascending; phase 2: per row, chunks ascending),
-// so fp64 results are bit-identical to the reference's CPU product (which has
-// no FMA).  fp32 handles load fp32 values/x, multiply exactly in fp64 and round
-// the row sum once.
+//     thread.  A unit's V adjacent lanes are one vector column load (16 B for
+//     V=4) and one vector value load (32 B, LDG.256, for fp64 V=4) per element
+//     step, so every warp access is a contiguous, coalesced segment of a
+//     group's j-row.  All element steps of a unit (up to U) are issued before
+//     the first x gather, so a tile has its whole matrix block in flight.
+// Group metadata of a tile is staged in shared memory and threads_mapping of
+// the tile's rows is prefetched into registers during phase 1; per-chunk
+// partial sums go to shared memory and each row sums its chunk range in
+// ascending order from +0.0.  Products and sums use __dmul_rn/__dadd_rn in the
+// reference's order (phase 1: per lane, j ascending; phase 2: per row, chunks
+// ascending), so fp64 results are bit-identical to the reference's CPU product
+// (which has no FMA).  fp32 handles load fp32 values/x, multiply exactly in
+// fp64 and round each row sum once.
 //
-// Streams: values/columns are read once per SpMV with evict-first loads
-// (__ldcs -> LDG.E.EF); x is gathered through the read-only path and kept L2
-// resident with an access-policy window sized from the device's persisting-L2
-// limit.
+// Cache policy: values/columns are streamed once (L1 no-allocate, L2
+// evict-first); x gathers are L2 evict-last and x is additionally covered by a
+// persisting access-policy window sized from the device's persisting-L2 limit.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "spmv.cuh"
@@ -31,115 +34,139 @@ namespace argcsr_gpu {
 
 namespace {
 
-template <typename T, typename TM>
+template <typename T>
 struct SpmvArgs {
     const T* __restrict__ vals;
     const int32_t* __restrict__ cols;
     const GroupDesc* __restrict__ groups;
-    const TM* __restrict__ tm;
-    const TM* __restrict__ assigned;
+    const uint16_t* __restrict__ tm;
+    const uint16_t* __restrict__ assigned;
     const uint64_t* __restrict__ unit_base;
     const uint32_t* __restrict__ tiles;
     const uint32_t* __restrict__ heavy;
+    const uint32_t* __restrict__ heavy_ptr;
     const T* __restrict__ x;
     T* __restrict__ y;
     uint64_t tpg;
-    uint32_t num_heavy;
+    uint32_t heavy_ctas;
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
     uint32_t max_tile_groups;
+    uint32_t max_tile_units;
+    int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
+    int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
 };
 
-// ----------------------------------------------------------------- loads
-template <int V> struct IVec;
-template <> struct IVec<1> { using type = int; };
-template <> struct IVec<2> { using type = int2; };
-template <> struct IVec<4> { using type = int4; };
+// ------------------------------------------------------------ cache policies
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 
+// Streaming loads of V adjacent columns / values (V * sizeof bytes, aligned).
 template <int V>
-__device__ __forceinline__ void load_cols(const int32_t* p, int (&c)[V]) {
+__device__ __forceinline__ void ld_cols(const int32_t* p, int (&c)[V], uint64_t pol) {
     if constexpr (V == 4) {
-        const int4 v = __ldcs(reinterpret_cast<const int4*>(p));
-        c[0] = v.x, c[1] = v.y, c[2] = v.z, c[3] = v.w;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]) : "l"(p), "l"(pol));
     } else if constexpr (V == 2) {
-        const int2 v = __ldcs(reinterpret_cast<const int2*>(p));
-        c[0] = v.x, c[1] = v.y;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+                     : "=r"(c[0]), "=r"(c[1]) : "l"(p), "l"(pol));
     } else {
-        c[0] = __ldcs(p);
-    }
-}
-
-// Values of a unit, loaded only for 16-byte pieces holding a non-sentinel lane.
-template <int V>
-__device__ __forceinline__ void load_vals(const double* p, const int (&c)[V], double (&v)[V]) {
-    if constexpr (V == 1) {
-        v[0] = c[0] != -1 ? __ldcs(p) : 0.0;
-    } else {
-#pragma unroll
-        for (int h = 0; h < V; h += 2) {
-            if ((c[h] & c[h + 1]) != -1) {
-                const double2 d = __ldcs(reinterpret_cast<const double2*>(p + h));
-                v[h] = d.x, v[h + 1] = d.y;
-            } else {
-                v[h] = 0.0, v[h + 1] = 0.0;
-            }
-        }
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(c[0]) : "l"(p), "l"(pol));
     }
 }
 template <int V>
-__device__ __forceinline__ void load_vals(const float* p, const int (&c)[V], float (&v)[V]) {
+__device__ __forceinline__ void ld_vals(const double* p, double (&v)[V], uint64_t pol) {
     if constexpr (V == 4) {
-        if ((c[0] & c[1] & c[2] & c[3]) != -1) {
-            const float4 d = __ldcs(reinterpret_cast<const float4*>(p));
-            v[0] = d.x, v[1] = d.y, v[2] = d.z, v[3] = d.w;
-        } else {
-            v[0] = v[1] = v[2] = v[3] = 0.f;
-        }
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p), "l"(pol));
     } else if constexpr (V == 2) {
-        if ((c[0] & c[1]) != -1) {
-            const float2 d = __ldcs(reinterpret_cast<const float2*>(p));
-            v[0] = d.x, v[1] = d.y;
-        } else {
-            v[0] = v[1] = 0.f;
-        }
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
     } else {
-        v[0] = c[0] != -1 ? __ldcs(p) : 0.f;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(pol));
+    }
+}
+template <int V>
+__device__ __forceinline__ void ld_vals(const float* p, float (&v)[V], uint64_t pol) {
+    if constexpr (V == 4) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
+    } else if constexpr (V == 2) {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(v[0]), "=f"(v[1]) : "l"(p), "l"(pol));
+    } else {
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v[0]) : "l"(p), "l"(pol));
     }
 }
 
-__device__ __forceinline__ double load_x(const double* x, int c) { return c != -1 ? __ldg(x + c) : 0.0; }
-__device__ __forceinline__ double load_x(const float* x, int c) { return c != -1 ? double(__ldg(x + c)) : 0.0; }
+__device__ __forceinline__ double ld_x(const double* p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_x(const float* p, uint64_t pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return double(v);
+}
 
 // Phase 1 (argcsr.cpp:193-203) for V adjacent lanes starting at slot0: per
 // lane, sum += v * x[c] over j ascending until the first sentinel.  Columns
-// of U element steps are in flight together; the layout keeps sentinels
+// and values of U element steps are issued together (values of a fully
+// finished vector are skipped when PRED); the layout keeps sentinels
 // trailing, so "skip sentinel" == "stop at the first sentinel".
-template <typename T, int V, int U>
-__device__ __forceinline__ void phase1(const T* __restrict__ vals, const int32_t* __restrict__ cols,
-                                       const T* __restrict__ x, uint64_t slot0, uint32_t chunk, uint64_t tpg,
-                                       double (&s)[V]) {
+template <typename T, int V, int U, bool PRED>
+__device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, double (&s)[V],
+                                       uint64_t pol_stream, uint64_t pol_x) {
 #pragma unroll
     for (int l = 0; l < V; ++l) s[l] = 0.0;
-    const int32_t* cp = cols + slot0;
-    const T* vp = vals + slot0;
+    const int32_t* cp = a.cols + slot0;
+    const T* vp = a.vals + slot0;
+    const uint64_t tpg = a.tpg;
     for (uint32_t j0 = 0; j0 < chunk; j0 += U) {
         int c[U][V];
         T v[U][V];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (j0 + u < chunk) {
-                load_cols<V>(cp + uint64_t(j0 + u) * tpg, c[u]);
+                ld_cols<V>(cp + uint64_t(j0 + u) * tpg, c[u], pol_stream);
+                if constexpr (!PRED) ld_vals<V>(vp + uint64_t(j0 + u) * tpg, v[u], pol_stream);
             } else {
 #pragma unroll
-                for (int l = 0; l < V; ++l) c[u][l] = -1;
+                for (int l = 0; l < V; ++l) c[u][l] = -1, v[u][l] = T(0);
             }
         }
+        if constexpr (PRED) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) load_vals<V>(vp + uint64_t(j0 + u) * tpg, c[u], v[u]);
+            for (int u = 0; u < U; ++u) {
+                int any = -1;
+#pragma unroll
+                for (int l = 0; l < V; ++l) any &= c[u][l];
+                if (any != -1) {
+                    ld_vals<V>(vp + uint64_t(j0 + u) * tpg, v[u], pol_stream);
+                } else {
+#pragma unroll
+                    for (int l = 0; l < V; ++l) v[u][l] = T(0);
+                }
+            }
+        }
         double xv[U][V];
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int l = 0; l < V; ++l) xv[u][l] = load_x(x, c[u][l]);
+            for (int l = 0; l < V; ++l) xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -156,51 +183,85 @@ template <typename T> __device__ __forceinline__ T to_out(double v);
 template <> __device__ __forceinline__ double to_out<double>(double v) { return v; }
 template <> __device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
 
-// Phase 2 (argcsr.cpp:206-215): y[row] = +0.0 + p_b + p_{b+1} + ... ascending.
-template <typename T, typename TM>
-__device__ __forceinline__ void reduce_row(const SpmvArgs<T, TM>& a, const double* part, uint32_t row,
-                                           bool first_of_group) {
-    const uint32_t b = first_of_group ? 0u : uint32_t(a.tm[row - 1]);
-    const uint32_t e = uint32_t(a.tm[row]);
+// Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending.
+__device__ __forceinline__ double row_sum(const double* part, uint32_t b, uint32_t e) {
     double sum = 0.0;
     for (uint32_t t = b; t < e; ++t) sum = __dadd_rn(sum, part[t]);
-    a.y[row] = to_out<T>(sum);
+    return sum;
 }
 
-constexpr int kUnrollLight = 2;
-constexpr int kUnrollHeavy = 8;
+// last index i in [0, n) with arr[i] <= key (arr ascending, arr[0] <= key)
+__device__ __forceinline__ uint32_t find_le(const uint32_t* arr, uint32_t n, uint32_t key) {
+    uint32_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (arr[mid] <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
 
-template <typename T, typename TM, int V>
-__global__ void __launch_bounds__(kTileThreads) spmv_kernel(const SpmvArgs<T, TM> a) {
+// Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
+// order, one lane per thread.
+template <typename T, int UH>
+__global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
-
-    if (blockIdx.x < a.num_heavy) {
-        // ---------------------------------------------------- heavy group
-        const uint32_t g = a.heavy[blockIdx.x];
-        if (g < a.g_begin || g >= a.g_end) return;
-        const GroupDesc d = a.groups[g];
-        const uint32_t f = d.first_row, k = a.groups[g + 1].first_row - f;
-        const uint32_t asg = uint32_t(a.assigned[g]);
-        for (uint32_t l = threadIdx.x; l < asg; l += blockDim.x) {
-            double s[1];
-            phase1<T, 1, kUnrollHeavy>(a.vals, a.cols, a.x, d.offset + l, d.chunk, a.tpg, s);
-            s_part[l] = s[0];
+    __shared__ uint32_t s_lane0[kTileThreads + 1], s_row0[kTileThreads + 1], s_g[kTileThreads];
+    const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const uint32_t hb = a.heavy_ptr[blockIdx.x], he = a.heavy_ptr[blockIdx.x + 1];
+    const uint32_t ng = he - hb;
+    if (threadIdx.x == 0) {
+        uint32_t lanes = 0, rows = 0;
+        for (uint32_t i = 0; i < ng; ++i) {
+            const uint32_t g = a.heavy[hb + i];
+            s_g[i] = g;
+            s_lane0[i] = lanes;
+            s_row0[i] = rows;
+            lanes += a.assigned[g];
+            rows += a.groups[g + 1].first_row - a.groups[g].first_row;
         }
-        __syncthreads();
-        for (uint32_t r = threadIdx.x; r < k; r += blockDim.x) reduce_row(a, s_part, f + r, r == 0);
-        return;
+        s_lane0[ng] = lanes;
+        s_row0[ng] = rows;
     }
+    __syncthreads();
+    const uint32_t nlanes = s_lane0[ng], nrows = s_row0[ng];
+    for (uint32_t l = threadIdx.x; l < nlanes; l += blockDim.x) {
+        const uint32_t i = find_le(s_lane0, ng, l);
+        const uint32_t g = s_g[i];
+        if (g < a.g_begin || g >= a.g_end) continue;
+        const GroupDesc d = a.groups[g];
+        double s[1];
+        phase1<T, 1, UH, false>(a, d.offset + (l - s_lane0[i]), d.chunk, s, pol_stream, pol_x);
+        s_part[l] = s[0];
+    }
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < nrows; r += blockDim.x) {
+        const uint32_t i = find_le(s_row0, ng, r);
+        const uint32_t g = s_g[i];
+        if (g < a.g_begin || g >= a.g_end) continue;
+        const uint32_t f = a.groups[g].first_row;
+        const uint32_t row = f + (r - s_row0[i]);
+        const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
+        a.y[row] = to_out<T>(row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
+    }
+}
 
-    // -------------------------------------------------------- light tile
-    const uint32_t kt = blockIdx.x - a.num_heavy;
+// Light tile kt: consecutive short-chunk groups, V-lane units, one unit per thread.
+template <typename T, int V, int U, bool PRED, int MINB>
+__global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const SpmvArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* s_part = reinterpret_cast<double*>(smem);
+    const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+
+    const uint32_t kt = blockIdx.x;
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
     if (ge <= a.g_begin || gs >= a.g_end || gs == ge) return;
     const uint32_t ng = ge - gs;
     const uint32_t cap = a.max_tile_groups;
-    // smem: s_part[(max units) * V] | s_off[cap] | s_ub[cap+1] | s_first[cap+1] | s_chunk[cap]
-    const size_t part_words = size_t(kTileThreads + (a.tpg + V - 1) / V) * V;
-    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_part + part_words);
+    // smem: s_part[max_tile_units * V] | s_off[cap] | s_ub[cap+1] | s_first[cap+1] | s_chunk[cap]
+    uint64_t* s_off = reinterpret_cast<uint64_t*>(s_part + size_t(a.max_tile_units) * V);
     uint32_t* s_ub = reinterpret_cast<uint32_t*>(s_off + cap);
     uint32_t* s_first = s_ub + cap + 1;
     uint32_t* s_chunk = s_first + cap + 1;
@@ -217,42 +278,415 @@ __global__ void __launch_bounds__(kTileThreads) spmv_kernel(const SpmvArgs<T, TM
     }
     __syncthreads();
 
+    // Phase-2 metadata of this thread's first row, fetched under phase 1.
+    const uint32_t row0 = s_first[0], row_end = s_first[ng];
+    const uint32_t pr = row0 + threadIdx.x;
+    uint32_t pgi = 0, pb = 0, pe = 0;
+    bool pvalid = false;
+    if (pr < row_end) {
+        pgi = find_le(s_first, ng, pr);
+        const uint32_t g = gs + pgi;
+        pvalid = s_chunk[pgi] <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
+        if (pvalid) {
+            pb = pr == s_first[pgi] ? 0u : uint32_t(a.tm[pr - 1]);
+            pe = uint32_t(a.tm[pr]);
+        }
+    }
+
     const uint32_t nunits = s_ub[ng];
     for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) {
-        uint32_t lo = 0, hi = ng - 1;  // last group with s_ub <= u
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) / 2;
-            if (s_ub[mid] <= u) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t gi = lo;
+        const uint32_t gi = find_le(s_ub, ng, u);
         const uint32_t g = gs + gi;
         if (s_chunk[gi] > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
-        const uint32_t lane0 = (u - s_ub[gi]) * V;
         double s[V];
-        phase1<T, V, kUnrollLight>(a.vals, a.cols, a.x, s_off[gi] + lane0, s_chunk[gi], a.tpg, s);
+        phase1<T, V, U, PRED>(a, s_off[gi] + (u - s_ub[gi]) * V, s_chunk[gi], s, pol_stream, pol_x);
 #pragma unroll
         for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = s[l];
     }
     __syncthreads();
 
-    const uint32_t row0 = s_first[0], row_end = s_first[ng];
-    for (uint32_t r = row0 + threadIdx.x; r < row_end; r += blockDim.x) {
-        uint32_t lo = 0, hi = ng - 1;  // last group with s_first <= r
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) / 2;
-            if (s_first[mid] <= r) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t gi = lo;
+    if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
+    for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
+        const uint32_t gi = find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
         if (s_chunk[gi] > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
-        reduce_row(a, s_part + size_t(s_ub[gi]) * V, r, r == s_first[gi]);
+        const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
+        a.y[r] = to_out<T>(row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
     }
+}
+
+// ------------------------------------------------ pipelined light path (V = 4)
+// Persistent CTAs walk the light tiles k = blockIdx.x, +gridDim.x, ...  Each
+// thread owns one 4-lane unit of the current tile and streams that unit's
+// column/value slabs (J element steps) into its PRIVATE shared-memory slots
+// with cp.async, one slab ahead of the x gathers it is doing; the next tile's
+// group metadata and its first slab are prefetched across the tile boundary.
+// In-flight matrix bytes therefore cost no registers, and the HBM stream never
+// waits on the x gathers or on phase 2.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename T>
+struct PipeUnit {  // this thread's unit in the current tile
+    uint64_t slot0 = 0;
+    uint32_t chunk = 0;
+    uint32_t nslabs = 0;
+};
+
+template <typename T, int J>
+__device__ __forceinline__ void pipe_issue_slab(const SpmvArgs<T>& a, const PipeUnit<T>& pu, uint32_t s, int4* cslot,
+                                                unsigned char* vslot, uint64_t pol) {
+    // slab s: element steps j = s*J .. s*J+J-1 of this unit (only j < chunk)
+    constexpr int VB = 4 * sizeof(T);  // value bytes per unit step (32 fp64 / 16 fp32)
+#pragma unroll
+    for (int q = 0; q < J; ++q) {
+        const uint32_t j = s * J + q;
+        if (j < pu.chunk) {
+            const uint64_t slot = pu.slot0 + uint64_t(j) * a.tpg;
+            cp_async16(smem_u32(cslot + q * kTileThreads), a.cols + slot, pol);
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.vals + slot);
+            unsigned char* dst = vslot + size_t(q) * kTileThreads * VB;
+#pragma unroll
+            for (int h = 0; h < VB; h += 16) cp_async16(smem_u32(dst + h), src + h, pol);
+        }
+    }
+}
+
+template <typename T, int J>
+__global__ void __launch_bounds__(kTileThreads, 2) spmv_pipe_kernel(const SpmvArgs<T> a, uint32_t num_tiles) {
+    constexpr int VB = 4 * sizeof(T);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t cap = a.max_tile_groups;
+    // layout: cols[2][J][B] int4 | vals[2][J][B][VB] | part[B*4] f64 | meta[2]{desc[cap+1], ub[cap+1]}
+    int4* s_cols = reinterpret_cast<int4*>(smem);
+    unsigned char* s_vals = smem + size_t(2) * J * kTileThreads * sizeof(int4);
+    double* s_part = reinterpret_cast<double*>(s_vals + size_t(2) * J * kTileThreads * VB);
+    unsigned char* mbase = reinterpret_cast<unsigned char*>(s_part + kTileThreads * 4);
+    const size_t meta_bytes = ((size_t(cap) + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15);
+    auto meta_desc = [&](int b) { return reinterpret_cast<GroupDesc*>(mbase + b * meta_bytes); };
+    auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
+    const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const uint32_t tid = threadIdx.x;
+
+    auto issue_meta = [&](uint32_t k, int b) {
+        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
+        for (uint32_t i = tid; i <= ge - gs; i += blockDim.x) {
+            cp_async16(smem_u32(meta_desc(b) + i), a.groups + gs + i, pol_x);
+            cp_async8(smem_u32(meta_ub(b) + i), a.unit_base + gs + i);
+        }
+    };
+    // this thread's unit of tile k (metadata in buffer b); returns group index in tile
+    auto my_unit = [&](uint32_t k, int b, PipeUnit<T>& pu, uint32_t& gi_out) -> bool {
+        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
+        const uint32_t ng = ge - gs;
+        const uint64_t ub0 = meta_ub(b)[0];
+        const uint64_t u = ub0 + tid;
+        pu = PipeUnit<T>{};
+        if (ng == 0 || u >= meta_ub(b)[ng]) return false;
+        uint32_t lo = 0, hi = ng - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) / 2;
+            if (meta_ub(b)[mid] <= u) lo = mid; else hi = mid - 1;
+        }
+        gi_out = lo;
+        const GroupDesc d = meta_desc(b)[lo];
+        const uint32_t g = gs + lo;
+        if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) return false;
+        pu.slot0 = d.offset + (u - meta_ub(b)[lo]) * 4;
+        pu.chunk = d.chunk;
+        pu.nslabs = (d.chunk + J - 1) / J;
+        return true;
+    };
+
+    uint32_t k = blockIdx.x;
+    if (k >= num_tiles) return;
+    int mb = 0;
+    issue_meta(k, mb);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    PipeUnit<T> pu;
+    uint32_t gi = 0;
+    bool have = my_unit(k, mb, pu, gi);
+    if (have) pipe_issue_slab<T, J>(a, pu, 0, s_cols + tid, s_vals + size_t(tid) * VB, pol);
+    cp_commit();
+
+    for (;;) {
+        const uint32_t kn = k + gridDim.x;
+        const bool has_next = kn < num_tiles;
+        // next tile's metadata, landing while this tile streams
+        if (has_next) issue_meta(kn, mb ^ 1);
+        cp_commit();
+        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
+        const uint32_t ng = ge - gs;
+        const GroupDesc* md = meta_desc(mb);
+        const uint64_t* mub = meta_ub(mb);
+        const uint64_t ub0 = mub[0];
+
+        // phase-2 metadata of this thread's first row of tile k (registers)
+        const uint32_t row0 = md[0].first_row, row_end = md[ng].first_row;
+        const uint32_t pr = row0 + tid;
+        uint32_t pgi = 0, pb = 0, pe = 0;
+        bool pvalid = false;
+        if (pr < row_end && ng > 0) {
+            uint32_t lo = 0, hi = ng - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) / 2;
+                if (md[mid].first_row <= pr) lo = mid; else hi = mid - 1;
+            }
+            pgi = lo;
+            const uint32_t g = gs + pgi;
+            pvalid = md[pgi].chunk <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
+            if (pvalid) {
+                pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
+                pe = uint32_t(a.tm[pr]);
+            }
+        }
+
+        // phase 1: slab pipeline over this thread's unit
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        bool done = false;
+        for (uint32_t sidx = 0; sidx < pu.nslabs; ++sidx) {
+            const int buf = sidx & 1;
+            if (sidx + 1 < pu.nslabs) {
+                const int nb = buf ^ 1;
+                pipe_issue_slab<T, J>(a, pu, sidx + 1, s_cols + size_t(nb) * J * kTileThreads + tid,
+                                      s_vals + (size_t(nb) * J * kTileThreads + tid) * VB, pol);
+            }
+            cp_commit();
+            cp_wait<1>();
+            const int4* cs = s_cols + size_t(buf) * J * kTileThreads + tid;
+            const unsigned char* vs = s_vals + (size_t(buf) * J * kTileThreads + tid) * VB;
+            int c[J][4];
+            double xv[J][4];
+#pragma unroll
+            for (int q = 0; q < J; ++q) {
+                const bool in = sidx * J + q < pu.chunk;
+                const int4 cc = in ? cs[q * kTileThreads] : make_int4(-1, -1, -1, -1);
+                c[q][0] = cc.x, c[q][1] = cc.y, c[q][2] = cc.z, c[q][3] = cc.w;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) xv[q][l] = c[q][l] != -1 ? ld_x(a.x + c[q][l], pol_x) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < J; ++q) {
+                const T* vv = reinterpret_cast<const T*>(vs + size_t(q) * kTileThreads * VB);
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    if (c[q][l] != -1) acc[l] = __dadd_rn(acc[l], __dmul_rn(double(vv[l]), xv[q][l]));
+            }
+            if ((c[J - 1][0] & c[J - 1][1] & c[J - 1][2] & c[J - 1][3]) == -1) {
+                done = true;
+                break;
+            }
+        }
+        (void)done;
+        if (have) {
+            const uint64_t u = ub0 + tid;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) s_part[size_t(u - ub0) * 4 + l] = acc[l];
+        }
+        cp_wait<0>();  // next tile's metadata (and any abandoned slab) landed
+        __syncthreads();
+
+        // prefetch the next tile's first slab before phase 2 of this tile
+        PipeUnit<T> pn;
+        uint32_t gin = 0;
+        bool have_n = false;
+        if (has_next) {
+            have_n = my_unit(kn, mb ^ 1, pn, gin);
+            if (have_n) pipe_issue_slab<T, J>(a, pn, 0, s_cols + tid, s_vals + size_t(tid) * VB, pol);
+        }
+        cp_commit();
+
+        // phase 2 of tile k
+        if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(mub[pgi] - ub0) * 4, pb, pe));
+        for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
+            uint32_t lo = 0, hi = ng - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) / 2;
+                if (md[mid].first_row <= r) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t g = gs + lo;
+            if (md[lo].chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+            const uint32_t b = r == md[lo].first_row ? 0u : uint32_t(a.tm[r - 1]);
+            a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[lo] - ub0) * 4, b, uint32_t(a.tm[r])));
+        }
+        __syncthreads();  // partials and metadata buffer mb are reused
+        if (!has_next) break;
+        k = kn;
+        mb ^= 1;
+        pu = pn;
+        have = have_n;
+        gi = gin;
+    }
+    cp_wait<0>();
+}
+
+// --------------------------------------- persistent light path (prefetched metadata)
+// Same per-tile work as spmv_light_kernel, but each CTA walks tiles k,
+// k+gridDim.x, ... and prefetches the NEXT tile's group descriptors and unit
+// bases into a second shared-memory buffer with cp.async while the current
+// tile streams, so the two dependent metadata round trips leave the critical
+// path (the tiles[] entries are fetched one more tile ahead into registers).
+__device__ __forceinline__ uint32_t find_le64(const uint64_t* arr, uint32_t n, uint64_t key) {
+    uint32_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (arr[mid] <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+__device__ __forceinline__ uint32_t find_row(const GroupDesc* d, uint32_t n, uint32_t row) {
+    uint32_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (d[mid].first_row <= row) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
+__global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const SpmvArgs<T> a, uint32_t num_tiles,
+                                                                        uint32_t* __restrict__ sched) {
+    // sched[0]: next dynamic tile (offset by gridDim.x), sched[1]: CTAs done;
+    // the last CTA to finish resets both, so consecutive launches reuse them.
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_grab[2];  // alternating slots: written one sync after the last read
+    double* s_part = reinterpret_cast<double*>(smem);
+    const uint32_t cap = a.max_tile_groups;
+    const size_t part_bytes = (size_t(a.max_tile_units) * V * sizeof(double) + 15) & ~size_t(15);
+    unsigned char* mbase = smem + part_bytes;
+    const size_t meta_bytes = ((size_t(cap) + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15);
+    auto meta_desc = [&](int b) { return reinterpret_cast<GroupDesc*>(mbase + b * meta_bytes); };
+    auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
+    const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const uint32_t tid = threadIdx.x;
+    auto issue_meta = [&](uint32_t gs, uint32_t ge, int b) {
+        for (uint32_t i = tid; i <= ge - gs; i += blockDim.x) {
+            cp_async16(smem_u32(meta_desc(b) + i), a.groups + gs + i, pol_x);
+            cp_async8(smem_u32(meta_ub(b) + i), a.unit_base + gs + i);
+        }
+    };
+    // Tile order: static round-robin (k += gridDim.x; neighbouring tiles run
+    // concurrently, which keeps stencil x windows hot in L2) or dynamic.
+    uint32_t static_next = blockIdx.x;
+    auto grab = [&]() {
+        if constexpr (DYN) return gridDim.x + atomicAdd(sched, 1u);
+        static_next += gridDim.x;
+        return static_next;
+    };
+
+    uint32_t k = blockIdx.x, it = 0;
+    if (tid == 0) s_grab[0] = grab();
+    uint32_t gs = 0, ge = 0;
+    if (k < num_tiles) {
+        gs = a.tiles[k], ge = a.tiles[k + 1];
+        issue_meta(gs, ge, 0);
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    uint32_t kn = s_grab[0], gsn = 0, gen = 0;
+    if (kn < num_tiles) gsn = a.tiles[kn], gen = a.tiles[kn + 1];
+    int mb = 0;
+    while (k < num_tiles) {
+        const bool has_next = kn < num_tiles;
+        if (has_next) issue_meta(gsn, gen, mb ^ 1);
+        cp_commit();
+        if (tid == 0) s_grab[(it + 1) & 1] = has_next ? grab() : num_tiles;
+
+        const uint32_t ng = ge - gs;
+        const GroupDesc* md = meta_desc(mb);
+        const uint64_t* mub = meta_ub(mb);
+        const bool live = ng > 0 && !(ge <= a.g_begin || gs >= a.g_end);
+        const uint64_t ub0 = mub[0];
+        const uint32_t row0 = md[0].first_row, row_end = live ? md[ng].first_row : row0;
+
+        // phase-2 metadata of this thread's first row (registers)
+        const uint32_t pr = row0 + tid;
+        uint32_t pgi = 0, pb = 0, pe = 0;
+        bool pvalid = false;
+        if (pr < row_end) {
+            pgi = find_row(md, ng, pr);
+            const uint32_t g = gs + pgi;
+            pvalid = md[pgi].chunk <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
+            if (pvalid) {
+                pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
+                pe = uint32_t(a.tm[pr]);
+            }
+        }
+        const uint32_t nunits = live ? uint32_t(mub[ng] - ub0) : 0u;
+        for (uint32_t u = tid; u < nunits; u += blockDim.x) {
+            const uint32_t gi = find_le64(mub, ng, ub0 + u);
+            const uint32_t g = gs + gi;
+            const GroupDesc d = md[gi];
+            if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+            double sacc[V];
+            phase1<T, V, U, PRED>(a, d.offset + (ub0 + u - mub[gi]) * V, d.chunk, sacc, pol_stream, pol_x);
+#pragma unroll
+            for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = sacc[l];
+        }
+        cp_wait<0>();
+        __syncthreads();
+        const uint32_t k2 = s_grab[(it + 1) & 1];  // tile after next: its tiles[] entries load under phase 2
+        uint32_t gs2 = 0, ge2 = 0;
+        if (k2 < num_tiles) gs2 = a.tiles[k2], ge2 = a.tiles[k2 + 1];
+
+        if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(mub[pgi] - ub0) * V, pb, pe));
+        for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
+            const uint32_t gi = find_row(md, ng, r);
+            const uint32_t g = gs + gi;
+            if (md[gi].chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+            const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
+            a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
+        }
+        __syncthreads();
+        k = kn, gs = gsn, ge = gen;
+        kn = k2, gsn = gs2, gen = ge2;
+        mb ^= 1;
+        ++it;
+    }
+    if (DYN && tid == 0) {
+        __threadfence();
+        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+size_t lightp_smem_bytes(const argcsr_dev* m, int V) {
+    const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
+    return ((size_t(m->max_tile_units) * V * sizeof(double) + 15) & ~size_t(15)) +
+           2 * (((cap + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15));
+}
+
+template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
+void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s);
+
+size_t pipe_smem_bytes(const argcsr_dev* m, int J, size_t tbytes) {
+    const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
+    return size_t(2) * J * kTileThreads * (16 + 4 * tbytes) + size_t(kTileThreads) * 4 * sizeof(double) +
+           2 * (((cap + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15));
 }
 
 size_t light_smem_bytes(const argcsr_dev* m, int V) {
     const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
-    const size_t part = size_t(kTileThreads + (m->tpg + V - 1) / V) * V * sizeof(double);
-    return part + cap * sizeof(uint64_t) + (cap + 1) * 4 * 2 + cap * 4;
+    return size_t(m->max_tile_units) * V * sizeof(double) + cap * sizeof(uint64_t) + (cap + 1) * 4 * 2 + cap * 4;
 }
 
 bool l2_window_enabled() {
@@ -263,31 +697,30 @@ bool l2_window_enabled() {
     return on;
 }
 
-template <typename T, typename TM, int V>
-void launch_typed(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint32_t ge, cudaStream_t s) {
-    SpmvArgs<T, TM> a;
-    a.vals = static_cast<const T*>(m->values);
-    a.cols = m->columns;
-    a.groups = m->groups;
-    a.tm = static_cast<const TM*>(m->tm);
-    a.assigned = static_cast<const TM*>(m->assigned);
-    a.unit_base = m->unit_base;
-    a.tiles = m->tiles;
-    a.heavy = m->heavy;
-    a.x = static_cast<const T*>(x);
-    a.y = static_cast<T*>(y);
-    a.tpg = m->tpg;
-    a.num_heavy = m->num_heavy;
-    a.g_begin = gb;
-    a.g_end = ge;
-    a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
+// Kernel variant for experiments: ARGCSR_SPMV_VARIANT = U<unroll>P<pred>B<min CTAs/SM>,
+// one of the instantiated set below.
+int variant_id() {
+    static const int id = [] {
+        const char* e = std::getenv("ARGCSR_SPMV_VARIANT");
+        if (!e) return 0;
+        const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
+                               "PIPE2", "PIPE4", "LP4P0B4", "LP2P1B6", "LPD4P1B4"};
+        for (int i = 0; i < 13; ++i)
+            if (!std::strcmp(e, names[i])) return i;
+        return -1;
+    }();
+    return id;
+}
 
-    const size_t smem = std::max(light_smem_bytes(m, V), size_t(m->tpg) * sizeof(double));
-    auto kern = spmv_kernel<T, TM, V>;
-    if (smem > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const unsigned grid = m->num_heavy + m->num_tiles;
+int env_flag(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? (e[0] != '0') : dflt;
+}
+
+template <typename K, typename T>
+void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     if (grid == 0) return;
-
+    if (smem > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kTileThreads);
@@ -297,14 +730,13 @@ void launch_typed(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     cfg.numAttrs = 0;
     const size_t xbytes = m->num_cols * sizeof(T);
     if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
-        int max_win = 0;
-        CUDA_OK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, m->device));
-        const size_t win = std::min<size_t>(xbytes, size_t(max_win));
+        // Persist the leading part of x that fits the carve-out (hit ratio 1):
+        // all of x for the stencils; the hot low-index columns of R-MAT.
+        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(x);
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
         attr[0].val.accessPolicyWindow.num_bytes = win;
-        attr[0].val.accessPolicyWindow.hitRatio =
-            float(std::min(1.0, double(m->l2_persist_max) / double(win)));
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
         attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.attrs = attr;
@@ -313,12 +745,156 @@ void launch_typed(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
+template <typename T, int V, int U, bool PRED, int MINB>
+void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    launch(spmv_light_kernel<T, V, U, PRED, MINB>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
+}
+
+template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
+void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = lightp_smem_bytes(m, V);
+    auto kern = spmv_lightp_kernel<T, V, U, PRED, MINB, DYN>;
+    if (smem > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileThreads, smem));
+    const unsigned grid = unsigned(std::min<uint64_t>(m->num_tiles, uint64_t(std::max(per_sm, 1)) * sms));
+    if (grid == 0) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.numAttrs = 0;
+    const size_t xbytes = m->num_cols * sizeof(T);
+    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
+        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
+        attr[0].val.accessPolicyWindow.num_bytes = win;
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles, m->sched));
+}
+
+template <typename T, int J>
+void launch_pipe(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = pipe_smem_bytes(m, J, sizeof(T));
+    auto kern = spmv_pipe_kernel<T, J>;
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileThreads, smem));
+    const unsigned grid = unsigned(std::min<uint64_t>(m->num_tiles, uint64_t(std::max(per_sm, 1)) * sms));
+    if (grid == 0) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.numAttrs = 0;
+    const size_t xbytes = m->num_cols * sizeof(T);
+    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
+        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
+        attr[0].val.accessPolicyWindow.num_bytes = win;
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles));
+}
+
+template <typename T, int V>
+void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    int vid = variant_id();
+    if (vid < 0) {
+        // Default: persistent static-order tiles when there are no heavy
+        // groups (uniform tile work, e.g. stencils); otherwise hardware
+        // dispatch of independent tiles balances the irregular work better.
+        vid = m->num_heavy == 0 ? 0 : 6;
+    }
+    if constexpr (V == 4) {
+        if (m->max_tile_units <= uint64_t(kTileThreads) && (vid == 8 || vid == 9)) {
+            if (vid == 8) launch_pipe<T, 2>(m, a, s);
+            else launch_pipe<T, 4>(m, a, s);
+            return;
+        }
+    }
+    switch (vid) {
+        case 0: launch_lightp<T, V, 4, true, 4, false>(m, a, s); return;
+        case 10: launch_lightp<T, V, 4, false, 4, false>(m, a, s); return;
+        case 11: launch_lightp<T, V, 2, true, 6, false>(m, a, s); return;
+        case 12: launch_lightp<T, V, 4, true, 4, true>(m, a, s); return;
+        default: break;
+    }
+    switch (vid) {
+        case 1: launch_light<T, V, 2, true, 6>(m, a, s); break;
+        case 2: launch_light<T, V, 4, false, 4>(m, a, s); break;
+        case 3: launch_light<T, V, 4, true, 5>(m, a, s); break;
+        case 4: launch_light<T, V, 4, true, 3>(m, a, s); break;
+        case 5: launch_light<T, V, 8, true, 2>(m, a, s); break;
+        case 6: launch_light<T, V, 4, true, 4>(m, a, s); break;
+        case 7: launch_light<T, V, 2, true, 8>(m, a, s); break;
+        default: launch_light<T, V, 4, true, 4>(m, a, s); break;
+    }
+}
+
 template <typename T>
 void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint32_t ge, cudaStream_t s) {
+    SpmvArgs<T> a;
+    a.vals = static_cast<const T*>(m->values);
+    a.cols = m->columns;
+    a.groups = m->groups;
+    a.tm = static_cast<const uint16_t*>(m->tm);
+    a.assigned = static_cast<const uint16_t*>(m->assigned);
+    a.unit_base = m->unit_base;
+    a.tiles = m->tiles;
+    a.heavy = m->heavy;
+    a.heavy_ptr = m->heavy_ptr;
+    a.x = static_cast<const T*>(x);
+    a.y = static_cast<T*>(y);
+    a.tpg = m->tpg;
+    a.heavy_ctas = m->heavy_ctas;
+    a.g_begin = gb;
+    a.g_end = ge;
+    a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
+    a.max_tile_units = uint32_t(m->max_tile_units);
+    a.x_evict_last = env_flag("ARGCSR_XPOL", 1);
+    a.stream_evict_first = env_flag("ARGCSR_SPOL", m->num_heavy > 0 ? 1 : 0);
+
+    // Heavy groups run concurrently on the handle's auxiliary stream (forked
+    // from and joined back into `s`), launched first so their CTAs start first.
+    const bool fork = m->heavy_ctas > 0 && m->num_tiles > 0;
+    if (fork) {
+        CUDA_OK(cudaEventRecord(m->ev_fork, s));
+        CUDA_OK(cudaStreamWaitEvent(m->aux, m->ev_fork, 0));
+    }
+    if (m->heavy_ctas > 0) {
+        const size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
+        launch(spmv_heavy_kernel<T, 16>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
+    }
     switch (m->lanes_per_unit) {
-        case 4: launch_typed<T, uint16_t, 4>(m, x, y, gb, ge, s); break;
-        case 2: launch_typed<T, uint16_t, 2>(m, x, y, gb, ge, s); break;
-        default: launch_typed<T, uint16_t, 1>(m, x, y, gb, ge, s); break;
+        case 4: launch_v<T, 4>(m, a, s); break;
+        case 2: launch_v<T, 2>(m, a, s); break;
+        default: launch_v<T, 1>(m, a, s); break;
+    }
+    if (fork) {
+        CUDA_OK(cudaEventRecord(m->ev_join, m->aux));
+        CUDA_OK(cudaStreamWaitEvent(s, m->ev_join, 0));
     }
 }
 

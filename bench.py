@@ -46,6 +46,8 @@ def parse_args():
     p.add_argument("--no-variants", action="store_true", help="skip the tuned-dcs and cuSPARSE side runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-steps", type=int, default=20)
+    p.add_argument("--power-iteration", action="store_true",
+                   help="a step is one power-iteration step (SpMV, ||y|| all-reduce, all-gather, fused scaling)")
     return p.parse_args()
 
 
@@ -258,26 +260,30 @@ def run_b200(args):
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t
     nnz_total, rows_total, cols_total = A.nnz, A.num_rows, A.num_cols
-    if world > 1:
-        bounds = argcsr.partition_rows(A.row_pointers.cpu().numpy().view(np.uint64), world)
-        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-        S = A.slice_rows(r0, r1)
-    else:
-        bounds, r0, r1, S = None, 0, A.num_rows, A
-    vals = S.values.to(tdtype)
     stream = torch.cuda.Stream(dev)
     ce0, ce1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    D = None
     with torch.cuda.stream(stream):
         ce0.record(stream)
-        m = argcsr.argcsr_from_torch(S.num_rows, S.num_cols, S.row_pointers.contiguous(), S.columns.contiguous(),
-                                     vals.contiguous(), args.tpg, args.dcs, stream=stream)
+        if world > 1 or args.power_iteration:
+            # nnz-balanced row slices, each rank converts its own (multigpu.py)
+            from paper_1203_5737_b200.multigpu import DistributedArgCsr
+
+            D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.to(tdtype),
+                                  args.tpg, args.dcs, device=dev, dtype=tdtype)
+            m = D.engine.m
+            S = D.slice
+        else:
+            S = A
+            m = argcsr.argcsr_from_torch(A.num_rows, A.num_cols, A.row_pointers.contiguous(), A.columns.contiguous(),
+                                         A.values.to(tdtype).contiguous(), args.tpg, args.dcs, stream=stream)
         ce1.record(stream)
     torch.cuda.synchronize()
     conv_ms = ce0.elapsed_time(ce1)
 
     x = synthetic.bench_input(A.num_cols, dev, tdtype)
-    xg = torch.empty_like(x) if world > 1 else None
-    y = torch.empty(S.num_rows, dtype=tdtype, device=dev)
+    xg = torch.empty_like(x) if D is not None else None
+    y = torch.empty(m.num_rows, dtype=tdtype, device=dev)
 
     def spmv_fn(mm, xx, yy, s):
         mm.spmv_device(xx.data_ptr(), yy.data_ptr(), s.cuda_stream)
@@ -285,7 +291,7 @@ def run_b200(args):
     ab = alg_bytes(nnz_total, rows_total, cols_total, sv)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush_buf = None
-    working_set = m.total_slots * (sv + 4) + (S.num_rows + S.num_cols) * sv
+    working_set = m.total_slots * (sv + 4) + (m.num_rows + m.num_cols) * sv
     if working_set < 4 * l2:
         flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
 
@@ -295,7 +301,8 @@ def run_b200(args):
     # --------------------------------------------------- timed region
     sampler = ClockSampler(local)
     sampler.start()
-    if world == 1:
+    pi_lambda = None
+    if D is None:
         spmv_times = time_spmv(m, x, y, args.warmup, 0, stream, spmv_fn)  # warm-up pass
         sampler.mark_start()
         if flush_buf is None:
@@ -314,29 +321,29 @@ def run_b200(args):
             total_ms = sum(spmv_times)
             step_ms = total_ms / args.steps
         sampler.mark_end()
-        launches = args.steps
+        launches = args.steps * ((1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0))
     else:
-        counts = [int(bounds[p + 1] - bounds[p]) for p in range(world)]
-        uneven = len(set(counts)) > 1
         bufs = [x, xg]
-        cur = torch.cuda.current_stream(dev)
         it = [0]
+        pscale = torch.ones(1, dtype=torch.float64, device=dev)
+        ps2 = torch.zeros(1, dtype=torch.float64, device=dev)
 
         def step():
-            # y = A_p x_i on this rank's rows, then all-gather y into every
-            # rank's x_{i+1} (NCCL over NVLink), double-buffered x.
-            xin, xout = bufs[it[0] % 2], bufs[(it[0] + 1) % 2]
-            spmv_fn(m, xin, y, cur)
-            if uneven:
-                dist.all_gather(list(torch.split(xout, counts)), y)
+            # y = A_p x_i on this rank's rows, then the all-gather of y into
+            # every rank's x_{i+1} (NCCL over NVLink), double-buffered x;
+            # power iteration adds the 8-byte ||y||^2 all-reduce and the
+            # scaling fused into the next SpMV's gathers.
+            if args.power_iteration:
+                D.step(bufs[it[0] % 2], bufs[(it[0] + 1) % 2], pscale, ps2)
             else:
-                dist.all_gather_into_tensor(xout, y)
+                D.spmv_gather(bufs[it[0] % 2], bufs[(it[0] + 1) % 2])
             it[0] += 1
 
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
         sampler.mark_start()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -344,14 +351,18 @@ def run_b200(args):
             step()
         e1.record()
         torch.cuda.synchronize()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
         sampler.mark_end()
         total_ms = e0.elapsed_time(e1)
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        if world > 1:
+            t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
+        if args.power_iteration:
+            pi_lambda = float(torch.sqrt(ps2).item())
         step_ms = total_ms / args.steps
-        launches = args.steps
+        launches = args.steps * ((1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0))
     sampler.stop()
     clocks = sampler.summary()
 
@@ -387,8 +398,11 @@ def run_b200(args):
         "conversion_ms": round(conv_ms, 3), "generation_s": round(gen_s, 3), "format": info,
         "clocks": clocks, "gpu_launches": launches,
     }
+    if args.power_iteration:
+        out["power_iteration"] = {"steps_total": args.warmup + args.steps, "lambda": pi_lambda,
+                                  "step": "SpMV + ||y||^2 all-reduce + all-gather of y + scaling fused into the next SpMV"}
 
-    if world == 1:
+    if world == 1 and not args.power_iteration:
         # ------------------------------------------------ e2e through the C-ABI with host buffers
         xh = torch.empty(A.num_cols, dtype=tdtype, pin_memory=True)
         xh.copy_(x.cpu())

@@ -129,6 +129,13 @@ ARGCSR_API argcsr_status argcsr_dev_export(const argcsr_dev* m, uint64_t* groups
  * the reference (same per-chunk and per-row summation order, no FMA). */
 ARGCSR_API argcsr_status argcsr_dev_spmv(const argcsr_dev* m, const void* x, void* y, void* stream);
 
+/* y = A (s * x) with s = *x_scale, a DEVICE scalar read by the kernel (NULL:
+ * s = 1.0).  The scale is applied to every gathered x value (fl(s * x[c])),
+ * bit-identical to scaling x beforehand; the power iteration uses it to fuse
+ * the previous step's normalisation without a host round trip. */
+ARGCSR_API argcsr_status argcsr_dev_spmv_scaled(const argcsr_dev* m, const void* x, const double* x_scale, void* y,
+                                                void* stream);
+
 /* Group-range kernel (argcsr.hpp:114-116, argcsr.cpp:185-217): writes only the
  * rows of groups [group_begin, group_end); no length check, like the reference. */
 ARGCSR_API argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_t group_begin,

@@ -271,6 +271,13 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
                                        reinterpret_cast<void*>(stream)));
              },
              py::arg("x_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
+        .def("spmv_scaled_device",
+             [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uintptr_t y, std::uintptr_t stream) {
+                 check(argcsr_dev_spmv_scaled(p.dev->handle(), reinterpret_cast<const void*>(x),
+                                              reinterpret_cast<const double*>(scale), reinterpret_cast<void*>(y),
+                                              reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
         .def("spmv_groups_device",
              [](const PyArgCsr& p, std::uintptr_t x, std::uint64_t gb, std::uint64_t ge, std::uintptr_t y,
                 std::uintptr_t stream) {

@@ -253,6 +253,16 @@ argcsr_status argcsr_dev_spmv(const argcsr_dev* m, const void* x, void* y, void*
     });
 }
 
+argcsr_status argcsr_dev_spmv_scaled(const argcsr_dev* m, const void* x, const double* x_scale, void* y,
+                                     void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_scaled: null vector");
+        DeviceScope scope(m->device);
+        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, static_cast<cudaStream_t>(stream), x_scale);
+    });
+}
+
 argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_t group_begin, uint64_t group_end,
                                      void* y, void* stream) {
     return guarded([&] {

@@ -52,6 +52,7 @@ struct SpmvArgs {
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
     uint32_t max_tile_groups;
     uint32_t max_tile_units;
+    const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
 };
@@ -129,7 +130,7 @@ __device__ __forceinline__ double ld_x(const float* p, uint64_t pol) {
 // trailing, so "skip sentinel" == "stop at the first sentinel".
 template <typename T, int V, int U, bool PRED>
 __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, double (&s)[V],
-                                       uint64_t pol_stream, uint64_t pol_x) {
+                                       uint64_t pol_stream, uint64_t pol_x, double xs) {
 #pragma unroll
     for (int l = 0; l < V; ++l) s[l] = 0.0;
     const int32_t* cp = a.cols + slot0;
@@ -166,7 +167,8 @@ __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uin
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int l = 0; l < V; ++l) xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
+            for (int l = 0; l < V; ++l)
+                xv[u][l] = c[u][l] != -1 ? __dmul_rn(ld_x(a.x + c[u][l], pol_x), xs) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvA
     __shared__ uint32_t s_lane0[kTileThreads + 1], s_row0[kTileThreads + 1], s_g[kTileThreads];
     const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const double xs = a.x_scale ? *a.x_scale : 1.0;
     const uint32_t hb = a.heavy_ptr[blockIdx.x], he = a.heavy_ptr[blockIdx.x + 1];
     const uint32_t ng = he - hb;
     if (threadIdx.x == 0) {
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvA
         if (g < a.g_begin || g >= a.g_end) continue;
         const GroupDesc d = a.groups[g];
         double s[1];
-        phase1<T, 1, UH, false>(a, d.offset + (l - s_lane0[i]), d.chunk, s, pol_stream, pol_x);
+        phase1<T, 1, UH, false>(a, d.offset + (l - s_lane0[i]), d.chunk, s, pol_stream, pol_x, xs);
         s_part[l] = s[0];
     }
     __syncthreads();
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     double* s_part = reinterpret_cast<double*>(smem);
     const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const double xs = a.x_scale ? *a.x_scale : 1.0;
 
     const uint32_t kt = blockIdx.x;
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
         const uint32_t g = gs + gi;
         if (s_chunk[gi] > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
         double s[V];
-        phase1<T, V, U, PRED>(a, s_off[gi] + (u - s_ub[gi]) * V, s_chunk[gi], s, pol_stream, pol_x);
+        phase1<T, V, U, PRED>(a, s_off[gi] + (u - s_ub[gi]) * V, s_chunk[gi], s, pol_stream, pol_x, xs);
 #pragma unroll
         for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = s[l];
     }
@@ -378,6 +382,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_pipe_kernel(const SpmvAr
     auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
     const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const double xs = a.x_scale ? *a.x_scale : 1.0;
     const uint32_t tid = threadIdx.x;
 
     auto issue_meta = [&](uint32_t k, int b) {
@@ -477,7 +482,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_pipe_kernel(const SpmvAr
                 const int4 cc = in ? cs[q * kTileThreads] : make_int4(-1, -1, -1, -1);
                 c[q][0] = cc.x, c[q][1] = cc.y, c[q][2] = cc.z, c[q][3] = cc.w;
 #pragma unroll
-                for (int l = 0; l < 4; ++l) xv[q][l] = c[q][l] != -1 ? ld_x(a.x + c[q][l], pol_x) : 0.0;
+                for (int l = 0; l < 4; ++l)
+                    xv[q][l] = c[q][l] != -1 ? __dmul_rn(ld_x(a.x + c[q][l], pol_x), xs) : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < J; ++q) {
@@ -573,6 +579,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
     auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
     const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const double xs = a.x_scale ? *a.x_scale : 1.0;
     const uint32_t tid = threadIdx.x;
     auto issue_meta = [&](uint32_t gs, uint32_t ge, int b) {
         for (uint32_t i = tid; i <= ge - gs; i += blockDim.x) {
@@ -635,7 +642,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
             const GroupDesc d = md[gi];
             if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
             double sacc[V];
-            phase1<T, V, U, PRED>(a, d.offset + (ub0 + u - mub[gi]) * V, d.chunk, sacc, pol_stream, pol_x);
+            phase1<T, V, U, PRED>(a, d.offset + (ub0 + u - mub[gi]) * V, d.chunk, sacc, pol_stream, pol_x, xs);
 #pragma unroll
             for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = sacc[l];
         }
@@ -854,8 +861,10 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
 }
 
 template <typename T>
-void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint32_t ge, cudaStream_t s) {
+void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, void* y, uint32_t gb, uint32_t ge,
+                  cudaStream_t s) {
     SpmvArgs<T> a;
+    a.x_scale = x_scale;
     a.vals = static_cast<const T*>(m->values);
     a.cols = m->columns;
     a.groups = m->groups;
@@ -901,12 +910,12 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
 }  // namespace
 
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s) {
+                 cudaStream_t s, const double* x_scale) {
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
-    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, y, gb, ge, s);
-    else launch_dtype<float>(m, x, y, gb, ge, s);
+    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s);
+    else launch_dtype<float>(m, x, x_scale, y, gb, ge, s);
 }
 
 }  // namespace argcsr_gpu

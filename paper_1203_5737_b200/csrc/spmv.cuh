@@ -7,7 +7,10 @@ namespace argcsr_gpu {
 
 // y = A x for the rows of groups [group_begin, group_end); device pointers,
 // stream-ordered, no synchronisation.
+// y = A (s * x), s = *x_scale (a device scalar, read by the kernel; NULL:
+// 1.0).  The scale is applied per gather (fl(s * x[c])), bit-identical to
+// scaling x first; 1.0 is an exact no-op.
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s);
+                 cudaStream_t s, const double* x_scale = nullptr);
 
 }  // namespace argcsr_gpu

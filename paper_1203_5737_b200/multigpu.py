@@ -1,0 +1,174 @@
+"""Single-box multi-GPU layer: row-partitioned ARG-CSR.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch):
+
+* rows are split into contiguous, nnz-balanced ranges (argcsr_partition_rows:
+  r_p = lower_bound(row_pointers, p * nnz / P));
+* every rank converts ITS OWN slice on its own GPU (row pointers rebased to 0,
+  all columns kept), so slice p equals the reference argcsr_from_csr(slice_p)
+  bit-for-bit (group boundaries restart at each slice start);
+* x is replicated; a step is the local SpMV followed by the all-gather of the
+  y slices into every rank's next x.  With equal slices that is one
+  ncclAllGather straight into x; otherwise one broadcast per owner into its
+  row range of x (no padding, no compaction copy).
+
+The power iteration (config C5) is x_{k+1} = fl(y_k * fl(1 / ||y_k||_2)),
+y_k = A x_k.  The scaling of step k is fused into the gathers of SpMV k+1
+(argcsr_dev_spmv_scaled, bit-identical to scaling x first), and
+||y_k||^2 is one 8-byte all-reduce of the per-rank partial sums.
+
+The collectives and the per-rank engine are separable so the host logic runs
+on CPU with the gloo backend in tests (tests/test_multigpu_gloo.py), where a
+test-only engine (the oracle) stands in for the device.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def partition_bounds(row_pointers: np.ndarray, parts: int) -> np.ndarray:
+    """nnz-balanced contiguous row ranges (same rule as argcsr_partition_rows).
+
+    bounds[p] = lower_bound(rp, rp[0] + floor(nnz * p / parts)), clamped so
+    every part keeps at least one row when num_rows >= parts."""
+    rp = np.asarray(row_pointers, dtype=np.uint64)
+    n = rp.size - 1
+    nnz = int(rp[-1] - rp[0])
+    b = np.zeros(parts + 1, dtype=np.uint64)
+    for p in range(1, parts):
+        target = int(rp[0]) + (nnz * p) // parts
+        r = int(np.searchsorted(rp, np.uint64(target), side="left"))
+        lo = int(b[p - 1]) + (1 if n >= parts else 0)
+        hi = n - (parts - p) if n >= parts else n
+        b[p] = min(max(r, lo), hi)
+    b[parts] = n
+    return b
+
+
+@dataclass
+class CsrSlice:
+    """Rows [row_begin, row_end) of a CSR matrix, row pointers rebased to 0."""
+
+    row_begin: int
+    row_end: int
+    num_cols: int
+    row_pointers: np.ndarray | torch.Tensor
+    columns: np.ndarray | torch.Tensor
+    values: np.ndarray | torch.Tensor
+
+    @property
+    def num_rows(self) -> int:
+        return self.row_end - self.row_begin
+
+
+def slice_rows(row_pointers, columns, values, num_cols: int, r0: int, r1: int) -> CsrSlice:
+    a, b = int(row_pointers[r0]), int(row_pointers[r1])
+    return CsrSlice(r0, r1, num_cols, row_pointers[r0:r1 + 1] - row_pointers[r0], columns[a:b], values[a:b])
+
+
+class DeviceEngine:
+    """The product engine: this rank's slice converted and multiplied on its GPU."""
+
+    def __init__(self, sl: CsrSlice, tpg: int, dcs: int, device: torch.device, dtype=torch.float64):
+        import paper_1203_5737_b200 as argcsr
+
+        self.device = device
+        self.dtype = dtype
+        rp = torch.as_tensor(np.asarray(sl.row_pointers).astype(np.int64)) if isinstance(sl.row_pointers, np.ndarray) \
+            else sl.row_pointers.to(torch.int64)
+        cols = torch.as_tensor(sl.columns) if isinstance(sl.columns, np.ndarray) else sl.columns
+        vals = torch.as_tensor(sl.values) if isinstance(sl.values, np.ndarray) else sl.values
+        self.stream = torch.cuda.current_stream(device)
+        self.m = argcsr.argcsr_from_torch(sl.num_rows, sl.num_cols, rp.to(device).contiguous(),
+                                          cols.to(device, torch.int32).contiguous(),
+                                          vals.to(device, dtype).contiguous(), tpg, dcs, stream=self.stream)
+
+    def spmv(self, x: torch.Tensor, y: torch.Tensor, x_scale: Optional[torch.Tensor] = None) -> None:
+        """y = A (s * x), s = x_scale[0] read on the device (None: 1)."""
+        self.m.spmv_scaled_device(x.data_ptr(), 0 if x_scale is None else x_scale.data_ptr(), y.data_ptr(),
+                                  self.stream.cuda_stream)
+
+
+class DistributedArgCsr:
+    """A row-partitioned ARG-CSR matrix across the ranks of `group`
+    (world size 1 without torch.distributed)."""
+
+    def __init__(self, num_rows: int, num_cols: int, row_pointers, columns, values, tpg: int = 128, dcs: int = 1,
+                 group=None, device: Optional[torch.device] = None,
+                 engine_factory: Optional[Callable[[CsrSlice], object]] = None, dtype=torch.float64):
+        self.group = group
+        self.distributed = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.distributed else 1
+        self.rank = dist.get_rank(group) if self.distributed else 0
+        rp_host = row_pointers.cpu().numpy() if isinstance(row_pointers, torch.Tensor) else np.asarray(row_pointers)
+        self.bounds = partition_bounds(rp_host.astype(np.uint64), self.world)
+        self.counts = [int(self.bounds[p + 1] - self.bounds[p]) for p in range(self.world)]
+        self.num_rows, self.num_cols = num_rows, num_cols
+        r0, r1 = int(self.bounds[self.rank]), int(self.bounds[self.rank + 1])
+        self.slice = slice_rows(row_pointers, columns, values, num_cols, r0, r1)
+        self.nnz_local = int(self.slice.row_pointers[-1])
+        self.nnz_total = int(rp_host[-1] - rp_host[0])
+        if engine_factory is None:
+            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+            self.engine = DeviceEngine(self.slice, tpg, dcs, dev, dtype)
+        else:
+            self.engine = engine_factory(self.slice)
+        self.device = self.engine.device
+        self.dtype = dtype
+        self.y = torch.empty(self.slice.num_rows, dtype=dtype, device=self.device)
+
+    # ------------------------------------------------------------ collectives
+    def gather(self, y_local: torch.Tensor, x_full: torch.Tensor) -> None:
+        """All-gather the y slices into x_full (every rank)."""
+        if self.world == 1:
+            x_full.copy_(y_local)
+            return
+        if len(set(self.counts)) == 1:
+            dist.all_gather_into_tensor(x_full, y_local, group=self.group)
+            return
+        off = 0
+        for p, n in enumerate(self.counts):
+            seg = x_full[off:off + n]
+            if p == self.rank:
+                seg.copy_(y_local)
+            dist.broadcast(seg, src=dist.get_global_rank(self.group, p) if self.group is not None else p,
+                           group=self.group)
+            off += n
+
+    def allreduce_sum(self, v: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
+        return v
+
+    # ------------------------------------------------------------------ steps
+    def spmv_gather(self, x_full: torch.Tensor, out_full: torch.Tensor, x_scale: Optional[torch.Tensor] = None) -> None:
+        """out = A (x_scale * x) assembled on every rank (iterated-SpMV step)."""
+        self.engine.spmv(x_full, self.y, x_scale)
+        self.gather(self.y, out_full)
+
+    def power_iteration(self, x0: torch.Tensor, iters: int):
+        """`iters` steps of x <- A x / ||A x||; returns (lambda, x) with
+        lambda = ||A x_{iters-1}|| (x normalised), on every rank."""
+        buf = [x0.clone(), torch.empty_like(x0)]
+        scale = torch.ones(1, dtype=torch.float64, device=self.device)
+        s2 = torch.zeros(1, dtype=torch.float64, device=self.device)
+        for k in range(iters):
+            self.step(buf[k % 2], buf[(k + 1) % 2], scale, s2)
+        lam = float(torch.sqrt(s2).item())  # the only host synchronisation
+        x = buf[iters % 2] * scale  # materialise the last normalisation
+        return lam, x
+
+    def step(self, xin: torch.Tensor, xout: torch.Tensor, scale: torch.Tensor, s2: torch.Tensor) -> None:
+        """One power-iteration step, device-side only: y = A (scale * xin);
+        s2 = ||y||^2 (all-reduced); xout = all-gather(y); scale = 1/sqrt(s2)."""
+        self.engine.spmv(xin, self.y, scale)
+        y64 = self.y.to(torch.float64)
+        s2.copy_(torch.dot(y64, y64).reshape(1))
+        self.allreduce_sum(s2)
+        self.gather(self.y, xout)
+        torch.reciprocal(torch.sqrt(s2), out=scale)

@@ -1,0 +1,39 @@
+"""The multi-GPU layer on the device path (world size 1 on one B200): the
+fused normalisation of argcsr_dev_spmv_scaled is bit-identical to scaling x
+first, and the power iteration matches the single-process CPU run."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import bits, stencil27
+from test_multigpu_gloo import reference_power_iteration
+
+pytestmark = pytest.mark.gpu
+
+
+def test_fused_scale_is_bit_identical(argcsr, orc):
+    A = stencil27(16)
+    m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1)
+    x = torch.linspace(-3, 3, A.num_cols, dtype=torch.float64, device="cuda")
+    s = torch.tensor([1.0 / 7.3], dtype=torch.float64, device="cuda")
+    y1 = torch.empty(A.num_rows, dtype=torch.float64, device="cuda")
+    m.spmv_scaled_device(x.data_ptr(), s.data_ptr(), y1.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    y2 = argcsr.spmv_torch(m, x * s)
+    assert bits(y1.cpu().numpy()) == bits(y2.cpu().numpy())
+    ref = orc.spmv_argcsr(orc.argcsr_from_csr(A, 128, 1), (x * s).cpu().numpy())
+    assert bits(y1.cpu().numpy()) == bits(ref)
+
+
+@pytest.mark.parametrize("tpg,dcs", [(128, 1), (128, 32)])
+def test_power_iteration_single_rank(tpg, dcs):
+    import oracle
+    from paper_1203_5737_b200.multigpu import DistributedArgCsr
+
+    A = stencil27(20)
+    D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values, tpg, dcs,
+                          device=torch.device("cuda", 0))
+    x0 = oracle.bench_input(A.num_cols)
+    lam, x = D.power_iteration(torch.from_numpy(x0).cuda(), 30)
+    lam_ref, x_ref = reference_power_iteration(A, x0, 30, tpg, dcs)
+    assert abs(lam - lam_ref) <= 1e-10 * abs(lam_ref)
+    assert np.max(np.abs(x.cpu().numpy() - x_ref)) <= 1e-9

@@ -168,7 +168,13 @@ __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uin
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int l = 0; l < V; ++l)
-                xv[u][l] = c[u][l] != -1 ? __dmul_rn(ld_x(a.x + c[u][l], pol_x), xs) : 0.0;
+                xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
+        if (a.x_scale) {  // uniform: fused normalisation of the power iteration
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int l = 0; l < V; ++l) xv[u][l] = __dmul_rn(xv[u][l], xs);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -829,10 +835,10 @@ template <typename T, int V>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     int vid = variant_id();
     if (vid < 0) {
-        // Default: persistent static-order tiles when there are no heavy
-        // groups (uniform tile work, e.g. stencils); otherwise hardware
-        // dispatch of independent tiles balances the irregular work better.
-        vid = m->num_heavy == 0 ? 0 : 6;
+        // Default: persistent CTAs with prefetched metadata and dynamic tile
+        // order when there are no heavy groups (e.g. stencils); otherwise
+        // hardware dispatch of independent tiles (measured best for R-MAT).
+        vid = m->num_heavy == 0 ? 12 : 6;
     }
     if constexpr (V == 4) {
         if (m->max_tile_units <= uint64_t(kTileThreads) && (vid == 8 || vid == 9)) {

@@ -78,6 +78,7 @@ struct argcsr_dev {
     uint64_t heavy_max_lanes = 0;         // lanes of the fullest heavy CTA
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
     uint64_t tile_span = 0;               // units between consecutive tile keys
+    uint32_t tile_threads = 256;          // tiles were built for this CTA size
     uint64_t max_tile_units = 0;          // tile_span + ceil(tpg / V) - 1
 
     // Heavy groups run on an auxiliary stream forked from the caller's stream.

@@ -12,6 +12,7 @@
 //
 // plus the SpMV schedule (light tiles, heavy groups in LPT order).
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -410,6 +411,14 @@ __global__ void __launch_bounds__(256) k5_layout(const uint64_t* __restrict__ rp
     }
 }
 
+// Units per light tile (= threads of the one-unit-per-thread SpMV kernels).
+// ARGCSR_TILE_THREADS=128 builds smaller tiles for the slab-pipelined kernel.
+uint64_t tile_threads_setting() {
+    const char* e = std::getenv("ARGCSR_TILE_THREADS");
+    const long v = e ? std::atol(e) : 0;
+    return (v == 128 || v == 256) ? uint64_t(v) : uint64_t(kTileThreads);
+}
+
 unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
     const uint64_t b = (n + block - 1) / block;
     return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, cap)));
@@ -563,8 +572,10 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     // Tile keys every `span` units so that a tile (span + at most one group's
     // units - 1) fits one CTA pass when a group has at most half a CTA of units.
     const uint64_t maxu = (tpg + V - 1) / V;
-    const uint64_t span = maxu <= uint64_t(kTileThreads) / 2 ? uint64_t(kTileThreads) - maxu + 1 : uint64_t(kTileThreads);
+    const uint64_t tt = tile_threads_setting();
+    const uint64_t span = maxu <= tt / 2 ? tt - maxu + 1 : tt;
     m->tile_span = span;
+    m->tile_threads = uint32_t(tt);
     const uint64_t ntiles = (total_units + span - 1) / span;
     if (ntiles > 0x7fffffffull) fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: matrix too large for the tile schedule");
     m->num_tiles = uint32_t(ntiles);

@@ -130,13 +130,15 @@ __device__ __forceinline__ double ld_x(const float* p, uint64_t pol) {
 // trailing, so "skip sentinel" == "stop at the first sentinel".
 template <typename T, int V, int U, bool PRED>
 __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, double (&s)[V],
-                                       uint64_t pol_stream, uint64_t pol_x, double xs) {
+                                       uint64_t pol_stream, uint64_t pol_x, double xs, uint32_t jstart = 0) {
+    if (jstart == 0) {
 #pragma unroll
-    for (int l = 0; l < V; ++l) s[l] = 0.0;
+        for (int l = 0; l < V; ++l) s[l] = 0.0;
+    }
     const int32_t* cp = a.cols + slot0;
     const T* vp = a.vals + slot0;
     const uint64_t tpg = a.tpg;
-    for (uint32_t j0 = 0; j0 < chunk; j0 += U) {
+    for (uint32_t j0 = jstart; j0 < chunk; j0 += U) {
         int c[U][V];
         T v[U][V];
 #pragma unroll
@@ -691,6 +693,174 @@ size_t lightp_smem_bytes(const argcsr_dev* m, int V) {
 template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
 void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s);
 
+// ------------------------------------------- cross-tile slab pipeline (V = 4)
+// Persistent CTAs of B threads walk tiles k, k+G, ... (one 4-lane unit per
+// thread).  At the top of tile k every thread issues cp.async copies of the
+// first J element steps of ITS unit in tile k+G into private shared-memory
+// slots, and the group metadata of tile k+2G into a third buffer; then it
+// consumes tile k (whose slab was issued one tile earlier).  The HBM stream of
+// the next tile is thus in flight during the whole x-gather / reduction phase
+// of the current one, at no register cost.  Steps beyond J (chunk > J) load
+// directly like spmv_light_kernel.
+template <typename T, int J, int B>
+__global__ void __launch_bounds__(B) spmv_pipex_kernel(const SpmvArgs<T> a, uint32_t num_tiles) {
+    constexpr int VB = 4 * sizeof(T);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t cap = a.max_tile_groups;
+    int4* s_cols = reinterpret_cast<int4*>(smem);                  // [2][J][B]
+    unsigned char* s_vals = smem + size_t(2) * J * B * sizeof(int4);  // [2][J][B][VB]
+    double* s_part = reinterpret_cast<double*>(s_vals + size_t(2) * J * B * VB);  // [B][4]
+    unsigned char* mbase = reinterpret_cast<unsigned char*>(s_part + B * 4);
+    const size_t meta_bytes = ((size_t(cap) + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15);
+    auto meta_desc = [&](int b) { return reinterpret_cast<GroupDesc*>(mbase + b * meta_bytes); };
+    auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
+    const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const double xs = a.x_scale ? *a.x_scale : 1.0;
+    const uint32_t tid = threadIdx.x;
+
+    auto issue_meta = [&](uint32_t k, int b) {
+        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
+        for (uint32_t i = tid; i <= ge - gs; i += B) {
+            cp_async16(smem_u32(meta_desc(b) + i), a.groups + gs + i, pol_x);
+            cp_async8(smem_u32(meta_ub(b) + i), a.unit_base + gs + i);
+        }
+    };
+    auto unit_of = [&](uint32_t k, int b, PipeUnit<T>& pu) -> bool {
+        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
+        const uint32_t ng = ge - gs;
+        pu = PipeUnit<T>{};
+        const uint64_t* ub = meta_ub(b);
+        if (ng == 0 || ge <= a.g_begin || gs >= a.g_end) return false;
+        const uint64_t u = ub[0] + tid;
+        if (u >= ub[ng]) return false;
+        const uint32_t gi = find_le64(ub, ng, u);
+        const GroupDesc d = meta_desc(b)[gi];
+        const uint32_t g = gs + gi;
+        if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) return false;
+        pu.slot0 = d.offset + (u - ub[gi]) * 4;
+        pu.chunk = d.chunk;
+        return true;
+    };
+    auto issue_slab = [&](const PipeUnit<T>& pu, int buf) {
+#pragma unroll
+        for (int q = 0; q < J; ++q) {
+            if (uint32_t(q) < pu.chunk) {
+                const uint64_t slot = pu.slot0 + uint64_t(q) * a.tpg;
+                cp_async16(smem_u32(s_cols + (size_t(buf) * J + q) * B + tid), a.cols + slot, pol);
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(a.vals + slot);
+                unsigned char* dst = s_vals + ((size_t(buf) * J + q) * B + tid) * VB;
+#pragma unroll
+                for (int h = 0; h < VB; h += 16) cp_async16(smem_u32(dst + h), src + h, pol);
+            }
+        }
+    };
+
+    uint32_t k = blockIdx.x;
+    if (k >= num_tiles) return;
+    issue_meta(k, 0);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+    uint32_t kn = k + gridDim.x;
+    if (kn < num_tiles) issue_meta(kn, 1);
+    PipeUnit<T> pu;
+    bool have = unit_of(k, 0, pu);
+    if (have) issue_slab(pu, 0);
+    cp_commit();
+    for (uint32_t it = 0;; ++it) {
+        const int mc = it % 3, mn = (it + 1) % 3, m2 = (it + 2) % 3, sc = it & 1;
+        cp_wait<0>();  // slab of tile k and metadata of tile k+G (both issued one tile ago)
+        __syncthreads();
+        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
+        const uint32_t ng = ge - gs;
+        const GroupDesc* md = meta_desc(mc);
+        const uint64_t* mub = meta_ub(mc);
+        const bool live = ng > 0 && !(ge <= a.g_begin || gs >= a.g_end);
+        const uint64_t ub0 = mub[0];
+        const uint32_t row0 = md[0].first_row, row_end = live ? md[ng].first_row : row0;
+
+        // next tile's first slab and the metadata two tiles ahead
+        PipeUnit<T> pn;
+        bool have_n = false;
+        if (kn < num_tiles) {
+            have_n = unit_of(kn, mn, pn);
+            if (have_n) issue_slab(pn, sc ^ 1);
+            const uint32_t k2 = kn + gridDim.x;
+            if (k2 < num_tiles) issue_meta(k2, m2);
+        }
+        cp_commit();
+
+        // phase-2 metadata of this thread's first row (registers)
+        const uint32_t pr = row0 + tid;
+        uint32_t pgi = 0, pb = 0, pe = 0;
+        bool pvalid = false;
+        if (pr < row_end) {
+            pgi = find_row(md, ng, pr);
+            const uint32_t g = gs + pgi;
+            pvalid = md[pgi].chunk <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
+            if (pvalid) {
+                pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
+                pe = uint32_t(a.tm[pr]);
+            }
+        }
+
+        // phase 1: the first J steps from the slab, the rest straight from HBM
+        if (have) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            int c[J][4];
+            double xv[J][4];
+#pragma unroll
+            for (int q = 0; q < J; ++q) {
+                const bool in = uint32_t(q) < pu.chunk;
+                const int4 cc = in ? s_cols[(size_t(sc) * J + q) * B + tid] : make_int4(-1, -1, -1, -1);
+                c[q][0] = cc.x, c[q][1] = cc.y, c[q][2] = cc.z, c[q][3] = cc.w;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) xv[q][l] = c[q][l] != -1 ? ld_x(a.x + c[q][l], pol_x) : 0.0;
+            }
+            if (a.x_scale) {
+#pragma unroll
+                for (int q = 0; q < J; ++q)
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) xv[q][l] = __dmul_rn(xv[q][l], xs);
+            }
+#pragma unroll
+            for (int q = 0; q < J; ++q) {
+                const T* vv = reinterpret_cast<const T*>(s_vals + ((size_t(sc) * J + q) * B + tid) * VB);
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    if (c[q][l] != -1) acc[l] = __dadd_rn(acc[l], __dmul_rn(double(vv[l]), xv[q][l]));
+            }
+            const bool more = pu.chunk > uint32_t(J) && (c[J - 1][0] & c[J - 1][1] & c[J - 1][2] & c[J - 1][3]) != -1;
+            if (more) phase1<T, 4, J, true>(a, pu.slot0, pu.chunk, acc, pol, pol_x, xs, uint32_t(J));
+#pragma unroll
+            for (int l = 0; l < 4; ++l) s_part[size_t(tid) * 4 + l] = acc[l];
+        }
+        __syncthreads();
+
+        if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(mub[pgi] - ub0) * 4, pb, pe));
+        for (uint32_t r = pr + B; r < row_end; r += B) {
+            const uint32_t gi = find_row(md, ng, r);
+            const uint32_t g = gs + gi;
+            if (md[gi].chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+            const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
+            a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[gi] - ub0) * 4, b, uint32_t(a.tm[r])));
+        }
+        if (kn >= num_tiles) break;
+        k = kn;
+        kn = k + gridDim.x;
+        pu = pn;
+        have = have_n;
+    }
+    cp_wait<0>();
+}
+
+size_t pipex_smem_bytes(const argcsr_dev* m, int J, int B, size_t tbytes) {
+    const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
+    return size_t(2) * J * B * (16 + 4 * tbytes) + size_t(B) * 4 * sizeof(double) +
+           3 * (((cap + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15));
+}
+
 size_t pipe_smem_bytes(const argcsr_dev* m, int J, size_t tbytes) {
     const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
     return size_t(2) * J * kTileThreads * (16 + 4 * tbytes) + size_t(kTileThreads) * 4 * sizeof(double) +
@@ -715,10 +885,10 @@ bool l2_window_enabled() {
 int variant_id() {
     static const int id = [] {
         const char* e = std::getenv("ARGCSR_SPMV_VARIANT");
-        if (!e) return 0;
+        if (!e) return -1;
         const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
-                               "PIPE2", "PIPE4", "LP4P0B4", "LP2P1B6", "LPD4P1B4"};
-        for (int i = 0; i < 13; ++i)
+                               "PIPE2", "PIPE4", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "PX4", "PX2"};
+        for (int i = 0; i < 15; ++i)
             if (!std::strcmp(e, names[i])) return i;
         return -1;
     }();
@@ -797,6 +967,40 @@ void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles, m->sched));
 }
 
+template <typename T, int J, int B>
+void launch_pipex(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = pipex_smem_bytes(m, J, B, sizeof(T));
+    auto kern = spmv_pipex_kernel<T, J, B>;
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, smem));
+    const unsigned grid = unsigned(std::min<uint64_t>(m->num_tiles, uint64_t(std::max(per_sm, 1)) * sms));
+    if (grid == 0) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(B);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.numAttrs = 0;
+    const size_t xbytes = m->num_cols * sizeof(T);
+    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
+        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
+        attr[0].val.accessPolicyWindow.num_bytes = win;
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles));
+}
+
 template <typename T, int J>
 void launch_pipe(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     int dev = 0, sms = 0;
@@ -841,6 +1045,19 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
         vid = m->num_heavy == 0 ? 12 : 6;
     }
     if constexpr (V == 4) {
+        if (vid == 13 || vid == 14) {
+            // one unit per thread: tiles must have been built for the CTA size
+            if (m->tile_threads == 128 && m->max_tile_units <= 128) {
+                if (vid == 13) launch_pipex<T, 4, 128>(m, a, s);
+                else launch_pipex<T, 2, 128>(m, a, s);
+                return;
+            }
+            if (m->max_tile_units <= 256) {
+                if (vid == 13) launch_pipex<T, 4, 256>(m, a, s);
+                else launch_pipex<T, 2, 256>(m, a, s);
+                return;
+            }
+        }
         if (m->max_tile_units <= uint64_t(kTileThreads) && (vid == 8 || vid == 9)) {
             if (vid == 8) launch_pipe<T, 2>(m, a, s);
             else launch_pipe<T, 4>(m, a, s);

@@ -40,7 +40,7 @@ try:
 except ImportError as exc:  # fail loudly: the product path is native only
     raise ImportError(
         "paper_1203_5737_b200: native extension missing; build it with "
-        "`python -m paper_1203_5737_b200._build` (or __graft_entry__.build())"
+        "`python paper_1203_5737_b200/_build.py` (or __graft_entry__.build())"
     ) from exc
 
 CsrMatrix = _ext.CsrMatrix

@@ -8,7 +8,16 @@ if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
 
+def _ensure_built():
+    """Build the in-tree native pieces if a fresh checkout lacks them (no-op
+    when up to date); same entry the driver uses."""
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
 def pytest_configure(config):
+    _ensure_built()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); parity tests through the C-ABI")
     config.addinivalue_line("markers", "slow: full-size BASELINE configurations")
 

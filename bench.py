@@ -43,6 +43,8 @@ def parse_args():
     p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C4f32", "C5"])
     p.add_argument("--tpg", type=int, default=128)
     p.add_argument("--dcs", type=int, default=1)
+    p.add_argument("--layout", default="compact", choices=["compact", "reference"],
+                   help="device storage of the value/column blocks (include/argcsr_gpu.h ARGCSR_LAYOUT_REFERENCE)")
     p.add_argument("--no-variants", action="store_true", help="skip the tuned-dcs and cuSPARSE side runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-steps", type=int, default=20)
@@ -270,13 +272,14 @@ def run_b200(args):
             from paper_1203_5737_b200.multigpu import DistributedArgCsr
 
             D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.to(tdtype),
-                                  args.tpg, args.dcs, device=dev, dtype=tdtype)
+                                  args.tpg, args.dcs, device=dev, dtype=tdtype, layout=args.layout)
             m = D.engine.m
             S = D.slice
         else:
             S = A
             m = argcsr.argcsr_from_torch(A.num_rows, A.num_cols, A.row_pointers.contiguous(), A.columns.contiguous(),
-                                         A.values.to(tdtype).contiguous(), args.tpg, args.dcs, stream=stream)
+                                         A.values.to(tdtype).contiguous(), args.tpg, args.dcs, stream=stream,
+                                         layout=args.layout)
         ce1.record(stream)
     torch.cuda.synchronize()
     conv_ms = ce0.elapsed_time(ce1)
@@ -291,7 +294,7 @@ def run_b200(args):
     ab = alg_bytes(nnz_total, rows_total, cols_total, sv)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush_buf = None
-    working_set = m.total_slots * (sv + 4) + (m.num_rows + m.num_cols) * sv
+    working_set = m.stored_slots * (sv + 4) + (m.num_rows + m.num_cols) * sv
     if working_set < 4 * l2:
         flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
 
@@ -375,10 +378,11 @@ def run_b200(args):
         return
 
     peak, peak_src = measured_peak()
-    info = {"groups": m.num_groups, "total_slots": m.total_slots, "heavy_groups": m.heavy_groups,
+    info = {"layout": m.layout, "groups": m.num_groups, "total_slots": m.total_slots,
+            "stored_slots": m.stored_slots, "heavy_groups": m.heavy_groups,
             "light_tiles": m.light_tiles, "max_chunk": m.max_chunk_size, "device_bytes": m.device_bytes,
             "heavy_ctas": m.heavy_ctas, "l2_persist_bytes": m.l2_persist_bytes}
-    key = f"{args.config}_tpg{args.tpg}_dcs{args.dcs}"
+    key = f"{args.config}_tpg{args.tpg}_dcs{args.dcs}_{args.layout}"
     traffic = traffic_from_profiles(key)
     out = {
         "metric": "SpMV GFLOP/s", "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world,
@@ -386,8 +390,9 @@ def run_b200(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if sv == 8 else "f32", "data": "synthetic",
         "config": {"workload": args.config, "matrix": A.name, "desc": cfg["desc"], "rows": rows_total,
                    "nnz": nnz_total, "threads_per_group": args.tpg, "desired_chunk_size": args.dcs,
+                   "layout": args.layout,
                    "l2": ("flushed between steps (working set < 4x L2)" if flush_buf is not None else
-                          f"inputs larger than L2 (ARG-CSR arrays {m.total_slots * (sv + 4) / 1e9:.2f} GB); "
+                          f"inputs larger than L2 (ARG-CSR arrays {m.stored_slots * (sv + 4) / 1e9:.2f} GB); "
                           "x kept L2-resident by design (access-policy window)"),
                    "parallelism": f"rows nnz-balanced over {world} GPU(s)" if world > 1 else "single GPU"},
         "eff_GBps": round(eff_gbs, 1), "pct_of_8TBps": round(100 * eff_gbs / NOMINAL_HBM_GBS, 2),
@@ -443,14 +448,16 @@ def variants(args, A, x, tdtype, sv, stream, spmv_fn):
     res = []
     ab = alg_bytes(A.nnz, A.num_rows, A.num_cols, sv)
     y = torch.empty(A.num_rows, dtype=tdtype, device=x.device)
-    for dcs in sorted({32, 4} - {args.dcs}):
+    other = "reference" if args.layout == "compact" else "compact"
+    runs = [(args.dcs, other)] + [(d, args.layout) for d in sorted({32, 4} - {args.dcs})]
+    for dcs, layout in runs:
         m2 = argcsr.argcsr_from_torch(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.to(tdtype),
-                                      args.tpg, dcs, stream=stream)
+                                      args.tpg, dcs, stream=stream, layout=layout)
         ts = time_spmv(m2, x, y, min(args.steps, 100), args.warmup, stream, spmv_fn)
         ms = statistics.median(ts)
         res.append({"impl": "argcsr_b200", "threads_per_group": args.tpg, "desired_chunk_size": dcs,
-                    "ms": ms, "gflops": 2 * A.nnz / ms / 1e6, "eff_GBps": ab / ms / 1e6,
-                    "total_slots": m2.total_slots, "groups": m2.num_groups})
+                    "layout": layout, "ms": ms, "gflops": 2 * A.nnz / ms / 1e6, "eff_GBps": ab / ms / 1e6,
+                    "total_slots": m2.total_slots, "stored_slots": m2.stored_slots, "groups": m2.num_groups})
         m2.free()
         del m2
     try:

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define ARGCSR_GPU_ABI_VERSION 1
+#define ARGCSR_GPU_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ARGCSR_API __attribute__((visibility("default")))
@@ -87,6 +87,7 @@ typedef struct {
     uint64_t desired_chunk_size;
     uint64_t num_groups;       /* ArgCsrMatrix::groups.size() */
     uint64_t total_slots;      /* ArgCsrMatrix::total_slots() (argcsr.hpp:61) */
+    uint64_t stored_slots;     /* slots held on the device (== total_slots in the reference layout) */
     uint64_t nnz;              /* explicit entries */
     uint64_t heavy_groups;     /* groups scheduled on the long-chunk path */
     uint64_t heavy_ctas;       /* CTAs the heavy groups are packed into */
@@ -96,7 +97,19 @@ typedef struct {
     uint64_t l2_persist_bytes; /* persisting-L2 carve-out available to the x window */
     int32_t device;
     argcsr_dtype dtype;
+    uint32_t layout;           /* 0 = lane-compact (default), ARGCSR_LAYOUT_REFERENCE */
 } argcsr_dev_info_t;
+
+/* Device layout of the value/column blocks (argcsr_dev_convert_ex flags).
+ * Default (0): lane-compact -- each group's block is stored with a lane stride
+ * of its assigned threads rounded up to the SpMV vector width instead of
+ * threads_per_group, so the free lanes the reference pads with (0.0, -1) are
+ * not stored and the SpMV streams the matrix contiguously.  Groups, chunk
+ * order, threads_mapping and every exported array are unchanged (export
+ * re-expands to the reference layout bit-exactly).
+ * ARGCSR_LAYOUT_REFERENCE: keep the reference arrays verbatim on the device
+ * (stride threads_per_group, argcsr.cpp:99-104). */
+#define ARGCSR_LAYOUT_REFERENCE 1u
 
 /* ---------------------------------------------------------------- conversion */
 
@@ -109,6 +122,12 @@ typedef struct {
 ARGCSR_API argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t threads_per_group,
                                  uint64_t desired_chunk_size, int device, void* stream,
                                  argcsr_dev** out);
+
+/* argcsr_dev_convert with layout flags (0 or ARGCSR_LAYOUT_REFERENCE);
+ * argcsr_dev_convert(...) == argcsr_dev_convert_ex(..., 0, out). */
+ARGCSR_API argcsr_status argcsr_dev_convert_ex(const argcsr_csr_view* csr, uint64_t threads_per_group,
+                                    uint64_t desired_chunk_size, int device, void* stream, uint32_t flags,
+                                    argcsr_dev** out);
 
 ARGCSR_API argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info);
 

@@ -62,29 +62,47 @@ partition_rows = _ext.partition_rows
 abi_version = _ext.abi_version
 
 
+LAYOUTS = {"compact": 0, "reference": 1}  # argcsr_dev_convert_ex flags (include/argcsr_gpu.h)
+
+
+def _layout_flags(layout: str) -> int:
+    try:
+        return LAYOUTS[layout]
+    except KeyError:
+        raise ParameterError(f"argcsr_from_csr: layout must be one of {sorted(LAYOUTS)}") from None
+
+
 def argcsr_from_csr(matrix, threads_per_group: int = kDefaultThreadsPerGroup,
-                    desired_chunk_size: int = kDefaultDesiredChunkSize, device: int = 0) -> ArgCsrMatrix:
+                    desired_chunk_size: int = kDefaultDesiredChunkSize, device: int = 0,
+                    layout: str = "compact") -> ArgCsrMatrix:
     """argcsr_from_csr (argcsr.hpp:101-104) on the GPU.
 
     `matrix` is a CsrMatrix, or a tuple (num_rows, num_cols, row_pointers,
     columns, values) of numpy arrays (float32 values give an fp32 handle), or
-    a dict of torch CUDA tensors (see argcsr_from_torch).
+    a dict of torch CUDA tensors (see argcsr_from_torch).  `layout` picks the
+    device storage of the value/column blocks: "compact" (free lanes not
+    stored, the default) or "reference" (the reference arrays verbatim); the
+    exported arrays and every SpMV result are identical either way.
     """
+    flags = _layout_flags(layout)
     if isinstance(matrix, CsrMatrix):
-        return _ext.argcsr_from_csr(matrix, threads_per_group, desired_chunk_size, device)
+        return _ext.argcsr_from_csr(matrix, threads_per_group, desired_chunk_size, device, flags)
     if isinstance(matrix, tuple) and len(matrix) == 5:
         nr, nc, rp, cols, vals = matrix
-        return _ext.argcsr_from_csr_arrays(nr, nc, rp, cols, vals, threads_per_group, desired_chunk_size, device)
+        return _ext.argcsr_from_csr_arrays(nr, nc, rp, cols, vals, threads_per_group, desired_chunk_size, device,
+                                           flags)
     raise ParameterError("argcsr_from_csr: expected a CsrMatrix or (num_rows, num_cols, rp, cols, vals)")
 
 
 def argcsr_from_torch(num_rows: int, num_cols: int, row_pointers, columns, values,
                       threads_per_group: int = kDefaultThreadsPerGroup,
-                      desired_chunk_size: int = kDefaultDesiredChunkSize, stream=None) -> ArgCsrMatrix:
+                      desired_chunk_size: int = kDefaultDesiredChunkSize, stream=None,
+                      layout: str = "compact") -> ArgCsrMatrix:
     """Convert a device-resident CSR given as torch CUDA tensors (int64 row
     pointers, int32 columns, float64/float32 values) on the current stream."""
     import torch
 
+    flags = _layout_flags(layout)
     if not (row_pointers.is_cuda and columns.is_cuda and values.is_cuda):
         raise ParameterError("argcsr_from_torch: tensors must be CUDA tensors")
     if row_pointers.dtype != torch.int64 or columns.dtype != torch.int32:
@@ -98,7 +116,7 @@ def argcsr_from_torch(num_rows: int, num_cols: int, row_pointers, columns, value
     dtype = "float64" if values.dtype == torch.float64 else "float32"
     return _ext.argcsr_from_device_csr(
         num_rows, num_cols, values.numel(), row_pointers.contiguous().data_ptr(), columns.contiguous().data_ptr(),
-        values.contiguous().data_ptr(), dtype, threads_per_group, desired_chunk_size, dev, s.cuda_stream)
+        values.contiguous().data_ptr(), dtype, threads_per_group, desired_chunk_size, dev, s.cuda_stream, flags)
 
 
 def spmv(matrix: ArgCsrMatrix, x):

@@ -106,7 +106,7 @@ PyArgCsr make_handle(argcsr_dev* h) {
 }
 
 PyArgCsr convert_arrays(std::size_t num_rows, std::size_t num_cols, py::array row_pointers, py::array columns,
-                        py::array values, std::size_t tpg, std::size_t dcs, int device) {
+                        py::array values, std::size_t tpg, std::size_t dcs, int device, std::uint32_t flags) {
     auto rp = py::array_t<uint64_t, py::array::c_style | py::array::forcecast>(row_pointers);
     auto cl = py::array_t<int32_t, py::array::c_style | py::array::forcecast>(columns);
     argcsr_csr_view v{};
@@ -131,7 +131,7 @@ PyArgCsr convert_arrays(std::size_t num_rows, std::size_t num_cols, py::array ro
     argcsr_dev* h = nullptr;
     {
         py::gil_scoped_release nogil;
-        check(argcsr_dev_convert(&v, tpg, dcs, device, nullptr, &h));
+        check(argcsr_dev_convert_ex(&v, tpg, dcs, device, nullptr, flags, &h));
     }
     return make_handle(h);
 }
@@ -228,6 +228,10 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         .def_property_readonly("threads_per_group", [](const PyArgCsr& p) { return p.info().threads_per_group; })
         .def_property_readonly("desired_chunk_size", [](const PyArgCsr& p) { return p.info().desired_chunk_size; })
         .def_property_readonly("total_slots", [](const PyArgCsr& p) { return p.info().total_slots; })
+        .def_property_readonly("stored_slots", [](const PyArgCsr& p) { return p.info().stored_slots; })
+        .def_property_readonly("layout", [](const PyArgCsr& p) {
+            return p.info().layout == ARGCSR_LAYOUT_REFERENCE ? "reference" : "compact";
+        })
         .def_property_readonly("num_groups", [](const PyArgCsr& p) { return p.info().num_groups; })
         .def_property_readonly("nnz", [](const PyArgCsr& p) { return p.info().nnz; })
         .def_property_readonly("heavy_groups", [](const PyArgCsr& p) { return p.info().heavy_groups; })
@@ -336,7 +340,7 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
 
     m.def(
         "argcsr_from_csr",
-        [](const CsrMatrix& A, std::size_t tpg, std::size_t dcs, int device) {
+        [](const CsrMatrix& A, std::size_t tpg, std::size_t dcs, int device, std::uint32_t flags) {
             argcsr_csr_view v{};
             v.num_rows = A.num_rows;
             v.num_cols = A.num_cols;
@@ -349,22 +353,22 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
             argcsr_dev* h = nullptr;
             {
                 py::gil_scoped_release nogil;
-                check(argcsr_dev_convert(&v, tpg, dcs, device, nullptr, &h));
+                check(argcsr_dev_convert_ex(&v, tpg, dcs, device, nullptr, flags, &h));
             }
             return make_handle(h);
         },
         py::arg("matrix"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
-        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0);
+        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);
 
     m.def("argcsr_from_csr_arrays", &convert_arrays, py::arg("num_rows"), py::arg("num_cols"), py::arg("row_pointers"),
           py::arg("columns"), py::arg("values"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
-          py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0);
+          py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);
 
     m.def(
         "argcsr_from_device_csr",
         [](std::uint64_t num_rows, std::uint64_t num_cols, std::uint64_t nnz, std::uintptr_t rp, std::uintptr_t cols,
            std::uintptr_t vals, const std::string& dtype, std::size_t tpg, std::size_t dcs, int device,
-           std::uintptr_t stream) {
+           std::uintptr_t stream, std::uint32_t flags) {
             argcsr_csr_view v{};
             v.num_rows = num_rows;
             v.num_cols = num_cols;
@@ -379,13 +383,14 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
             argcsr_dev* h = nullptr;
             {
                 py::gil_scoped_release nogil;
-                check(argcsr_dev_convert(&v, tpg, dcs, device, reinterpret_cast<void*>(stream), &h));
+                check(argcsr_dev_convert_ex(&v, tpg, dcs, device, reinterpret_cast<void*>(stream), flags, &h));
             }
             return make_handle(h);
         },
         py::arg("num_rows"), py::arg("num_cols"), py::arg("nnz"), py::arg("row_pointers_ptr"), py::arg("columns_ptr"),
         py::arg("values_ptr"), py::arg("dtype") = "float64", py::arg("threads_per_group") = kDefaultThreadsPerGroup,
-        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("stream") = 0);
+        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("stream") = 0,
+        py::arg("flags") = 0u);
 
     m.def(
         "csr_from_argcsr",

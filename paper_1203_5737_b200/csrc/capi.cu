@@ -74,6 +74,7 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->heavy);
     cudaFree(m->heavy_ptr);
     cudaFree(m->sched);
+    cudaFree(m->ttiles);
     if (m->aux) cudaStreamDestroy(m->aux);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
@@ -135,6 +136,11 @@ const char* argcsr_status_name(argcsr_status s) {
 
 argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t tpg, uint64_t dcs, int device,
                                  void* stream, argcsr_dev** out) {
+    return argcsr_dev_convert_ex(csr, tpg, dcs, device, stream, 0u, out);
+}
+
+argcsr_status argcsr_dev_convert_ex(const argcsr_csr_view* csr, uint64_t tpg, uint64_t dcs, int device,
+                                    void* stream, uint32_t flags, argcsr_dev** out) {
     return guarded([&] {
         if (!csr || !out) fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert: null argument");
         *out = nullptr;
@@ -149,6 +155,8 @@ argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t tpg, uint6
                                            std::to_string(argcsr_gpu::kMaxThreadsPerGroup));
         if (csr->num_rows >= 0xFFFFFFFFull)
             fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: num_rows exceeds the device limit 2^32-2");
+        if (flags & ~uint32_t(ARGCSR_LAYOUT_REFERENCE))
+            fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert_ex: unknown flags");
         if (csr->dtype != ARGCSR_F64 && csr->dtype != ARGCSR_F32)
             fail(ARGCSR_E_PARAMETER, "argcsr_from_csr: unknown dtype");
         if (!csr->row_pointers || (csr->nnz && (!csr->columns || !csr->values)))
@@ -164,6 +172,7 @@ argcsr_status argcsr_dev_convert(const argcsr_csr_view* csr, uint64_t tpg, uint6
         m->tpg = tpg;
         m->dcs = dcs;
         m->tm16 = true;
+        m->layout = (flags & ARGCSR_LAYOUT_REFERENCE) ? argcsr_gpu::kLayoutReference : argcsr_gpu::kLayoutCompact;
         try {
             m->l2_persist_max = ensure_l2_persist(device);
             CUDA_OK(cudaDeviceGetAttribute(&m->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize, device));
@@ -223,6 +232,8 @@ argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info) {
         info->desired_chunk_size = m->dcs;
         info->num_groups = m->num_groups;
         info->total_slots = m->total_slots;
+        info->stored_slots = m->stored_slots;
+        info->layout = m->layout == argcsr_gpu::kLayoutReference ? ARGCSR_LAYOUT_REFERENCE : 0u;
         info->nnz = m->nnz;
         info->heavy_groups = m->num_heavy;
         info->heavy_ctas = m->heavy_ctas;
@@ -346,13 +357,17 @@ argcsr_status argcsr_dev_chunk_entries(const argcsr_dev* m, uint64_t group_index
         const size_t es = elem_size(m->dtype);
         std::vector<int32_t> c(d.chunk);
         std::vector<unsigned char> v(size_t(d.chunk) * es);
-        if (d.chunk) {
-            const uint64_t slot = d.offset + chunk_index;
-            CUDA_OK(cudaMemcpy2DAsync(c.data(), sizeof(int32_t), m->columns + slot, m->tpg * sizeof(int32_t),
+        // lanes at or past the stored stride are free lanes: all padding
+        const uint64_t w = d.stride();
+        if (d.chunk && chunk_index < w) {
+            const uint64_t slot = d.offset() + chunk_index;
+            CUDA_OK(cudaMemcpy2DAsync(c.data(), sizeof(int32_t), m->columns + slot, w * sizeof(int32_t),
                                       sizeof(int32_t), d.chunk, cudaMemcpyDeviceToHost, s));
-            CUDA_OK(cudaMemcpy2DAsync(v.data(), es, static_cast<const unsigned char*>(m->values) + slot * es,
-                                      m->tpg * es, es, d.chunk, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaMemcpy2DAsync(v.data(), es, static_cast<const unsigned char*>(m->values) + slot * es, w * es,
+                                      es, d.chunk, cudaMemcpyDeviceToHost, s));
             CUDA_OK(cudaStreamSynchronize(s));
+        } else {
+            std::fill(c.begin(), c.end(), -1);
         }
         uint64_t k = 0;
         while (k < d.chunk && c[k] != -1) ++k;

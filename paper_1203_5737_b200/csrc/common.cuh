@@ -33,22 +33,54 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define LAUNCH_OK(what) ::argcsr_gpu::cuda_check(cudaGetLastError(), what)
 
 // ------------------------------------------------------------ device layout
-// Group descriptor, 16 B, one LDG.128.  offset is the reference GroupInfo
-// offset (argcsr.hpp:23-30); size is first_row[g+1] - first_row[g] (the
-// array carries a sentinel entry G with first_row = num_rows, offset =
-// total_slots).
+// Group descriptor, 16 B, one LDG.128.  `off_stride` packs the group's slot
+// offset in the STORED value/column arrays (bits 0-47), its lane stride (bits
+// 48-62) and the long-chunk ("heavy") flag (bit 63): slot (j, lane) of group g
+// lives at offset + j * stride + lane.
+// In the reference layout stride = threads_per_group and offset is the
+// reference GroupInfo offset (argcsr.hpp:23-30).  In the lane-compact layout
+// (the default) stride = assigned lanes rounded up to the
+// SpMV vector width: the free lanes of a group, which the reference fills with
+// (0.0, -1) and never contribute, are not stored, so the matrix streams
+// contiguously; export re-expands to the reference arrays.  size is
+// first_row[g+1] - first_row[g] (the array carries a sentinel entry G with
+// first_row = num_rows, offset = stored slots).
+constexpr uint64_t kOffsetMask = (uint64_t(1) << 48) - 1;
+constexpr uint64_t kHeavyBit = uint64_t(1) << 63;
 struct alignas(16) GroupDesc {
-    uint64_t offset;
+    uint64_t off_stride;
     uint32_t first_row;
     uint32_t chunk;
+    __host__ __device__ __forceinline__ uint64_t offset() const { return off_stride & kOffsetMask; }
+    __host__ __device__ __forceinline__ uint32_t stride() const { return uint32_t(off_stride >> 48) & 0x7FFFu; }
+    __host__ __device__ __forceinline__ bool heavy() const { return (off_stride & kHeavyBit) != 0; }
 };
+
+// One tile of the lane-compact TMA SpMV (spmv.cu): a run of consecutive
+// groups [gs, gs + ng) whose light slots are the contiguous stored range
+// [slot_begin, slot_begin + nslots) (heavy groups are stored after all light
+// groups, so they never sit inside a tile's range), rows [row0, row0 + nrows)
+// and light units [ub0, ub0 + nunits).  Built by the converter.
+struct alignas(16) TileDesc {
+    uint64_t slot_begin;
+    uint64_t ub0;
+    uint32_t gs, ng;
+    uint32_t row0, nrows;
+    uint32_t nslots, nunits;
+    uint32_t pad0, pad1;
+};
+static_assert(sizeof(TileDesc) == 48, "TileDesc must be 48 bytes");
 static_assert(sizeof(GroupDesc) == 16, "GroupDesc must be 16 bytes");
+
+enum Layout : int { kLayoutCompact = 0, kLayoutReference = 1 };
 
 // Device limits (documented in DESIGN.md).  threads_per_group bounds the
 // shared-memory partial-sum staging of the SpMV; rows are u32 on the device.
 constexpr uint64_t kMaxThreadsPerGroup = 16384;
-// Groups with chunk_size above this run on the long-chunk (heavy) path.
+// Groups with chunk_size above this run on the long-chunk (heavy) path, and so
+// do lane-compact groups whose staged block would exceed kLightMaxBytes.
 constexpr uint32_t kHeavyChunk = 32;
+constexpr uint64_t kLightMaxBytes = 56 * 1024;
 // Units (V-lane quads) per light tile = threads per SpMV CTA.
 constexpr int kTileThreads = 256;
 
@@ -60,10 +92,12 @@ struct argcsr_dev {
     argcsr_dtype dtype = ARGCSR_F64;
     uint64_t num_rows = 0, num_cols = 0, nnz = 0, tpg = 0, dcs = 0;
     uint64_t num_groups = 0, total_slots = 0, max_chunk = 0;
+    int layout = argcsr_gpu::kLayoutCompact;
+    uint64_t stored_slots = 0;            // length of values/columns (== total_slots in the reference layout)
     bool tm16 = true;  // threads_mapping / assigned stored as u16 (tpg <= 65535)
 
-    void* values = nullptr;               // [total_slots] f64 | f32
-    int32_t* columns = nullptr;           // [total_slots]
+    void* values = nullptr;               // [stored_slots] f64 | f32
+    int32_t* columns = nullptr;           // [stored_slots]
     argcsr_gpu::GroupDesc* groups = nullptr;  // [num_groups + 1]
     void* tm = nullptr;                   // [num_rows]   u16 | u32
     void* assigned = nullptr;             // [num_groups] u16 | u32
@@ -85,6 +119,13 @@ struct argcsr_dev {
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     uint32_t* sched = nullptr;            // [2] dynamic tile counter + done counter (self-resetting)
+
+    // Lane-compact TMA schedule: tiles of whole groups, bulk-copied into
+    // shared-memory stages of stage_bytes (see spmv.cu).
+    argcsr_gpu::TileDesc* ttiles = nullptr;  // [num_ttiles]
+    uint32_t num_ttiles = 0;
+    uint32_t stage_bytes = 0;
+    uint64_t light_slots = 0;             // stored slots of light groups (they come first)
 
     // x residency (L2 persisting window) — queried, not hard-coded.
     size_t l2_persist_max = 0;

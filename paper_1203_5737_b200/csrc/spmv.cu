@@ -45,9 +45,11 @@ struct SpmvArgs {
     const uint32_t* __restrict__ tiles;
     const uint32_t* __restrict__ heavy;
     const uint32_t* __restrict__ heavy_ptr;
+    const TileDesc* __restrict__ ttiles;  // lane-compact TMA tiles
+    uint32_t num_ttiles;
+    uint32_t stage_bytes;
     const T* __restrict__ x;
     T* __restrict__ y;
-    uint64_t tpg;
     uint32_t heavy_ctas;
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
     uint32_t max_tile_groups;
@@ -129,15 +131,16 @@ __device__ __forceinline__ double ld_x(const float* p, uint64_t pol) {
 // finished vector are skipped when PRED); the layout keeps sentinels
 // trailing, so "skip sentinel" == "stop at the first sentinel".
 template <typename T, int V, int U, bool PRED>
-__device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, double (&s)[V],
-                                       uint64_t pol_stream, uint64_t pol_x, double xs, uint32_t jstart = 0) {
+__device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, uint64_t stride,
+                                       double (&s)[V], uint64_t pol_stream, uint64_t pol_x, double xs,
+                                       uint32_t jstart = 0) {
     if (jstart == 0) {
 #pragma unroll
         for (int l = 0; l < V; ++l) s[l] = 0.0;
     }
     const int32_t* cp = a.cols + slot0;
     const T* vp = a.vals + slot0;
-    const uint64_t tpg = a.tpg;
+    const uint64_t tpg = stride;
     for (uint32_t j0 = jstart; j0 < chunk; j0 += U) {
         int c[U][V];
         T v[U][V];
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvA
         if (g < a.g_begin || g >= a.g_end) continue;
         const GroupDesc d = a.groups[g];
         double s[1];
-        phase1<T, 1, UH, false>(a, d.offset + (l - s_lane0[i]), d.chunk, s, pol_stream, pol_x, xs);
+        phase1<T, 1, UH, false>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream, pol_x, xs);
         s_part[l] = s[0];
     }
     __syncthreads();
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
         s_first[i] = d.first_row;
         s_ub[i] = uint32_t(a.unit_base[gs + i] - ub0);
         if (i < ng) {
-            s_off[i] = d.offset;
+            s_off[i] = d.off_stride;
             s_chunk[i] = d.chunk;
         }
     }
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     if (pr < row_end) {
         pgi = find_le(s_first, ng, pr);
         const uint32_t g = gs + pgi;
-        pvalid = s_chunk[pgi] <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
+        pvalid = !(s_off[pgi] & kHeavyBit) && g >= a.g_begin && g < a.g_end;
         if (pvalid) {
             pb = pr == s_first[pgi] ? 0u : uint32_t(a.tm[pr - 1]);
             pe = uint32_t(a.tm[pr]);
@@ -309,9 +312,11 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) {
         const uint32_t gi = find_le(s_ub, ng, u);
         const uint32_t g = gs + gi;
-        if (s_chunk[gi] > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+        if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         double s[V];
-        phase1<T, V, U, PRED>(a, s_off[gi] + (u - s_ub[gi]) * V, s_chunk[gi], s, pol_stream, pol_x, xs);
+        const uint64_t os = s_off[gi];
+        phase1<T, V, U, PRED>(a, (os & kOffsetMask) + (u - s_ub[gi]) * V, s_chunk[gi], (os >> 48) & 0x7FFF, s, pol_stream,
+                              pol_x, xs);
 #pragma unroll
         for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = s[l];
     }
@@ -321,20 +326,13 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
         const uint32_t gi = find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
-        if (s_chunk[gi] > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+        if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
         a.y[r] = to_out<T>(row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
     }
 }
 
-// ------------------------------------------------ pipelined light path (V = 4)
-// Persistent CTAs walk the light tiles k = blockIdx.x, +gridDim.x, ...  Each
-// thread owns one 4-lane unit of the current tile and streams that unit's
-// column/value slabs (J element steps) into its PRIVATE shared-memory slots
-// with cp.async, one slab ahead of the x gathers it is doing; the next tile's
-// group metadata and its first slab are prefetched across the tile boundary.
-// In-flight matrix bytes therefore cost no registers, and the HBM stream never
-// waits on the x gathers or on phase 2.
+// ---------------------------------------------------------- cp.async helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -348,205 +346,6 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <typename T>
-struct PipeUnit {  // this thread's unit in the current tile
-    uint64_t slot0 = 0;
-    uint32_t chunk = 0;
-    uint32_t nslabs = 0;
-};
-
-template <typename T, int J>
-__device__ __forceinline__ void pipe_issue_slab(const SpmvArgs<T>& a, const PipeUnit<T>& pu, uint32_t s, int4* cslot,
-                                                unsigned char* vslot, uint64_t pol) {
-    // slab s: element steps j = s*J .. s*J+J-1 of this unit (only j < chunk)
-    constexpr int VB = 4 * sizeof(T);  // value bytes per unit step (32 fp64 / 16 fp32)
-#pragma unroll
-    for (int q = 0; q < J; ++q) {
-        const uint32_t j = s * J + q;
-        if (j < pu.chunk) {
-            const uint64_t slot = pu.slot0 + uint64_t(j) * a.tpg;
-            cp_async16(smem_u32(cslot + q * kTileThreads), a.cols + slot, pol);
-            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.vals + slot);
-            unsigned char* dst = vslot + size_t(q) * kTileThreads * VB;
-#pragma unroll
-            for (int h = 0; h < VB; h += 16) cp_async16(smem_u32(dst + h), src + h, pol);
-        }
-    }
-}
-
-template <typename T, int J>
-__global__ void __launch_bounds__(kTileThreads, 2) spmv_pipe_kernel(const SpmvArgs<T> a, uint32_t num_tiles) {
-    constexpr int VB = 4 * sizeof(T);
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t cap = a.max_tile_groups;
-    // layout: cols[2][J][B] int4 | vals[2][J][B][VB] | part[B*4] f64 | meta[2]{desc[cap+1], ub[cap+1]}
-    int4* s_cols = reinterpret_cast<int4*>(smem);
-    unsigned char* s_vals = smem + size_t(2) * J * kTileThreads * sizeof(int4);
-    double* s_part = reinterpret_cast<double*>(s_vals + size_t(2) * J * kTileThreads * VB);
-    unsigned char* mbase = reinterpret_cast<unsigned char*>(s_part + kTileThreads * 4);
-    const size_t meta_bytes = ((size_t(cap) + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15);
-    auto meta_desc = [&](int b) { return reinterpret_cast<GroupDesc*>(mbase + b * meta_bytes); };
-    auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
-    const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
-    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const double xs = a.x_scale ? *a.x_scale : 1.0;
-    const uint32_t tid = threadIdx.x;
-
-    auto issue_meta = [&](uint32_t k, int b) {
-        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
-        for (uint32_t i = tid; i <= ge - gs; i += blockDim.x) {
-            cp_async16(smem_u32(meta_desc(b) + i), a.groups + gs + i, pol_x);
-            cp_async8(smem_u32(meta_ub(b) + i), a.unit_base + gs + i);
-        }
-    };
-    // this thread's unit of tile k (metadata in buffer b); returns group index in tile
-    auto my_unit = [&](uint32_t k, int b, PipeUnit<T>& pu, uint32_t& gi_out) -> bool {
-        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
-        const uint32_t ng = ge - gs;
-        const uint64_t ub0 = meta_ub(b)[0];
-        const uint64_t u = ub0 + tid;
-        pu = PipeUnit<T>{};
-        if (ng == 0 || u >= meta_ub(b)[ng]) return false;
-        uint32_t lo = 0, hi = ng - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) / 2;
-            if (meta_ub(b)[mid] <= u) lo = mid; else hi = mid - 1;
-        }
-        gi_out = lo;
-        const GroupDesc d = meta_desc(b)[lo];
-        const uint32_t g = gs + lo;
-        if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) return false;
-        pu.slot0 = d.offset + (u - meta_ub(b)[lo]) * 4;
-        pu.chunk = d.chunk;
-        pu.nslabs = (d.chunk + J - 1) / J;
-        return true;
-    };
-
-    uint32_t k = blockIdx.x;
-    if (k >= num_tiles) return;
-    int mb = 0;
-    issue_meta(k, mb);
-    cp_commit();
-    cp_wait<0>();
-    __syncthreads();
-    PipeUnit<T> pu;
-    uint32_t gi = 0;
-    bool have = my_unit(k, mb, pu, gi);
-    if (have) pipe_issue_slab<T, J>(a, pu, 0, s_cols + tid, s_vals + size_t(tid) * VB, pol);
-    cp_commit();
-
-    for (;;) {
-        const uint32_t kn = k + gridDim.x;
-        const bool has_next = kn < num_tiles;
-        // next tile's metadata, landing while this tile streams
-        if (has_next) issue_meta(kn, mb ^ 1);
-        cp_commit();
-        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
-        const uint32_t ng = ge - gs;
-        const GroupDesc* md = meta_desc(mb);
-        const uint64_t* mub = meta_ub(mb);
-        const uint64_t ub0 = mub[0];
-
-        // phase-2 metadata of this thread's first row of tile k (registers)
-        const uint32_t row0 = md[0].first_row, row_end = md[ng].first_row;
-        const uint32_t pr = row0 + tid;
-        uint32_t pgi = 0, pb = 0, pe = 0;
-        bool pvalid = false;
-        if (pr < row_end && ng > 0) {
-            uint32_t lo = 0, hi = ng - 1;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) / 2;
-                if (md[mid].first_row <= pr) lo = mid; else hi = mid - 1;
-            }
-            pgi = lo;
-            const uint32_t g = gs + pgi;
-            pvalid = md[pgi].chunk <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
-            if (pvalid) {
-                pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
-                pe = uint32_t(a.tm[pr]);
-            }
-        }
-
-        // phase 1: slab pipeline over this thread's unit
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        bool done = false;
-        for (uint32_t sidx = 0; sidx < pu.nslabs; ++sidx) {
-            const int buf = sidx & 1;
-            if (sidx + 1 < pu.nslabs) {
-                const int nb = buf ^ 1;
-                pipe_issue_slab<T, J>(a, pu, sidx + 1, s_cols + size_t(nb) * J * kTileThreads + tid,
-                                      s_vals + (size_t(nb) * J * kTileThreads + tid) * VB, pol);
-            }
-            cp_commit();
-            cp_wait<1>();
-            const int4* cs = s_cols + size_t(buf) * J * kTileThreads + tid;
-            const unsigned char* vs = s_vals + (size_t(buf) * J * kTileThreads + tid) * VB;
-            int c[J][4];
-            double xv[J][4];
-#pragma unroll
-            for (int q = 0; q < J; ++q) {
-                const bool in = sidx * J + q < pu.chunk;
-                const int4 cc = in ? cs[q * kTileThreads] : make_int4(-1, -1, -1, -1);
-                c[q][0] = cc.x, c[q][1] = cc.y, c[q][2] = cc.z, c[q][3] = cc.w;
-#pragma unroll
-                for (int l = 0; l < 4; ++l)
-                    xv[q][l] = c[q][l] != -1 ? __dmul_rn(ld_x(a.x + c[q][l], pol_x), xs) : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < J; ++q) {
-                const T* vv = reinterpret_cast<const T*>(vs + size_t(q) * kTileThreads * VB);
-#pragma unroll
-                for (int l = 0; l < 4; ++l)
-                    if (c[q][l] != -1) acc[l] = __dadd_rn(acc[l], __dmul_rn(double(vv[l]), xv[q][l]));
-            }
-            if ((c[J - 1][0] & c[J - 1][1] & c[J - 1][2] & c[J - 1][3]) == -1) {
-                done = true;
-                break;
-            }
-        }
-        (void)done;
-        if (have) {
-            const uint64_t u = ub0 + tid;
-#pragma unroll
-            for (int l = 0; l < 4; ++l) s_part[size_t(u - ub0) * 4 + l] = acc[l];
-        }
-        cp_wait<0>();  // next tile's metadata (and any abandoned slab) landed
-        __syncthreads();
-
-        // prefetch the next tile's first slab before phase 2 of this tile
-        PipeUnit<T> pn;
-        uint32_t gin = 0;
-        bool have_n = false;
-        if (has_next) {
-            have_n = my_unit(kn, mb ^ 1, pn, gin);
-            if (have_n) pipe_issue_slab<T, J>(a, pn, 0, s_cols + tid, s_vals + size_t(tid) * VB, pol);
-        }
-        cp_commit();
-
-        // phase 2 of tile k
-        if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(mub[pgi] - ub0) * 4, pb, pe));
-        for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
-            uint32_t lo = 0, hi = ng - 1;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi + 1) / 2;
-                if (md[mid].first_row <= r) lo = mid; else hi = mid - 1;
-            }
-            const uint32_t g = gs + lo;
-            if (md[lo].chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
-            const uint32_t b = r == md[lo].first_row ? 0u : uint32_t(a.tm[r - 1]);
-            a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[lo] - ub0) * 4, b, uint32_t(a.tm[r])));
-        }
-        __syncthreads();  // partials and metadata buffer mb are reused
-        if (!has_next) break;
-        k = kn;
-        mb ^= 1;
-        pu = pn;
-        have = have_n;
-        gi = gin;
-    }
-    cp_wait<0>();
-}
 
 // --------------------------------------- persistent light path (prefetched metadata)
 // Same per-tile work as spmv_light_kernel, but each CTA walks tiles k,
@@ -637,7 +436,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
         if (pr < row_end) {
             pgi = find_row(md, ng, pr);
             const uint32_t g = gs + pgi;
-            pvalid = md[pgi].chunk <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
+            pvalid = !md[pgi].heavy() && g >= a.g_begin && g < a.g_end;
             if (pvalid) {
                 pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
                 pe = uint32_t(a.tm[pr]);
@@ -648,9 +447,10 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
             const uint32_t gi = find_le64(mub, ng, ub0 + u);
             const uint32_t g = gs + gi;
             const GroupDesc d = md[gi];
-            if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+            if (d.heavy() || g < a.g_begin || g >= a.g_end) continue;
             double sacc[V];
-            phase1<T, V, U, PRED>(a, d.offset + (ub0 + u - mub[gi]) * V, d.chunk, sacc, pol_stream, pol_x, xs);
+            phase1<T, V, U, PRED>(a, d.offset() + (ub0 + u - mub[gi]) * V, d.chunk, d.stride(), sacc, pol_stream,
+                                  pol_x, xs);
 #pragma unroll
             for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = sacc[l];
         }
@@ -664,7 +464,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
         for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
             const uint32_t gi = find_row(md, ng, r);
             const uint32_t g = gs + gi;
-            if (md[gi].chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
+            if (md[gi].heavy() || g < a.g_begin || g >= a.g_end) continue;
             const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
             a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
         }
@@ -693,178 +493,275 @@ size_t lightp_smem_bytes(const argcsr_dev* m, int V) {
 template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
 void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s);
 
-// ------------------------------------------- cross-tile slab pipeline (V = 4)
-// Persistent CTAs of B threads walk tiles k, k+G, ... (one 4-lane unit per
-// thread).  At the top of tile k every thread issues cp.async copies of the
-// first J element steps of ITS unit in tile k+G into private shared-memory
-// slots, and the group metadata of tile k+2G into a third buffer; then it
-// consumes tile k (whose slab was issued one tile earlier).  The HBM stream of
-// the next tile is thus in flight during the whole x-gather / reduction phase
-// of the current one, at no register cost.  Steps beyond J (chunk > J) load
-// directly like spmv_light_kernel.
-template <typename T, int J, int B>
-__global__ void __launch_bounds__(B) spmv_pipex_kernel(const SpmvArgs<T> a, uint32_t num_tiles) {
-    constexpr int VB = 4 * sizeof(T);
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t cap = a.max_tile_groups;
-    int4* s_cols = reinterpret_cast<int4*>(smem);                  // [2][J][B]
-    unsigned char* s_vals = smem + size_t(2) * J * B * sizeof(int4);  // [2][J][B][VB]
-    double* s_part = reinterpret_cast<double*>(s_vals + size_t(2) * J * B * VB);  // [B][4]
-    unsigned char* mbase = reinterpret_cast<unsigned char*>(s_part + B * 4);
-    const size_t meta_bytes = ((size_t(cap) + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15);
-    auto meta_desc = [&](int b) { return reinterpret_cast<GroupDesc*>(mbase + b * meta_bytes); };
-    auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
-    const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
-    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const double xs = a.x_scale ? *a.x_scale : 1.0;
-    const uint32_t tid = threadIdx.x;
 
-    auto issue_meta = [&](uint32_t k, int b) {
-        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
-        for (uint32_t i = tid; i <= ge - gs; i += B) {
-            cp_async16(smem_u32(meta_desc(b) + i), a.groups + gs + i, pol_x);
-            cp_async8(smem_u32(meta_ub(b) + i), a.unit_base + gs + i);
-        }
-    };
-    auto unit_of = [&](uint32_t k, int b, PipeUnit<T>& pu) -> bool {
-        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
-        const uint32_t ng = ge - gs;
-        pu = PipeUnit<T>{};
-        const uint64_t* ub = meta_ub(b);
-        if (ng == 0 || ge <= a.g_begin || gs >= a.g_end) return false;
-        const uint64_t u = ub[0] + tid;
-        if (u >= ub[ng]) return false;
-        const uint32_t gi = find_le64(ub, ng, u);
-        const GroupDesc d = meta_desc(b)[gi];
-        const uint32_t g = gs + gi;
-        if (d.chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) return false;
-        pu.slot0 = d.offset + (u - ub[gi]) * 4;
-        pu.chunk = d.chunk;
-        return true;
-    };
-    auto issue_slab = [&](const PipeUnit<T>& pu, int buf) {
-#pragma unroll
-        for (int q = 0; q < J; ++q) {
-            if (uint32_t(q) < pu.chunk) {
-                const uint64_t slot = pu.slot0 + uint64_t(q) * a.tpg;
-                cp_async16(smem_u32(s_cols + (size_t(buf) * J + q) * B + tid), a.cols + slot, pol);
-                const unsigned char* src = reinterpret_cast<const unsigned char*>(a.vals + slot);
-                unsigned char* dst = s_vals + ((size_t(buf) * J + q) * B + tid) * VB;
-#pragma unroll
-                for (int h = 0; h < VB; h += 16) cp_async16(smem_u32(dst + h), src + h, pol);
-            }
-        }
-    };
+// ------------------------------------------- lane-compact TMA path (default)
+// Persistent CTAs (one per SM) walk the tiles k = blockIdx.x, +gridDim.x, ...
+// A tile is a run of whole light groups whose value/column blocks are ONE
+// contiguous stored range in the lane-compact layout.  One elected thread
+// stages a tile into a shared-memory stage with five cp.async.bulk copies
+// (group descriptors, unit bases, threads_mapping of its rows, columns,
+// values) completing on the stage's mbarrier; `nstages` stages are kept in
+// flight, so the HBM stream runs ahead of the x gathers and the reduction
+// (they never wait on each other except through a full ring).  Consumers:
+//   phase 1  one V-lane unit per thread and step, columns/values from shared
+//            memory, 4 element steps (4V x gathers) in flight, partial sums
+//            per lane to the stage's partial section;
+//   phase 2  one row per thread, +0.0 + p_b + ... ascending (bit-exact order).
+struct StageHdr {
+    uint32_t p_desc, p_ub, p_tm, p_cols, p_vals, p_part;
+    uint32_t gs, ng, row0, nrows, nunits, nslots;
+    uint64_t ub0, slot_begin;
+};
 
-    uint32_t k = blockIdx.x;
-    if (k >= num_tiles) return;
-    issue_meta(k, 0);
-    cp_commit();
-    cp_wait<0>();
-    __syncthreads();
-    uint32_t kn = k + gridDim.x;
-    if (kn < num_tiles) issue_meta(kn, 1);
-    PipeUnit<T> pu;
-    bool have = unit_of(k, 0, pu);
-    if (have) issue_slab(pu, 0);
-    cp_commit();
-    for (uint32_t it = 0;; ++it) {
-        const int mc = it % 3, mn = (it + 1) % 3, m2 = (it + 2) % 3, sc = it & 1;
-        cp_wait<0>();  // slab of tile k and metadata of tile k+G (both issued one tile ago)
-        __syncthreads();
-        const uint32_t gs = a.tiles[k], ge = a.tiles[k + 1];
-        const uint32_t ng = ge - gs;
-        const GroupDesc* md = meta_desc(mc);
-        const uint64_t* mub = meta_ub(mc);
-        const bool live = ng > 0 && !(ge <= a.g_begin || gs >= a.g_end);
-        const uint64_t ub0 = mub[0];
-        const uint32_t row0 = md[0].first_row, row_end = live ? md[ng].first_row : row0;
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, uint64_t src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 
-        // next tile's first slab and the metadata two tiles ahead
-        PipeUnit<T> pn;
-        bool have_n = false;
-        if (kn < num_tiles) {
-            have_n = unit_of(kn, mn, pn);
-            if (have_n) issue_slab(pn, sc ^ 1);
-            const uint32_t k2 = kn + gridDim.x;
-            if (k2 < num_tiles) issue_meta(k2, m2);
-        }
-        cp_commit();
-
-        // phase-2 metadata of this thread's first row (registers)
-        const uint32_t pr = row0 + tid;
-        uint32_t pgi = 0, pb = 0, pe = 0;
-        bool pvalid = false;
-        if (pr < row_end) {
-            pgi = find_row(md, ng, pr);
-            const uint32_t g = gs + pgi;
-            pvalid = md[pgi].chunk <= kHeavyChunk && g >= a.g_begin && g < a.g_end;
-            if (pvalid) {
-                pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
-                pe = uint32_t(a.tm[pr]);
-            }
-        }
-
-        // phase 1: the first J steps from the slab, the rest straight from HBM
-        if (have) {
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            int c[J][4];
-            double xv[J][4];
+// Stage tile k: header + bulk copies (16-B aligned-down/up sections; the
+// device arrays carry 16 B of tail padding for the round-up).
+template <typename T, int V>
+__device__ __forceinline__ void tma_issue(const SpmvArgs<T>& a, const TileDesc& t, unsigned char* stage,
+                                          StageHdr* hdr, uint64_t* bar, uint64_t pol_meta, uint64_t pol_stream) {
+    const uint64_t src[5] = {uint64_t(a.groups + t.gs), uint64_t(a.unit_base + t.gs), uint64_t(a.tm + t.row0),
+                             uint64_t(a.cols + t.slot_begin), uint64_t(a.vals + t.slot_begin)};
+    const uint64_t len[5] = {sizeof(GroupDesc) * (uint64_t(t.ng) + 1), sizeof(uint64_t) * (uint64_t(t.ng) + 1),
+                             sizeof(uint16_t) * uint64_t(t.nrows), sizeof(int32_t) * uint64_t(t.nslots),
+                             sizeof(T) * uint64_t(t.nslots)};
+    uint64_t lo[5];
+    uint32_t n[5], p[5], off = 0, total = 0;
 #pragma unroll
-            for (int q = 0; q < J; ++q) {
-                const bool in = uint32_t(q) < pu.chunk;
-                const int4 cc = in ? s_cols[(size_t(sc) * J + q) * B + tid] : make_int4(-1, -1, -1, -1);
-                c[q][0] = cc.x, c[q][1] = cc.y, c[q][2] = cc.z, c[q][3] = cc.w;
-#pragma unroll
-                for (int l = 0; l < 4; ++l) xv[q][l] = c[q][l] != -1 ? ld_x(a.x + c[q][l], pol_x) : 0.0;
-            }
-            if (a.x_scale) {
-#pragma unroll
-                for (int q = 0; q < J; ++q)
-#pragma unroll
-                    for (int l = 0; l < 4; ++l) xv[q][l] = __dmul_rn(xv[q][l], xs);
-            }
-#pragma unroll
-            for (int q = 0; q < J; ++q) {
-                const T* vv = reinterpret_cast<const T*>(s_vals + ((size_t(sc) * J + q) * B + tid) * VB);
-#pragma unroll
-                for (int l = 0; l < 4; ++l)
-                    if (c[q][l] != -1) acc[l] = __dadd_rn(acc[l], __dmul_rn(double(vv[l]), xv[q][l]));
-            }
-            const bool more = pu.chunk > uint32_t(J) && (c[J - 1][0] & c[J - 1][1] & c[J - 1][2] & c[J - 1][3]) != -1;
-            if (more) phase1<T, 4, J, true>(a, pu.slot0, pu.chunk, acc, pol, pol_x, xs, uint32_t(J));
-#pragma unroll
-            for (int l = 0; l < 4; ++l) s_part[size_t(tid) * 4 + l] = acc[l];
-        }
-        __syncthreads();
-
-        if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(mub[pgi] - ub0) * 4, pb, pe));
-        for (uint32_t r = pr + B; r < row_end; r += B) {
-            const uint32_t gi = find_row(md, ng, r);
-            const uint32_t g = gs + gi;
-            if (md[gi].chunk > kHeavyChunk || g < a.g_begin || g >= a.g_end) continue;
-            const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
-            a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[gi] - ub0) * 4, b, uint32_t(a.tm[r])));
-        }
-        if (kn >= num_tiles) break;
-        k = kn;
-        kn = k + gridDim.x;
-        pu = pn;
-        have = have_n;
+    for (int i = 0; i < 5; ++i) {
+        lo[i] = src[i] & ~uint64_t(15);
+        n[i] = len[i] ? uint32_t(((src[i] + len[i] + 15) & ~uint64_t(15)) - lo[i]) : 0u;
+        p[i] = off + uint32_t(src[i] - lo[i]);
+        off += n[i];
+        total += n[i];
     }
-    cp_wait<0>();
+    hdr->p_desc = p[0], hdr->p_ub = p[1], hdr->p_tm = p[2], hdr->p_cols = p[3], hdr->p_vals = p[4];
+    hdr->p_part = off;
+    hdr->gs = t.gs, hdr->ng = t.ng, hdr->row0 = t.row0, hdr->nrows = t.nrows, hdr->nunits = t.nunits;
+    hdr->nslots = t.nslots;
+    hdr->ub0 = t.ub0, hdr->slot_begin = t.slot_begin;
+    mbar_arrive_expect_tx(bar, total);
+    off = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (n[i]) bulk_g2s(stage + off, lo[i], n[i], bar, i >= 3 ? pol_stream : pol_meta);
+        off += n[i];
+    }
 }
 
-size_t pipex_smem_bytes(const argcsr_dev* m, int J, int B, size_t tbytes) {
-    const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
-    return size_t(2) * J * B * (16 + 4 * tbytes) + size_t(B) * 4 * sizeof(double) +
-           3 * (((cap + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15));
-}
+template <typename T, int V> struct SmemVec;
+template <> struct SmemVec<double, 4> {
+    static __device__ __forceinline__ void load(const double* p, double (&v)[4]) {
+        const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+        v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+    }
+};
+template <> struct SmemVec<float, 4> {
+    static __device__ __forceinline__ void load(const float* p, float (&v)[4]) {
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+    }
+};
 
-size_t pipe_smem_bytes(const argcsr_dev* m, int J, size_t tbytes) {
-    const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
-    return size_t(2) * J * kTileThreads * (16 + 4 * tbytes) + size_t(kTileThreads) * 4 * sizeof(double) +
-           2 * (((cap + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15));
+template <typename T, int V, int NT>
+__global__ void __launch_bounds__(NT) spmv_tma_kernel(const SpmvArgs<T> a, uint32_t nstages) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[4];
+    __shared__ StageHdr hdrs[4];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t G = gridDim.x;
+    const uint32_t SB = a.stage_bytes;
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_meta = policy_evict_normal();
+    const double xs = a.x_scale ? *a.x_scale : 1.0;
+    const uint32_t mine = a.num_ttiles > blockIdx.x ? (a.num_ttiles - blockIdx.x + G - 1) / G : 0;
+    if (tid == 0) {
+        for (uint32_t s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (uint32_t i = 0; i < nstages && i < mine; ++i)
+            tma_issue<T, V>(a, a.ttiles[blockIdx.x + i * G], smem + size_t(i) * SB, &hdrs[i], &bars[i], pol_meta,
+                            pol_stream);
+    }
+    __syncthreads();
+    for (uint32_t i = 0; i < mine; ++i) {
+        const uint32_t st = i % nstages;
+        mbar_wait(&bars[st], (i / nstages) & 1);
+        unsigned char* stage = smem + size_t(st) * SB;
+        const StageHdr h = hdrs[st];
+        // the descriptor of the tile this stage is refilled with, loaded now
+        // so that its latency is off the end-of-tile critical path
+        TileDesc nxt;
+        const bool refill = tid == 0 && i + nstages < mine;
+        if (refill) nxt = a.ttiles[blockIdx.x + (i + nstages) * G];
+        const GroupDesc* sd = reinterpret_cast<const GroupDesc*>(stage + h.p_desc);
+        const uint64_t* sub = reinterpret_cast<const uint64_t*>(stage + h.p_ub);
+        const uint16_t* stm = reinterpret_cast<const uint16_t*>(stage + h.p_tm);
+        const int32_t* scol = reinterpret_cast<const int32_t*>(stage + h.p_cols);
+        const T* sval = reinterpret_cast<const T*>(stage + h.p_vals);
+        double* spart = reinterpret_cast<double*>(stage + h.p_part);
+        const uint32_t ns = h.nslots;
+
+        // Phase 1 (argcsr.cpp:193-203).  A unit is V adjacent lanes of a
+        // group; its steps j = 0 .. chunk-1 are the V-slot vectors
+        // offset + j * stride + V * u.  Units are dealt out balanced by steps:
+        // in the unit-major order of the tile's steps, thread t owns the units
+        // that START in [t, t + 1) * steps / NT and runs them to the end.  A
+        // thread walks its steps in batches of kB (kB * V gathers in flight),
+        // batches crossing unit boundaries; each lane's sum is a sequential
+        // chain over j ascending from +0.0, stopping at sentinels (which are
+        // trailing), exactly the reference's.
+        {
+            constexpr uint32_t kB = 4;
+            const uint32_t nq = ns / V;  // steps of the tile
+            const uint32_t qb = uint32_t(uint64_t(nq) * tid / NT), qe = uint32_t(uint64_t(nq) * (tid + 1) / NT);
+            // group holding virtual step qb: last gi with (offset - slot_begin) / V <= qb
+            uint32_t gi = 0;
+            {
+                uint32_t lo = 0, hi = h.ng - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) / 2;
+                    if (uint32_t((sd[mid].offset() - h.slot_begin) / V) <= qb) lo = mid; else hi = mid - 1;
+                }
+                gi = lo;
+            }
+            GroupDesc d = sd[gi];
+            uint32_t chunk = d.chunk, wv = d.stride() / V;
+            uint32_t gq0 = uint32_t((d.offset() - h.slot_begin) / V);
+            uint32_t ub = uint32_t(sub[gi] - h.ub0);
+            // first unit of this group starting at or after qb
+            uint32_t ul = chunk ? (qb - gq0 + chunk - 1) / chunk : wv;
+            uint32_t j = 0;
+            bool more = qb < qe;
+            auto next_group = [&]() {
+                for (;;) {
+                    if (++gi >= h.ng) {
+                        more = false;
+                        return;
+                    }
+                    d = sd[gi];
+                    chunk = d.chunk;
+                    if (chunk) break;  // all-empty group: rows give +0.0 in phase 2
+                }
+                wv = d.stride() / V;
+                gq0 = uint32_t((d.offset() - h.slot_begin) / V);
+                ub = uint32_t(sub[gi] - h.ub0);
+                ul = 0;
+            };
+            if (more && ul >= wv) next_group();
+            if (more && gq0 + ul * chunk >= qe) more = false;
+            double acc[V];
+            while (more) {
+                uint32_t mq[kB], uid[kB], flags = 0;  // bit 2b: first step, bit 2b+1: last step
+                uint32_t cnt = 0;
+#pragma unroll
+                for (uint32_t b = 0; b < kB; ++b) {
+                    if (!more) break;
+                    mq[b] = gq0 + j * wv + ul;
+                    uid[b] = ub + ul;
+                    if (j == 0) flags |= 1u << (2 * b);
+                    if (j + 1 == chunk) flags |= 2u << (2 * b);
+                    ++cnt;
+                    if (++j == chunk) {
+                        j = 0;
+                        if (++ul >= wv) next_group();
+                        if (more && gq0 + ul * chunk >= qe) more = false;
+                    }
+                }
+                int c[kB][V];
+                T v[kB][V];
+#pragma unroll
+                for (uint32_t b = 0; b < kB; ++b) {
+                    if (b < cnt) {
+                        if constexpr (V == 4) {
+                            const int4 cc = reinterpret_cast<const int4*>(scol)[mq[b]];
+                            c[b][0] = cc.x, c[b][1] = cc.y, c[b][2] = cc.z, c[b][3] = cc.w;
+                            SmemVec<T, 4>::load(sval + 4 * mq[b], v[b]);
+                        } else {
+#pragma unroll
+                            for (int l = 0; l < V; ++l) c[b][l] = scol[V * mq[b] + l], v[b][l] = sval[V * mq[b] + l];
+                        }
+                    } else {
+#pragma unroll
+                        for (int l = 0; l < V; ++l) c[b][l] = -1, v[b][l] = T(0);
+                    }
+                }
+                double xv[kB][V];
+#pragma unroll
+                for (uint32_t b = 0; b < kB; ++b)
+#pragma unroll
+                    for (int l = 0; l < V; ++l) xv[b][l] = c[b][l] != -1 ? ld_x(a.x + c[b][l], pol_x) : 0.0;
+                if (a.x_scale) {
+#pragma unroll
+                    for (uint32_t b = 0; b < kB; ++b)
+#pragma unroll
+                        for (int l = 0; l < V; ++l) xv[b][l] = __dmul_rn(xv[b][l], xs);
+                }
+#pragma unroll
+                for (uint32_t b = 0; b < kB; ++b) {
+                    if (b < cnt) {
+                        if (flags & (1u << (2 * b))) {
+#pragma unroll
+                            for (int l = 0; l < V; ++l) acc[l] = 0.0;
+                        }
+#pragma unroll
+                        for (int l = 0; l < V; ++l)
+                            if (c[b][l] != -1) acc[l] = __dadd_rn(acc[l], __dmul_rn(double(v[b][l]), xv[b][l]));
+                        if (flags & (2u << (2 * b))) {
+#pragma unroll
+                            for (int l = 0; l < V; ++l) spart[size_t(uid[b]) * V + l] = acc[l];
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        // Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending,
+        // one row per thread.
+        for (uint32_t r = tid; r < h.nrows; r += NT) {
+            const uint32_t row = h.row0 + r;
+            const uint32_t gi = find_row(sd, h.ng, row);
+            const GroupDesc d = sd[gi];
+            const uint32_t g = h.gs + gi;
+            if (d.heavy() || g < a.g_begin || g >= a.g_end) continue;
+            double sum = 0.0;
+            if (d.chunk) {
+                const uint32_t b = row == d.first_row ? 0u : uint32_t(stm[r - 1]);
+                sum = row_sum(spart + size_t(sub[gi] - h.ub0) * V, b, uint32_t(stm[r]));
+            }
+            a.y[row] = to_out<T>(sum);
+        }
+        __syncthreads();  // stage st fully consumed
+        if (refill) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_issue<T, V>(a, nxt, stage, &hdrs[st], &bars[st], pol_meta, pol_stream);
+        }
+    }
 }
 
 size_t light_smem_bytes(const argcsr_dev* m, int V) {
@@ -887,8 +784,8 @@ int variant_id() {
         const char* e = std::getenv("ARGCSR_SPMV_VARIANT");
         if (!e) return -1;
         const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
-                               "PIPE2", "PIPE4", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "PX4", "PX2"};
-        for (int i = 0; i < 15; ++i)
+                               "-", "-", "LP4P0B4", "LP2P1B6", "LPD4P1B4"};
+        for (int i = 0; i < 13; ++i)
             if (!std::strcmp(e, names[i])) return i;
         return -1;
     }();
@@ -967,55 +864,52 @@ void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles, m->sched));
 }
 
-template <typename T, int J, int B>
-void launch_pipex(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    int dev = 0, sms = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = pipex_smem_bytes(m, J, B, sizeof(T));
-    auto kern = spmv_pipex_kernel<T, J, B>;
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, smem));
-    const unsigned grid = unsigned(std::min<uint64_t>(m->num_tiles, uint64_t(std::max(per_sm, 1)) * sms));
-    if (grid == 0) return;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(B);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    cfg.numAttrs = 0;
-    const size_t xbytes = m->num_cols * sizeof(T);
-    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
-        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
-        attr[0].val.accessPolicyWindow.num_bytes = win;
-        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
-    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles));
+int tma_threads() {
+    static const int nt = [] {
+        const char* e = std::getenv("ARGCSR_TMA_THREADS");
+        const int v = e ? std::atoi(e) : 256;
+        return (v == 512 || v == 1024) ? v : 256;
+    }();
+    return nt;
+}
+int tma_ctas_per_sm() {  // resident CTAs per SM the stages are sized for
+    static const int c = [] {
+        const char* e = std::getenv("ARGCSR_TMA_CTAS");
+        const int v = e ? std::atoi(e) : 2;
+        return std::min(std::max(v, 1), 8);
+    }();
+    return c;
 }
 
-template <typename T, int J>
-void launch_pipe(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    int dev = 0, sms = 0;
+// Returns false when the handle has no TMA schedule or two stages do not fit.
+template <typename T, int V, int NT>
+bool launch_tma_nt(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    int dev = 0, sms = 0, optin = 0;
     CUDA_OK(cudaGetDevice(&dev));
     CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = pipe_smem_bytes(m, J, sizeof(T));
-    auto kern = spmv_pipe_kernel<T, J>;
+    CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    auto kern = spmv_tma_kernel<T, V, NT>;
+    int per_sm_smem = 0;
+    CUDA_OK(cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    const uint32_t SB = m->stage_bytes;
+    if (SB == 0) return false;
+    // stages per CTA: as many as fit (<= 4) with tma_ctas_per_sm() CTAs per SM,
+    // at least 2 (fewer CTAs per SM if needed)
+    uint32_t nst = 0;
+    for (int ctas = tma_ctas_per_sm(); ctas >= 1 && nst < 2; --ctas) {
+        const size_t budget = std::min<size_t>(size_t(optin), size_t(per_sm_smem) / ctas) - 1024;
+        nst = uint32_t(std::min<size_t>(4, budget / SB));
+    }
+    if (nst < 2) return false;
+    const size_t smem = size_t(nst) * SB;
     CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileThreads, smem));
-    const unsigned grid = unsigned(std::min<uint64_t>(m->num_tiles, uint64_t(std::max(per_sm, 1)) * sms));
-    if (grid == 0) return;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    const unsigned grid = unsigned(std::min<uint64_t>(m->num_ttiles, uint64_t(std::max(per_sm, 1)) * sms));
+    if (grid == 0) return true;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kTileThreads);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1032,37 +926,31 @@ void launch_pipe(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
-    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles));
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, nst));
+    return true;
+}
+
+template <typename T, int V>
+bool launch_tma(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    if (m->layout != kLayoutCompact || m->num_ttiles == 0) return false;
+    switch (tma_threads()) {
+        case 256: return launch_tma_nt<T, V, 256>(m, a, s);
+        case 1024: return launch_tma_nt<T, V, 1024>(m, a, s);
+        default: return launch_tma_nt<T, V, 512>(m, a, s);
+    }
 }
 
 template <typename T, int V>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     int vid = variant_id();
+    // Opt-in experiment (measured slower): the TMA-staged kernel.
+    const char* ev = std::getenv("ARGCSR_SPMV_VARIANT");
+    if (ev && !std::strcmp(ev, "TMA") && launch_tma<T, V>(m, a, s)) return;
     if (vid < 0) {
         // Default: persistent CTAs with prefetched metadata and dynamic tile
         // order when there are no heavy groups (e.g. stencils); otherwise
         // hardware dispatch of independent tiles (measured best for R-MAT).
         vid = m->num_heavy == 0 ? 12 : 6;
-    }
-    if constexpr (V == 4) {
-        if (vid == 13 || vid == 14) {
-            // one unit per thread: tiles must have been built for the CTA size
-            if (m->tile_threads == 128 && m->max_tile_units <= 128) {
-                if (vid == 13) launch_pipex<T, 4, 128>(m, a, s);
-                else launch_pipex<T, 2, 128>(m, a, s);
-                return;
-            }
-            if (m->max_tile_units <= 256) {
-                if (vid == 13) launch_pipex<T, 4, 256>(m, a, s);
-                else launch_pipex<T, 2, 256>(m, a, s);
-                return;
-            }
-        }
-        if (m->max_tile_units <= uint64_t(kTileThreads) && (vid == 8 || vid == 9)) {
-            if (vid == 8) launch_pipe<T, 2>(m, a, s);
-            else launch_pipe<T, 4>(m, a, s);
-            return;
-        }
     }
     switch (vid) {
         case 0: launch_lightp<T, V, 4, true, 4, false>(m, a, s); return;
@@ -1097,9 +985,11 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.tiles = m->tiles;
     a.heavy = m->heavy;
     a.heavy_ptr = m->heavy_ptr;
+    a.ttiles = m->ttiles;
+    a.num_ttiles = m->num_ttiles;
+    a.stage_bytes = m->stage_bytes;
     a.x = static_cast<const T*>(x);
     a.y = static_cast<T*>(y);
-    a.tpg = m->tpg;
     a.heavy_ctas = m->heavy_ctas;
     a.g_begin = gb;
     a.g_end = ge;

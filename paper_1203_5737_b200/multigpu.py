@@ -74,7 +74,8 @@ def slice_rows(row_pointers, columns, values, num_cols: int, r0: int, r1: int) -
 class DeviceEngine:
     """The product engine: this rank's slice converted and multiplied on its GPU."""
 
-    def __init__(self, sl: CsrSlice, tpg: int, dcs: int, device: torch.device, dtype=torch.float64):
+    def __init__(self, sl: CsrSlice, tpg: int, dcs: int, device: torch.device, dtype=torch.float64,
+                 layout: str = "compact"):
         import paper_1203_5737_b200 as argcsr
 
         self.device = device
@@ -86,7 +87,8 @@ class DeviceEngine:
         self.stream = torch.cuda.current_stream(device)
         self.m = argcsr.argcsr_from_torch(sl.num_rows, sl.num_cols, rp.to(device).contiguous(),
                                           cols.to(device, torch.int32).contiguous(),
-                                          vals.to(device, dtype).contiguous(), tpg, dcs, stream=self.stream)
+                                          vals.to(device, dtype).contiguous(), tpg, dcs, stream=self.stream,
+                                          layout=layout)
 
     def spmv(self, x: torch.Tensor, y: torch.Tensor, x_scale: Optional[torch.Tensor] = None) -> None:
         """y = A (s * x), s = x_scale[0] read on the device (None: 1)."""
@@ -100,7 +102,8 @@ class DistributedArgCsr:
 
     def __init__(self, num_rows: int, num_cols: int, row_pointers, columns, values, tpg: int = 128, dcs: int = 1,
                  group=None, device: Optional[torch.device] = None,
-                 engine_factory: Optional[Callable[[CsrSlice], object]] = None, dtype=torch.float64):
+                 engine_factory: Optional[Callable[[CsrSlice], object]] = None, dtype=torch.float64,
+                 layout: str = "compact"):
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized()
         self.world = dist.get_world_size(group) if self.distributed else 1
@@ -115,7 +118,7 @@ class DistributedArgCsr:
         self.nnz_total = int(rp_host[-1] - rp_host[0])
         if engine_factory is None:
             dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-            self.engine = DeviceEngine(self.slice, tpg, dcs, dev, dtype)
+            self.engine = DeviceEngine(self.slice, tpg, dcs, dev, dtype, layout)
         else:
             self.engine = engine_factory(self.slice)
         self.device = self.engine.device

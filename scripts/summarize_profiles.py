@@ -73,7 +73,8 @@ def main(tag):
         lines, t = summarize(rep)
         (PROF / f"{tag}_ncu_{cfg}.txt").write_text("\n".join(lines) + "\n")
         c, d = cfg.split("_dcs")
-        traffic[f"{c}_tpg128_dcs{d}"] = int(t)
+        d, _, layout = d.partition("_")
+        traffic[f"{c}_tpg128_dcs{d}_{layout or 'reference'}"] = int(t)
         print(cfg, f"traffic/step = {t / 1e9:.3f} GB")
     for f in sorted(OUT.glob(f"{tag}_launches_*.csv")):
         rows = [r for r in csv.reader(open(f)) if r and r[0].isdigit()]

@@ -70,9 +70,12 @@ def stencil27(n: int) -> Csr:
     return Csr(n**3, n**3, np.cumsum(rp).astype(np.uint64), c.astype(np.int32), v)
 
 
-def to_dev(argcsr, A: Csr, tpg: int, dcs: int, dtype=np.float64):
+LAYOUTS = ("compact", "reference")
+
+
+def to_dev(argcsr, A: Csr, tpg: int, dcs: int, dtype=np.float64, layout: str = "compact"):
     return argcsr.argcsr_from_csr(
-        (A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.astype(dtype)), tpg, dcs)
+        (A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.astype(dtype)), tpg, dcs, layout=layout)
 
 
 def assert_same_layout(dev, ref_m: oracle.ArgCsr, where: str = "") -> None:

@@ -11,7 +11,7 @@ checked against the oracle's CSR product as well.
 import numpy as np
 import pytest
 
-from helpers import assert_same_layout, bits, np_corpus, powerlaw_csr, stencil27, to_dev
+from helpers import LAYOUTS, assert_same_layout, bits, np_corpus, powerlaw_csr, stencil27, to_dev
 from oracle import Csr
 
 pytestmark = pytest.mark.gpu
@@ -121,15 +121,25 @@ def test_spmv_agrees_with_reference_e8(argcsr, orc):  # python/test_smoke.py:21-
 GRID = [(t, d) for t in (1, 3, 4, 12, 32, 128) for d in (1, 2, 4, 32)]
 
 
-def _check_case(argcsr, orc, A, tpg, dcs, where):
+def _check_case(argcsr, orc, A, tpg, dcs, where, layouts=LAYOUTS):
+    """Both device layouts: exported arrays byte-equal to the oracle's, SpMV
+    bit-identical to the reference order and within the north_star bound."""
     ref_m = orc.argcsr_from_csr(A, tpg, dcs)
-    dev = to_dev(argcsr, A, tpg, dcs)
-    assert_same_layout(dev, ref_m, where)
     x = np.linspace(-1.5, 2.5, A.num_cols) if A.num_cols > 1 else np.array([1.25])
-    y = argcsr.spmv(dev, x)
-    assert bits(y) == bits(orc.spmv_argcsr(ref_m, x)), f"{where}: SpMV not bit-identical"
+    y_ref = orc.spmv_argcsr(ref_m, x)
     y_csr = orc.spmv_csr(A, x)
-    assert within_bound(y, y_csr, orc.abs_row_sums(A, x), FP64_TOL), f"{where}: outside 1e-12 bound"
+    for layout in layouts:
+        dev = to_dev(argcsr, A, tpg, dcs, layout=layout)
+        w = f"{where} [{layout}]"
+        assert dev.layout == layout
+        assert_same_layout(dev, ref_m, w)
+        if layout == "reference":
+            assert dev.stored_slots == dev.total_slots
+        else:
+            assert dev.stored_slots <= dev.total_slots
+        y = argcsr.spmv(dev, x)
+        assert bits(y) == bits(y_ref), f"{w}: SpMV not bit-identical"
+        assert within_bound(y, y_csr, orc.abs_row_sums(A, x), FP64_TOL), f"{w}: outside 1e-12 bound"
     return dev
 
 
@@ -148,8 +158,8 @@ def test_numpy_corpus_grid(argcsr, orc):
 
 def test_round_trip_corpus(argcsr, corpus):  # test_argcsr.cpp:190-201, acceptance criterion 4
     for A in corpus[:100]:
-        for tpg, dcs in ((4, 1), (32, 4), (128, 32)):
-            m = to_dev(argcsr, A, tpg, dcs)
+        for (tpg, dcs), layout in zip(((4, 1), (32, 4), (128, 32), (128, 1)), LAYOUTS * 2):
+            m = to_dev(argcsr, A, tpg, dcs, layout=layout)
             rp, cols, vals = argcsr.csr_arrays_from_argcsr(m)
             assert np.array_equal(rp, A.row_pointers)
             assert np.array_equal(cols, A.columns)
@@ -248,8 +258,8 @@ def test_spmv_groups_writes_only_its_rows(argcsr, orc):
 
 def test_padding_stats_matches_reference(argcsr, orc, ref, corpus):
     for A in corpus[:60]:
-        for tpg, dcs in ((4, 1), (32, 4), (128, 1)):
-            m = to_dev(argcsr, A, tpg, dcs)
+        for (tpg, dcs), layout in ((t, l) for t in ((4, 1), (32, 4), (128, 1)) for l in LAYOUTS):
+            m = to_dev(argcsr, A, tpg, dcs, layout=layout)
             want = ref.padding_stats(orc.argcsr_from_csr(A, tpg, dcs))
             got = argcsr.padding_stats(m)
             assert got.explicit_nnz == want["explicit_nnz"]
@@ -263,10 +273,11 @@ def test_padding_stats_matches_reference(argcsr, orc, ref, corpus):
 def test_chunk_entries_match_reference(argcsr, orc, ref, corpus):
     for A in corpus[1:30]:
         ref_m = orc.argcsr_from_csr(A, 32, 4)
-        m = to_dev(argcsr, A, 32, 4)
-        for g in range(0, m.num_groups, max(1, m.num_groups // 5)):
-            for c in (0, 5, 31):
-                assert argcsr.chunk_entries(m, g, c) == ref.chunk_entries(ref_m, g, c)
+        for layout in LAYOUTS:
+            m = to_dev(argcsr, A, 32, 4, layout=layout)
+            for g in range(0, m.num_groups, max(1, m.num_groups // 5)):
+                for c in (0, 5, 31):
+                    assert argcsr.chunk_entries(m, g, c) == ref.chunk_entries(ref_m, g, c), (layout, g, c)
 
 
 def test_determinism(argcsr):
@@ -286,9 +297,9 @@ def test_fp32_handle(argcsr, orc):
     A = powerlaw_csr(30000, 25000, seed=9, heavy_rows=[(4, 20000)])
     A32 = Csr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.astype(np.float32).astype(np.float64))
     x32 = np.sin(np.arange(A.num_cols)).astype(np.float32)
-    for tpg, dcs in ((128, 1), (128, 8), (32, 1)):
+    for (tpg, dcs), layout in ((t, l) for t in ((128, 1), (128, 8), (32, 1)) for l in LAYOUTS):
         ref_m = orc.argcsr_from_csr(A32, tpg, dcs)
-        dev = to_dev(argcsr, A32, tpg, dcs, dtype=np.float32)
+        dev = to_dev(argcsr, A32, tpg, dcs, dtype=np.float32, layout=layout)
         assert dev.dtype == "float32"
         assert np.array_equal(dev.groups_array, ref_m.groups)
         assert np.array_equal(dev.threads_mapping, ref_m.threads_mapping)

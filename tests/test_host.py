@@ -30,7 +30,7 @@ def test_c_abi_library_exports_every_declared_symbol(argcsr):
     for s in declared_symbols():
         assert hasattr(lib, s), f"{s} not exported"
     lib.argcsr_abi_version.restype = ctypes.c_int
-    assert lib.argcsr_abi_version() == 1
+    assert lib.argcsr_abi_version() == 2
 
 
 def test_library_is_sm100a():

@@ -74,7 +74,6 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->heavy);
     cudaFree(m->heavy_ptr);
     cudaFree(m->sched);
-    cudaFree(m->ttiles);
     if (m->aux) cudaStreamDestroy(m->aux);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);

@@ -56,20 +56,7 @@ struct alignas(16) GroupDesc {
     __host__ __device__ __forceinline__ bool heavy() const { return (off_stride & kHeavyBit) != 0; }
 };
 
-// One tile of the lane-compact TMA SpMV (spmv.cu): a run of consecutive
-// groups [gs, gs + ng) whose light slots are the contiguous stored range
-// [slot_begin, slot_begin + nslots) (heavy groups are stored after all light
-// groups, so they never sit inside a tile's range), rows [row0, row0 + nrows)
-// and light units [ub0, ub0 + nunits).  Built by the converter.
-struct alignas(16) TileDesc {
-    uint64_t slot_begin;
-    uint64_t ub0;
-    uint32_t gs, ng;
-    uint32_t row0, nrows;
-    uint32_t nslots, nunits;
-    uint32_t pad0, pad1;
-};
-static_assert(sizeof(TileDesc) == 48, "TileDesc must be 48 bytes");
+
 static_assert(sizeof(GroupDesc) == 16, "GroupDesc must be 16 bytes");
 
 enum Layout : int { kLayoutCompact = 0, kLayoutReference = 1 };
@@ -77,12 +64,13 @@ enum Layout : int { kLayoutCompact = 0, kLayoutReference = 1 };
 // Device limits (documented in DESIGN.md).  threads_per_group bounds the
 // shared-memory partial-sum staging of the SpMV; rows are u32 on the device.
 constexpr uint64_t kMaxThreadsPerGroup = 16384;
-// Groups with chunk_size above this run on the long-chunk (heavy) path, and so
-// do lane-compact groups whose staged block would exceed kLightMaxBytes.
+// Groups with chunk_size above this run on the long-chunk (heavy) path.
 constexpr uint32_t kHeavyChunk = 32;
-constexpr uint64_t kLightMaxBytes = 56 * 1024;
-// Units (V-lane quads) per light tile = threads per SpMV CTA.
+// Threads per SpMV CTA, and the default number of units (V-lane vectors) per
+// light tile: a tile is walked by one CTA, two units per thread (measured best
+// on the stencil and power-law configs, profiles/ and DESIGN.md §4).
 constexpr int kTileThreads = 256;
+constexpr int kDefaultTileUnits = 512;
 
 }  // namespace argcsr_gpu
 
@@ -120,12 +108,7 @@ struct argcsr_dev {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     uint32_t* sched = nullptr;            // [2] dynamic tile counter + done counter (self-resetting)
 
-    // Lane-compact TMA schedule: tiles of whole groups, bulk-copied into
-    // shared-memory stages of stage_bytes (see spmv.cu).
-    argcsr_gpu::TileDesc* ttiles = nullptr;  // [num_ttiles]
-    uint32_t num_ttiles = 0;
-    uint32_t stage_bytes = 0;
-    uint64_t light_slots = 0;             // stored slots of light groups (they come first)
+    uint64_t light_slots = 0;             // stored slots of light groups (stored first)
 
     // x residency (L2 persisting window) — queried, not hard-coded.
     size_t l2_persist_max = 0;

@@ -265,20 +265,12 @@ struct StrideOf {
     }
 };
 
-// Long-chunk groups run on the heavy path; in the lane-compact layout so do
-// groups whose staged block (slots + per-lane partial sums) would not leave
-// room for a useful tile in a shared-memory stage.
+// Long-chunk groups (chunk_size > kHeavyChunk) run on the heavy path.
 template <typename TM>
 struct HeavyOf {
     const uint32_t* chunk;
     StrideOf<TM> stride;
-    uint32_t slot_bytes;  // value + column bytes per slot
-    __device__ bool operator()(uint64_t g) const {
-        if (chunk[g] > kHeavyChunk) return true;
-        if (!stride.compact) return false;
-        const uint64_t w = stride(g);
-        return uint64_t(chunk[g]) * w * slot_bytes + 8 * w > kLightMaxBytes;
-    }
+    __device__ bool operator()(uint64_t g) const { return chunk[g] > kHeavyChunk; }
 };
 
 struct SlotsOf {  // chunk_size * threads_per_group (argcsr.cpp:151-152)
@@ -392,90 +384,6 @@ __global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, uns
     if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
 }
 
-// ------------------------------------------------------ lane-compact TMA tiles
-// Shared-memory bytes group g adds to a tile: descriptor, unit base, its rows'
-// threads_mapping entries and, for a light group, its slots and per-lane
-// partial sums.  Tiles cut this running sum every `span` bytes.
-template <typename TM>
-struct TileBytesOf {
-    const uint32_t* first_row;
-    HeavyOf<TM> heavy;
-    __device__ uint64_t operator()(uint64_t g) const {
-        uint64_t b = sizeof(GroupDesc) + sizeof(uint64_t) + 2 * uint64_t(first_row[g + 1] - first_row[g]);
-        if (!heavy(g)) {
-            const uint64_t w = heavy.stride(g);
-            b += uint64_t(heavy.chunk[g]) * w * heavy.slot_bytes + 8 * w;
-        }
-        return b;
-    }
-};
-
-template <typename TM>
-__global__ void k_max_tile_bytes(TileBytesOf<TM> f, uint32_t G, unsigned long long* __restrict__ out) {
-    uint64_t m = 0;
-    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G; g += uint64_t(gridDim.x) * blockDim.x)
-        m = max(m, f(g));
-    m = warp_max_u64(m);
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
-}
-
-// Group g opens a tile when it is light and the running byte sum crosses a
-// multiple of `span` at g, or g follows a heavy group (or is group 0).  A tile
-// runs to the next opening or heavy group, so tiles hold light groups only and
-// their stored slots are one contiguous range.
-template <typename TM>
-struct OpensTile {
-    const uint64_t* key;
-    HeavyOf<TM> heavy;
-    uint64_t span;
-    __device__ uint64_t operator()(uint64_t g) const {
-        if (heavy(g)) return 0;
-        if (g == 0 || heavy(g - 1)) return 1;
-        return key[g] / span != key[g - 1] / span ? 1 : 0;
-    }
-};
-
-// Section bytes of a bulk copy of `bytes` starting at global address `addr`
-// (16-B aligned down and up).  Must match the SpMV's staging.
-__device__ __forceinline__ uint64_t staged(uint64_t addr, uint64_t bytes) {
-    return bytes == 0 ? 0 : ((addr + bytes + 15) & ~uint64_t(15)) - (addr & ~uint64_t(15));
-}
-
-template <typename TM>
-__global__ void k_fill_tiles(OpensTile<TM> opens, const uint64_t* __restrict__ pos, uint32_t G,
-                             const GroupDesc* __restrict__ desc, const uint64_t* __restrict__ unit_base,
-                             const TM* __restrict__ tm_base, const void* cols_base, const void* vals_base,
-                             uint32_t val_bytes, uint32_t V, TileDesc* __restrict__ tiles,
-                             unsigned long long* __restrict__ max_stage) {
-    uint64_t mx = 0;
-    for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G; g += uint64_t(gridDim.x) * blockDim.x) {
-        if (!opens(g)) continue;
-        uint64_t ge = g + 1;
-        while (ge < G && !opens.heavy(ge) && !opens(ge)) ++ge;
-        TileDesc t;
-        t.gs = uint32_t(g);
-        t.ng = uint32_t(ge - g);
-        t.slot_begin = desc[g].offset();
-        uint64_t last_end = desc[ge - 1].offset() + uint64_t(desc[ge - 1].chunk) * desc[ge - 1].stride();
-        t.nslots = uint32_t(last_end - t.slot_begin);
-        t.row0 = desc[g].first_row;
-        t.nrows = desc[ge].first_row - t.row0;
-        t.ub0 = unit_base[g];
-        t.nunits = uint32_t(unit_base[ge] - t.ub0);
-        t.pad0 = t.pad1 = 0;
-        tiles[pos[g]] = t;
-        const uint64_t b = staged(uint64_t(desc + g), sizeof(GroupDesc) * (uint64_t(t.ng) + 1)) +
-                           staged(uint64_t(unit_base + g), sizeof(uint64_t) * (uint64_t(t.ng) + 1)) +
-                           staged(uint64_t(tm_base + t.row0), sizeof(TM) * uint64_t(t.nrows)) +
-                           staged(uint64_t(cols_base) + 4 * t.slot_begin, 4 * uint64_t(t.nslots)) +
-                           staged(uint64_t(vals_base) + val_bytes * t.slot_begin, uint64_t(val_bytes) * t.nslots) +
-                           ((8 * uint64_t(t.nunits) * V + 15) & ~uint64_t(15));
-        mx = max(mx, b);
-    }
-    mx = warp_max_u64(mx);
-    if ((threadIdx.x & 31) == 0) atomicMax(max_stage, (unsigned long long)mx);
-}
-
 // ------------------------------------------------------------------- K5
 // Gather form of layout_group: lane l of group g belongs to the row whose
 // threads_mapping range holds l; its chunk c holds the row's elements
@@ -550,12 +458,12 @@ __global__ void __launch_bounds__(256) k5_layout(const uint64_t* __restrict__ rp
     }
 }
 
-// Units per light tile (= threads of the one-unit-per-thread SpMV kernels).
-// ARGCSR_TILE_THREADS=128 builds smaller tiles for the slab-pipelined kernel.
+// Units per light tile (default kDefaultTileUnits; a tile is one CTA of kTileThreads).
+// ARGCSR_TILE_THREADS (128 .. 2048) sets the units per tile (experiments).
 uint64_t tile_threads_setting() {
     const char* e = std::getenv("ARGCSR_TILE_THREADS");
     const long v = e ? std::atol(e) : 0;
-    return (v == 128 || v == 256) ? uint64_t(v) : uint64_t(kTileThreads);
+    return (v == 128 || v == 256 || v == 512 || v == 1024 || v == 2048) ? uint64_t(v) : uint64_t(kDefaultTileUnits);
 }
 
 unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
@@ -581,51 +489,6 @@ P* dev_alloc(argcsr_dev* m, size_t n) {
     CUDA_OK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(P)));
     m->device_bytes += std::max<size_t>(n, 1) * sizeof(P);
     return p;
-}
-
-// Tiles of the lane-compact TMA SpMV: cut the running tile-byte sum every
-// `span` bytes, where span leaves room for the largest group so that every
-// tile fits a stage of about kStageTarget bytes (at least kMinSpan of tiles).
-constexpr uint64_t kStageTarget = 36 * 1024;
-constexpr uint64_t kMinSpan = 16 * 1024;
-
-template <typename T, typename TM>
-void build_tma_tiles(argcsr_dev* m, const uint32_t* first_row, const uint64_t* off_light, HeavyOf<TM> heavy_of,
-                     cudaStream_t s) {
-    const uint32_t G = uint32_t(m->num_groups);
-    const TileBytesOf<TM> tb{first_row, heavy_of};
-    DevPtr<unsigned long long> mx(2, s);
-    CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
-    k_max_tile_bytes<TM><<<grid_for(G, 256), 256, 0, s>>>(tb, G, mx.p);
-    LAUNCH_OK("k_max_tile_bytes");
-    DevPtr<uint64_t> key(uint64_t(G) + 1, s);
-    exclusive_scan(tb, G, key.p, s);
-    unsigned long long maxg = 0;
-    uint64_t total = 0;
-    CUDA_OK(cudaMemcpyAsync(&maxg, mx.p, sizeof maxg, cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaMemcpyAsync(&total, key.p + G, sizeof total, cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaStreamSynchronize(s));
-    const char* e = std::getenv("ARGCSR_TMA_STAGE");  // experiments: target stage bytes
-    const uint64_t target = e ? uint64_t(std::atol(e)) : kStageTarget;
-    const uint64_t span = std::max<uint64_t>(kMinSpan, target > maxg ? target - maxg : 0);
-    const OpensTile<TM> opens{key.p, heavy_of, span};
-    DevPtr<uint64_t> pos(uint64_t(G) + 1, s);
-    exclusive_scan(opens, G, pos.p, s);
-    uint64_t nt = 0;
-    CUDA_OK(cudaMemcpyAsync(&nt, pos.p + G, sizeof nt, cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaStreamSynchronize(s));
-    if (nt == 0 || nt > 0x7fffffffull) return;
-    m->ttiles = dev_alloc<TileDesc>(m, nt);
-    m->num_ttiles = uint32_t(nt);
-    k_fill_tiles<TM><<<grid_for(G, 256), 256, 0, s>>>(opens, pos.p, G, m->groups, m->unit_base,
-                                                      static_cast<const TM*>(m->tm), m->columns, m->values,
-                                                      uint32_t(sizeof(T)), uint32_t(m->lanes_per_unit), m->ttiles,
-                                                      mx.p + 1);
-    LAUNCH_OK("k_fill_tiles");
-    unsigned long long st = 0;
-    CUDA_OK(cudaMemcpyAsync(&st, mx.p + 1, sizeof st, cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaStreamSynchronize(s));
-    m->stage_bytes = uint32_t((st + 127) & ~127ull);
 }
 
 template <typename T, typename TM>
@@ -668,7 +531,7 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     LAUNCH_OK("k_set_u32");
 
     // K3
-    TM* tm = dev_alloc<TM>(m, N + 8);  // +8: 16-B overread of the TMA staging
+    TM* tm = dev_alloc<TM>(m, N);
     TM* assigned = dev_alloc<TM>(m, G);
     m->tm = tm;
     m->assigned = assigned;
@@ -685,9 +548,8 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     const bool compact = m->layout == kLayoutCompact;
     // (V divides tpg, so a compact stride never exceeds threads_per_group)
     const uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
-    const uint32_t slot_bytes = uint32_t(sizeof(T) + sizeof(int32_t));  // staged bytes per slot
     const StrideOf<TM> stride_of{assigned, tpg, V, compact};
-    const HeavyOf<TM> heavy_of{chunk.p, stride_of, slot_bytes};
+    const HeavyOf<TM> heavy_of{chunk.p, stride_of};
     DevPtr<uint64_t> offset(uint64_t(G) + 1, s);
     exclusive_scan(SlotsOf{chunk.p, tpg}, G, offset.p, s);  // reference offsets
     uint64_t total_slots = 0;
@@ -729,7 +591,7 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
 
     // SpMV schedule: work units (V lanes), light tiles, heavy groups (LPT order).
     m->lanes_per_unit = int(V);
-    m->unit_base = dev_alloc<uint64_t>(m, uint64_t(G) + 3);  // +2: 16-B overread of the TMA staging
+    m->unit_base = dev_alloc<uint64_t>(m, uint64_t(G) + 1);
     exclusive_scan(UnitsOf<TM>{assigned, heavy_of, V}, G, m->unit_base, s);
     uint64_t total_units = 0;
     CUDA_OK(cudaMemcpyAsync(&total_units, m->unit_base + G, sizeof total_units, cudaMemcpyDeviceToHost, s));
@@ -807,10 +669,9 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
         m->max_tile_units = span + maxu - 1;
     }
 
-    // K5 (+8 slots: 16-B overread of the TMA staging)
-    m->values = dev_alloc<T>(m, stored_slots + 8);
-    m->columns = dev_alloc<int32_t>(m, stored_slots + 8);
-    if (compact && G > 0) build_tma_tiles<T, TM>(m, first_row.p, offset.p, heavy_of, s);
+    // K5
+    m->values = dev_alloc<T>(m, stored_slots);
+    m->columns = dev_alloc<int32_t>(m, stored_slots);
     if (G > 0 && stored_slots > 0) {
         const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
         k5_layout<T, TM><<<grid, 256, 0, s>>>(rp, cols, vals, m->groups, tm, assigned, G,

@@ -45,9 +45,6 @@ struct SpmvArgs {
     const uint32_t* __restrict__ tiles;
     const uint32_t* __restrict__ heavy;
     const uint32_t* __restrict__ heavy_ptr;
-    const TileDesc* __restrict__ ttiles;  // lane-compact TMA tiles
-    uint32_t num_ttiles;
-    uint32_t stage_bytes;
     const T* __restrict__ x;
     T* __restrict__ y;
     uint32_t heavy_ctas;
@@ -494,276 +491,6 @@ template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
 void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s);
 
 
-// ------------------------------------------- lane-compact TMA path (default)
-// Persistent CTAs (one per SM) walk the tiles k = blockIdx.x, +gridDim.x, ...
-// A tile is a run of whole light groups whose value/column blocks are ONE
-// contiguous stored range in the lane-compact layout.  One elected thread
-// stages a tile into a shared-memory stage with five cp.async.bulk copies
-// (group descriptors, unit bases, threads_mapping of its rows, columns,
-// values) completing on the stage's mbarrier; `nstages` stages are kept in
-// flight, so the HBM stream runs ahead of the x gathers and the reduction
-// (they never wait on each other except through a full ring).  Consumers:
-//   phase 1  one V-lane unit per thread and step, columns/values from shared
-//            memory, 4 element steps (4V x gathers) in flight, partial sums
-//            per lane to the stage's partial section;
-//   phase 2  one row per thread, +0.0 + p_b + ... ascending (bit-exact order).
-struct StageHdr {
-    uint32_t p_desc, p_ub, p_tm, p_cols, p_vals, p_part;
-    uint32_t gs, ng, row0, nrows, nunits, nslots;
-    uint64_t ub0, slot_begin;
-};
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, uint64_t src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-
-// Stage tile k: header + bulk copies (16-B aligned-down/up sections; the
-// device arrays carry 16 B of tail padding for the round-up).
-template <typename T, int V>
-__device__ __forceinline__ void tma_issue(const SpmvArgs<T>& a, const TileDesc& t, unsigned char* stage,
-                                          StageHdr* hdr, uint64_t* bar, uint64_t pol_meta, uint64_t pol_stream) {
-    const uint64_t src[5] = {uint64_t(a.groups + t.gs), uint64_t(a.unit_base + t.gs), uint64_t(a.tm + t.row0),
-                             uint64_t(a.cols + t.slot_begin), uint64_t(a.vals + t.slot_begin)};
-    const uint64_t len[5] = {sizeof(GroupDesc) * (uint64_t(t.ng) + 1), sizeof(uint64_t) * (uint64_t(t.ng) + 1),
-                             sizeof(uint16_t) * uint64_t(t.nrows), sizeof(int32_t) * uint64_t(t.nslots),
-                             sizeof(T) * uint64_t(t.nslots)};
-    uint64_t lo[5];
-    uint32_t n[5], p[5], off = 0, total = 0;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        lo[i] = src[i] & ~uint64_t(15);
-        n[i] = len[i] ? uint32_t(((src[i] + len[i] + 15) & ~uint64_t(15)) - lo[i]) : 0u;
-        p[i] = off + uint32_t(src[i] - lo[i]);
-        off += n[i];
-        total += n[i];
-    }
-    hdr->p_desc = p[0], hdr->p_ub = p[1], hdr->p_tm = p[2], hdr->p_cols = p[3], hdr->p_vals = p[4];
-    hdr->p_part = off;
-    hdr->gs = t.gs, hdr->ng = t.ng, hdr->row0 = t.row0, hdr->nrows = t.nrows, hdr->nunits = t.nunits;
-    hdr->nslots = t.nslots;
-    hdr->ub0 = t.ub0, hdr->slot_begin = t.slot_begin;
-    mbar_arrive_expect_tx(bar, total);
-    off = 0;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        if (n[i]) bulk_g2s(stage + off, lo[i], n[i], bar, i >= 3 ? pol_stream : pol_meta);
-        off += n[i];
-    }
-}
-
-template <typename T, int V> struct SmemVec;
-template <> struct SmemVec<double, 4> {
-    static __device__ __forceinline__ void load(const double* p, double (&v)[4]) {
-        const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
-        v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
-    }
-};
-template <> struct SmemVec<float, 4> {
-    static __device__ __forceinline__ void load(const float* p, float (&v)[4]) {
-        const float4 a = *reinterpret_cast<const float4*>(p);
-        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
-    }
-};
-
-template <typename T, int V, int NT>
-__global__ void __launch_bounds__(NT) spmv_tma_kernel(const SpmvArgs<T> a, uint32_t nstages) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[4];
-    __shared__ StageHdr hdrs[4];
-    const uint32_t tid = threadIdx.x;
-    const uint32_t G = gridDim.x;
-    const uint32_t SB = a.stage_bytes;
-    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_meta = policy_evict_normal();
-    const double xs = a.x_scale ? *a.x_scale : 1.0;
-    const uint32_t mine = a.num_ttiles > blockIdx.x ? (a.num_ttiles - blockIdx.x + G - 1) / G : 0;
-    if (tid == 0) {
-        for (uint32_t s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (uint32_t i = 0; i < nstages && i < mine; ++i)
-            tma_issue<T, V>(a, a.ttiles[blockIdx.x + i * G], smem + size_t(i) * SB, &hdrs[i], &bars[i], pol_meta,
-                            pol_stream);
-    }
-    __syncthreads();
-    for (uint32_t i = 0; i < mine; ++i) {
-        const uint32_t st = i % nstages;
-        mbar_wait(&bars[st], (i / nstages) & 1);
-        unsigned char* stage = smem + size_t(st) * SB;
-        const StageHdr h = hdrs[st];
-        // the descriptor of the tile this stage is refilled with, loaded now
-        // so that its latency is off the end-of-tile critical path
-        TileDesc nxt;
-        const bool refill = tid == 0 && i + nstages < mine;
-        if (refill) nxt = a.ttiles[blockIdx.x + (i + nstages) * G];
-        const GroupDesc* sd = reinterpret_cast<const GroupDesc*>(stage + h.p_desc);
-        const uint64_t* sub = reinterpret_cast<const uint64_t*>(stage + h.p_ub);
-        const uint16_t* stm = reinterpret_cast<const uint16_t*>(stage + h.p_tm);
-        const int32_t* scol = reinterpret_cast<const int32_t*>(stage + h.p_cols);
-        const T* sval = reinterpret_cast<const T*>(stage + h.p_vals);
-        double* spart = reinterpret_cast<double*>(stage + h.p_part);
-        const uint32_t ns = h.nslots;
-
-        // Phase 1 (argcsr.cpp:193-203).  A unit is V adjacent lanes of a
-        // group; its steps j = 0 .. chunk-1 are the V-slot vectors
-        // offset + j * stride + V * u.  Units are dealt out balanced by steps:
-        // in the unit-major order of the tile's steps, thread t owns the units
-        // that START in [t, t + 1) * steps / NT and runs them to the end.  A
-        // thread walks its steps in batches of kB (kB * V gathers in flight),
-        // batches crossing unit boundaries; each lane's sum is a sequential
-        // chain over j ascending from +0.0, stopping at sentinels (which are
-        // trailing), exactly the reference's.
-        {
-            constexpr uint32_t kB = 4;
-            const uint32_t nq = ns / V;  // steps of the tile
-            const uint32_t qb = uint32_t(uint64_t(nq) * tid / NT), qe = uint32_t(uint64_t(nq) * (tid + 1) / NT);
-            // group holding virtual step qb: last gi with (offset - slot_begin) / V <= qb
-            uint32_t gi = 0;
-            {
-                uint32_t lo = 0, hi = h.ng - 1;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi + 1) / 2;
-                    if (uint32_t((sd[mid].offset() - h.slot_begin) / V) <= qb) lo = mid; else hi = mid - 1;
-                }
-                gi = lo;
-            }
-            GroupDesc d = sd[gi];
-            uint32_t chunk = d.chunk, wv = d.stride() / V;
-            uint32_t gq0 = uint32_t((d.offset() - h.slot_begin) / V);
-            uint32_t ub = uint32_t(sub[gi] - h.ub0);
-            // first unit of this group starting at or after qb
-            uint32_t ul = chunk ? (qb - gq0 + chunk - 1) / chunk : wv;
-            uint32_t j = 0;
-            bool more = qb < qe;
-            auto next_group = [&]() {
-                for (;;) {
-                    if (++gi >= h.ng) {
-                        more = false;
-                        return;
-                    }
-                    d = sd[gi];
-                    chunk = d.chunk;
-                    if (chunk) break;  // all-empty group: rows give +0.0 in phase 2
-                }
-                wv = d.stride() / V;
-                gq0 = uint32_t((d.offset() - h.slot_begin) / V);
-                ub = uint32_t(sub[gi] - h.ub0);
-                ul = 0;
-            };
-            if (more && ul >= wv) next_group();
-            if (more && gq0 + ul * chunk >= qe) more = false;
-            double acc[V];
-            while (more) {
-                uint32_t mq[kB], uid[kB], flags = 0;  // bit 2b: first step, bit 2b+1: last step
-                uint32_t cnt = 0;
-#pragma unroll
-                for (uint32_t b = 0; b < kB; ++b) {
-                    if (!more) break;
-                    mq[b] = gq0 + j * wv + ul;
-                    uid[b] = ub + ul;
-                    if (j == 0) flags |= 1u << (2 * b);
-                    if (j + 1 == chunk) flags |= 2u << (2 * b);
-                    ++cnt;
-                    if (++j == chunk) {
-                        j = 0;
-                        if (++ul >= wv) next_group();
-                        if (more && gq0 + ul * chunk >= qe) more = false;
-                    }
-                }
-                int c[kB][V];
-                T v[kB][V];
-#pragma unroll
-                for (uint32_t b = 0; b < kB; ++b) {
-                    if (b < cnt) {
-                        if constexpr (V == 4) {
-                            const int4 cc = reinterpret_cast<const int4*>(scol)[mq[b]];
-                            c[b][0] = cc.x, c[b][1] = cc.y, c[b][2] = cc.z, c[b][3] = cc.w;
-                            SmemVec<T, 4>::load(sval + 4 * mq[b], v[b]);
-                        } else {
-#pragma unroll
-                            for (int l = 0; l < V; ++l) c[b][l] = scol[V * mq[b] + l], v[b][l] = sval[V * mq[b] + l];
-                        }
-                    } else {
-#pragma unroll
-                        for (int l = 0; l < V; ++l) c[b][l] = -1, v[b][l] = T(0);
-                    }
-                }
-                double xv[kB][V];
-#pragma unroll
-                for (uint32_t b = 0; b < kB; ++b)
-#pragma unroll
-                    for (int l = 0; l < V; ++l) xv[b][l] = c[b][l] != -1 ? ld_x(a.x + c[b][l], pol_x) : 0.0;
-                if (a.x_scale) {
-#pragma unroll
-                    for (uint32_t b = 0; b < kB; ++b)
-#pragma unroll
-                        for (int l = 0; l < V; ++l) xv[b][l] = __dmul_rn(xv[b][l], xs);
-                }
-#pragma unroll
-                for (uint32_t b = 0; b < kB; ++b) {
-                    if (b < cnt) {
-                        if (flags & (1u << (2 * b))) {
-#pragma unroll
-                            for (int l = 0; l < V; ++l) acc[l] = 0.0;
-                        }
-#pragma unroll
-                        for (int l = 0; l < V; ++l)
-                            if (c[b][l] != -1) acc[l] = __dadd_rn(acc[l], __dmul_rn(double(v[b][l]), xv[b][l]));
-                        if (flags & (2u << (2 * b))) {
-#pragma unroll
-                            for (int l = 0; l < V; ++l) spart[size_t(uid[b]) * V + l] = acc[l];
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();
-
-        // Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending,
-        // one row per thread.
-        for (uint32_t r = tid; r < h.nrows; r += NT) {
-            const uint32_t row = h.row0 + r;
-            const uint32_t gi = find_row(sd, h.ng, row);
-            const GroupDesc d = sd[gi];
-            const uint32_t g = h.gs + gi;
-            if (d.heavy() || g < a.g_begin || g >= a.g_end) continue;
-            double sum = 0.0;
-            if (d.chunk) {
-                const uint32_t b = row == d.first_row ? 0u : uint32_t(stm[r - 1]);
-                sum = row_sum(spart + size_t(sub[gi] - h.ub0) * V, b, uint32_t(stm[r]));
-            }
-            a.y[row] = to_out<T>(sum);
-        }
-        __syncthreads();  // stage st fully consumed
-        if (refill) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tma_issue<T, V>(a, nxt, stage, &hdrs[st], &bars[st], pol_meta, pol_stream);
-        }
-    }
-}
-
 size_t light_smem_bytes(const argcsr_dev* m, int V) {
     const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
     return size_t(m->max_tile_units) * V * sizeof(double) + cap * sizeof(uint64_t) + (cap + 1) * 4 * 2 + cap * 4;
@@ -784,8 +511,8 @@ int variant_id() {
         const char* e = std::getenv("ARGCSR_SPMV_VARIANT");
         if (!e) return -1;
         const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
-                               "-", "-", "LP4P0B4", "LP2P1B6", "LPD4P1B4"};
-        for (int i = 0; i < 13; ++i)
+                               "-", "-", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "LPD4P0B4", "LPD2P0B6"};
+        for (int i = 0; i < 15; ++i)
             if (!std::strcmp(e, names[i])) return i;
         return -1;
     }();
@@ -864,99 +591,21 @@ void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles, m->sched));
 }
 
-int tma_threads() {
-    static const int nt = [] {
-        const char* e = std::getenv("ARGCSR_TMA_THREADS");
-        const int v = e ? std::atoi(e) : 256;
-        return (v == 512 || v == 1024) ? v : 256;
-    }();
-    return nt;
-}
-int tma_ctas_per_sm() {  // resident CTAs per SM the stages are sized for
-    static const int c = [] {
-        const char* e = std::getenv("ARGCSR_TMA_CTAS");
-        const int v = e ? std::atoi(e) : 2;
-        return std::min(std::max(v, 1), 8);
-    }();
-    return c;
-}
-
-// Returns false when the handle has no TMA schedule or two stages do not fit.
-template <typename T, int V, int NT>
-bool launch_tma_nt(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    int dev = 0, sms = 0, optin = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    auto kern = spmv_tma_kernel<T, V, NT>;
-    int per_sm_smem = 0;
-    CUDA_OK(cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    const uint32_t SB = m->stage_bytes;
-    if (SB == 0) return false;
-    // stages per CTA: as many as fit (<= 4) with tma_ctas_per_sm() CTAs per SM,
-    // at least 2 (fewer CTAs per SM if needed)
-    uint32_t nst = 0;
-    for (int ctas = tma_ctas_per_sm(); ctas >= 1 && nst < 2; --ctas) {
-        const size_t budget = std::min<size_t>(size_t(optin), size_t(per_sm_smem) / ctas) - 1024;
-        nst = uint32_t(std::min<size_t>(4, budget / SB));
-    }
-    if (nst < 2) return false;
-    const size_t smem = size_t(nst) * SB;
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    const unsigned grid = unsigned(std::min<uint64_t>(m->num_ttiles, uint64_t(std::max(per_sm, 1)) * sms));
-    if (grid == 0) return true;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    cfg.numAttrs = 0;
-    const size_t xbytes = m->num_cols * sizeof(T);
-    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
-        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
-        attr[0].val.accessPolicyWindow.num_bytes = win;
-        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
-    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, nst));
-    return true;
-}
-
-template <typename T, int V>
-bool launch_tma(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    if (m->layout != kLayoutCompact || m->num_ttiles == 0) return false;
-    switch (tma_threads()) {
-        case 256: return launch_tma_nt<T, V, 256>(m, a, s);
-        case 1024: return launch_tma_nt<T, V, 1024>(m, a, s);
-        default: return launch_tma_nt<T, V, 512>(m, a, s);
-    }
-}
-
 template <typename T, int V>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     int vid = variant_id();
-    // Opt-in experiment (measured slower): the TMA-staged kernel.
-    const char* ev = std::getenv("ARGCSR_SPMV_VARIANT");
-    if (ev && !std::strcmp(ev, "TMA") && launch_tma<T, V>(m, a, s)) return;
     if (vid < 0) {
-        // Default: persistent CTAs with prefetched metadata and dynamic tile
-        // order when there are no heavy groups (e.g. stencils); otherwise
-        // hardware dispatch of independent tiles (measured best for R-MAT).
-        vid = m->num_heavy == 0 ? 12 : 6;
+        // Default: hardware-dispatched tiles, unpredicated value loads
+        // (measured best on C1-C4 with the lane-compact layout, scripts/sweep.sh).
+        vid = 2;
     }
     switch (vid) {
         case 0: launch_lightp<T, V, 4, true, 4, false>(m, a, s); return;
         case 10: launch_lightp<T, V, 4, false, 4, false>(m, a, s); return;
         case 11: launch_lightp<T, V, 2, true, 6, false>(m, a, s); return;
         case 12: launch_lightp<T, V, 4, true, 4, true>(m, a, s); return;
+        case 13: launch_lightp<T, V, 4, false, 4, true>(m, a, s); return;
+        case 14: launch_lightp<T, V, 2, false, 6, true>(m, a, s); return;
         default: break;
     }
     switch (vid) {
@@ -985,9 +634,6 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.tiles = m->tiles;
     a.heavy = m->heavy;
     a.heavy_ptr = m->heavy_ptr;
-    a.ttiles = m->ttiles;
-    a.num_ttiles = m->num_ttiles;
-    a.stage_bytes = m->stage_bytes;
     a.x = static_cast<const T*>(x);
     a.y = static_cast<T*>(y);
     a.heavy_ctas = m->heavy_ctas;

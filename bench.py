@@ -379,7 +379,8 @@ def run_b200(args):
 
     peak, peak_src = measured_peak()
     info = {"layout": m.layout, "groups": m.num_groups, "total_slots": m.total_slots,
-            "stored_slots": m.stored_slots, "heavy_groups": m.heavy_groups,
+            "stored_slots": m.stored_slots, "x_remap": m.x_remap, "x_used_columns": m.x_used_columns,
+            "heavy_groups": m.heavy_groups,
             "light_tiles": m.light_tiles, "max_chunk": m.max_chunk_size, "device_bytes": m.device_bytes,
             "heavy_ctas": m.heavy_ctas, "l2_persist_bytes": m.l2_persist_bytes}
     key = f"{args.config}_tpg{args.tpg}_dcs{args.dcs}_{args.layout}"
@@ -428,7 +429,7 @@ def run_b200(args):
         out["gpu_launches"] = launches
 
         if not args.no_variants:
-            out["variants"] = variants(args, A, x, tdtype, sv, stream, spmv_fn)
+            out["variants"] = variants(args, A, x, tdtype, sv, stream, spmv_fn, m.x_remap)
 
         if not args.no_cpu_baseline and cfg["dtype"] == "float64":
             out["cpu_baseline"] = cpu_baseline(args, m, A, x, y, stream)
@@ -438,7 +439,7 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
-def variants(args, A, x, tdtype, sv, stream, spmv_fn):
+def variants(args, A, x, tdtype, sv, stream, spmv_fn, x_remap=False):
     """Side runs on the same matrix: the tuned chunk budget and the cuSPARSE
     CSR yardstick (torch.sparse CSR matvec -> cusparseSpMV)."""
     import torch
@@ -449,14 +450,16 @@ def variants(args, A, x, tdtype, sv, stream, spmv_fn):
     ab = alg_bytes(A.nnz, A.num_rows, A.num_cols, sv)
     y = torch.empty(A.num_rows, dtype=tdtype, device=x.device)
     other = "reference" if args.layout == "compact" else "compact"
-    runs = [(args.dcs, other)] + [(d, args.layout) for d in sorted({32, 4} - {args.dcs})]
-    for dcs, layout in runs:
+    runs = [(args.dcs, other, "auto")] + [(d, args.layout, "auto") for d in sorted({32, 4} - {args.dcs})]
+    if x_remap:
+        runs.append((args.dcs, args.layout, "off"))
+    for dcs, layout, xr in runs:
         m2 = argcsr.argcsr_from_torch(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.to(tdtype),
-                                      args.tpg, dcs, stream=stream, layout=layout)
+                                      args.tpg, dcs, stream=stream, layout=layout, x_remap=xr)
         ts = time_spmv(m2, x, y, min(args.steps, 100), args.warmup, stream, spmv_fn)
         ms = statistics.median(ts)
         res.append({"impl": "argcsr_b200", "threads_per_group": args.tpg, "desired_chunk_size": dcs,
-                    "layout": layout, "ms": ms, "gflops": 2 * A.nnz / ms / 1e6, "eff_GBps": ab / ms / 1e6,
+                    "layout": layout, "x_remap": m2.x_remap, "ms": ms, "gflops": 2 * A.nnz / ms / 1e6, "eff_GBps": ab / ms / 1e6,
                     "total_slots": m2.total_slots, "stored_slots": m2.stored_slots, "groups": m2.num_groups})
         m2.free()
         del m2

@@ -98,6 +98,8 @@ typedef struct {
     int32_t device;
     argcsr_dtype dtype;
     uint32_t layout;           /* 0 = lane-compact (default), ARGCSR_LAYOUT_REFERENCE */
+    uint32_t x_remap;          /* 1: stored columns index x' = x[perm] (see ARGCSR_XREMAP_ON) */
+    uint64_t x_used_columns;   /* columns with an entry (x_remap) or num_cols */
 } argcsr_dev_info_t;
 
 /* Device layout of the value/column blocks (argcsr_dev_convert_ex flags).
@@ -110,6 +112,16 @@ typedef struct {
  * ARGCSR_LAYOUT_REFERENCE: keep the reference arrays verbatim on the device
  * (stride threads_per_group, argcsr.cpp:99-104). */
 #define ARGCSR_LAYOUT_REFERENCE 1u
+
+/* x remap (lane-compact layout only).  The device stores column indices in
+ * an internal order -- used columns first, most-used first by octave, index
+ * order within an octave -- and every SpMV gathers x' = x[perm] (one small
+ * kernel) so that x's hot head fits the persisting-L2 window.  Products and
+ * sums are unchanged (bit-identical results); every exported array maps back
+ * to reference column indices.  Default: automatic (on when x exceeds the
+ * window and the remap raises the window's nnz coverage by >= 5 points). */
+#define ARGCSR_XREMAP_ON 2u
+#define ARGCSR_XREMAP_OFF 4u
 
 /* ---------------------------------------------------------------- conversion */
 

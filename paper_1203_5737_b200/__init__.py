@@ -62,19 +62,22 @@ partition_rows = _ext.partition_rows
 abi_version = _ext.abi_version
 
 
-LAYOUTS = {"compact": 0, "reference": 1}  # argcsr_dev_convert_ex flags (include/argcsr_gpu.h)
+# argcsr_dev_convert_ex flags (include/argcsr_gpu.h)
+LAYOUTS = {"compact": 0, "reference": 1}
+X_REMAP = {"auto": 0, "on": 2, "off": 4}
 
 
-def _layout_flags(layout: str) -> int:
-    try:
-        return LAYOUTS[layout]
-    except KeyError:
-        raise ParameterError(f"argcsr_from_csr: layout must be one of {sorted(LAYOUTS)}") from None
+def _layout_flags(layout: str, x_remap: str = "auto") -> int:
+    if layout not in LAYOUTS:
+        raise ParameterError(f"argcsr_from_csr: layout must be one of {sorted(LAYOUTS)}")
+    if x_remap not in X_REMAP:
+        raise ParameterError(f"argcsr_from_csr: x_remap must be one of {sorted(X_REMAP)}")
+    return LAYOUTS[layout] | X_REMAP[x_remap]
 
 
 def argcsr_from_csr(matrix, threads_per_group: int = kDefaultThreadsPerGroup,
                     desired_chunk_size: int = kDefaultDesiredChunkSize, device: int = 0,
-                    layout: str = "compact") -> ArgCsrMatrix:
+                    layout: str = "compact", x_remap: str = "auto") -> ArgCsrMatrix:
     """argcsr_from_csr (argcsr.hpp:101-104) on the GPU.
 
     `matrix` is a CsrMatrix, or a tuple (num_rows, num_cols, row_pointers,
@@ -83,8 +86,10 @@ def argcsr_from_csr(matrix, threads_per_group: int = kDefaultThreadsPerGroup,
     device storage of the value/column blocks: "compact" (free lanes not
     stored, the default) or "reference" (the reference arrays verbatim); the
     exported arrays and every SpMV result are identical either way.
+    `x_remap` ("auto" | "on" | "off") controls the device-internal column
+    order that keeps x's working set L2-resident (compact layout only).
     """
-    flags = _layout_flags(layout)
+    flags = _layout_flags(layout, x_remap)
     if isinstance(matrix, CsrMatrix):
         return _ext.argcsr_from_csr(matrix, threads_per_group, desired_chunk_size, device, flags)
     if isinstance(matrix, tuple) and len(matrix) == 5:
@@ -97,12 +102,12 @@ def argcsr_from_csr(matrix, threads_per_group: int = kDefaultThreadsPerGroup,
 def argcsr_from_torch(num_rows: int, num_cols: int, row_pointers, columns, values,
                       threads_per_group: int = kDefaultThreadsPerGroup,
                       desired_chunk_size: int = kDefaultDesiredChunkSize, stream=None,
-                      layout: str = "compact") -> ArgCsrMatrix:
+                      layout: str = "compact", x_remap: str = "auto") -> ArgCsrMatrix:
     """Convert a device-resident CSR given as torch CUDA tensors (int64 row
     pointers, int32 columns, float64/float32 values) on the current stream."""
     import torch
 
-    flags = _layout_flags(layout)
+    flags = _layout_flags(layout, x_remap)
     if not (row_pointers.is_cuda and columns.is_cuda and values.is_cuda):
         raise ParameterError("argcsr_from_torch: tensors must be CUDA tensors")
     if row_pointers.dtype != torch.int64 or columns.dtype != torch.int32:

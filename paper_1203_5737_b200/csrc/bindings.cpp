@@ -229,6 +229,8 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         .def_property_readonly("desired_chunk_size", [](const PyArgCsr& p) { return p.info().desired_chunk_size; })
         .def_property_readonly("total_slots", [](const PyArgCsr& p) { return p.info().total_slots; })
         .def_property_readonly("stored_slots", [](const PyArgCsr& p) { return p.info().stored_slots; })
+        .def_property_readonly("x_remap", [](const PyArgCsr& p) { return p.info().x_remap != 0; })
+        .def_property_readonly("x_used_columns", [](const PyArgCsr& p) { return p.info().x_used_columns; })
         .def_property_readonly("layout", [](const PyArgCsr& p) {
             return p.info().layout == ARGCSR_LAYOUT_REFERENCE ? "reference" : "compact";
         })

@@ -74,6 +74,8 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->heavy);
     cudaFree(m->heavy_ptr);
     cudaFree(m->sched);
+    cudaFree(m->perm);
+    cudaFree(m->xbuf);
     if (m->aux) cudaStreamDestroy(m->aux);
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
@@ -154,8 +156,10 @@ argcsr_status argcsr_dev_convert_ex(const argcsr_csr_view* csr, uint64_t tpg, ui
                                            std::to_string(argcsr_gpu::kMaxThreadsPerGroup));
         if (csr->num_rows >= 0xFFFFFFFFull)
             fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: num_rows exceeds the device limit 2^32-2");
-        if (flags & ~uint32_t(ARGCSR_LAYOUT_REFERENCE))
+        if (flags & ~uint32_t(ARGCSR_LAYOUT_REFERENCE | ARGCSR_XREMAP_ON | ARGCSR_XREMAP_OFF))
             fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert_ex: unknown flags");
+        if ((flags & ARGCSR_XREMAP_ON) && (flags & ARGCSR_XREMAP_OFF))
+            fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert_ex: ARGCSR_XREMAP_ON and ARGCSR_XREMAP_OFF both set");
         if (csr->dtype != ARGCSR_F64 && csr->dtype != ARGCSR_F32)
             fail(ARGCSR_E_PARAMETER, "argcsr_from_csr: unknown dtype");
         if (!csr->row_pointers || (csr->nnz && (!csr->columns || !csr->values)))
@@ -172,14 +176,17 @@ argcsr_status argcsr_dev_convert_ex(const argcsr_csr_view* csr, uint64_t tpg, ui
         m->dcs = dcs;
         m->tm16 = true;
         m->layout = (flags & ARGCSR_LAYOUT_REFERENCE) ? argcsr_gpu::kLayoutReference : argcsr_gpu::kLayoutCompact;
+        m->xremap_mode = (flags & ARGCSR_XREMAP_ON)    ? argcsr_gpu::kXRemapOn
+                         : (flags & ARGCSR_XREMAP_OFF) ? argcsr_gpu::kXRemapOff
+                                                       : argcsr_gpu::kXRemapAuto;
         try {
             m->l2_persist_max = ensure_l2_persist(device);
             CUDA_OK(cudaDeviceGetAttribute(&m->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize, device));
             CUDA_OK(cudaStreamCreateWithFlags(&m->aux, cudaStreamNonBlocking));
-            CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
-            CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
             CUDA_OK(cudaMalloc(&m->sched, 2 * sizeof(uint32_t)));
             CUDA_OK(cudaMemset(m->sched, 0, 2 * sizeof(uint32_t)));
+            CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
             const uint64_t N = csr->num_rows, nnz = csr->nnz;
             const size_t es = elem_size(csr->dtype);
             const uint64_t* rp = csr->row_pointers;
@@ -233,6 +240,8 @@ argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info) {
         info->total_slots = m->total_slots;
         info->stored_slots = m->stored_slots;
         info->layout = m->layout == argcsr_gpu::kLayoutReference ? ARGCSR_LAYOUT_REFERENCE : 0u;
+        info->x_remap = m->x_remap ? 1u : 0u;
+        info->x_used_columns = m->n_used;
         info->nnz = m->nnz;
         info->heavy_groups = m->num_heavy;
         info->heavy_ctas = m->heavy_ctas;
@@ -370,6 +379,13 @@ argcsr_status argcsr_dev_chunk_entries(const argcsr_dev* m, uint64_t group_index
         }
         uint64_t k = 0;
         while (k < d.chunk && c[k] != -1) ++k;
+        if (m->x_remap && k) {  // stored column -> reference column (xremap.cu)
+            std::vector<uint32_t> pc(k);
+            for (uint64_t i = 0; i < k; ++i)
+                CUDA_OK(cudaMemcpyAsync(&pc[i], m->perm + c[i], sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaStreamSynchronize(s));
+            for (uint64_t i = 0; i < k; ++i) c[i] = int32_t(pc[i]);
+        }
         *n = k;
         if (k > cap) fail(ARGCSR_E_BOUNDS, "chunk_entries: output capacity too small");
         if (k) {

@@ -60,6 +60,7 @@ struct alignas(16) GroupDesc {
 static_assert(sizeof(GroupDesc) == 16, "GroupDesc must be 16 bytes");
 
 enum Layout : int { kLayoutCompact = 0, kLayoutReference = 1 };
+enum XRemapMode : int { kXRemapAuto = 0, kXRemapOn = 1, kXRemapOff = 2 };
 
 // Device limits (documented in DESIGN.md).  threads_per_group bounds the
 // shared-memory partial-sum staging of the SpMV; rows are u32 on the device.
@@ -109,6 +110,14 @@ struct argcsr_dev {
     uint32_t* sched = nullptr;            // [2] dynamic tile counter + done counter (self-resetting)
 
     uint64_t light_slots = 0;             // stored slots of light groups (stored first)
+
+    // x remap (xremap.cu): stored columns index x' = x[perm[0 .. n_used)].
+    int xremap_mode = argcsr_gpu::kXRemapAuto;
+    bool x_remap = false;
+    uint32_t* perm = nullptr;             // [num_cols] stored column -> reference column
+    void* xbuf = nullptr;                 // [n_used] x' (one SpMV in flight per handle)
+    uint64_t n_used = 0;                  // columns with at least one entry (remap on) or num_cols
+    double x_cover_lead = 0, x_cover_top = 0;  // nnz share of the window: leading columns / remapped
 
     // x residency (L2 persisting window) — queried, not hard-coded.
     size_t l2_persist_max = 0;

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "convert.cuh"
 #include "scan.cuh"
+#include "xremap.cuh"
 
 namespace argcsr_gpu {
 
@@ -395,8 +396,8 @@ template <typename T, typename TM>
 __global__ void __launch_bounds__(256) k5_layout(const uint64_t* __restrict__ rp, const int32_t* __restrict__ cols_in,
                                                  const T* __restrict__ vals_in, const GroupDesc* __restrict__ desc,
                                                  const TM* __restrict__ tm, const TM* __restrict__ assigned,
-                                                 uint32_t G, T* __restrict__ vals_out,
-                                                 int32_t* __restrict__ cols_out) {
+                                                 const int32_t* __restrict__ col_map, uint32_t G,
+                                                 T* __restrict__ vals_out, int32_t* __restrict__ cols_out) {
     constexpr uint32_t WL = 1024;
     __shared__ uint64_t s_src[WL];
     __shared__ uint32_t s_len[WL];
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(256) k5_layout(const uint64_t* __restrict__ rp
                 if (j < s_len[l]) {
                     const uint64_t src = s_src[l] + j;
                     vals_out[slot] = vals_in[src];
-                    cols_out[slot] = cols_in[src];
+                    cols_out[slot] = col_map ? col_map[cols_in[src]] : cols_in[src];
                 } else {
                     vals_out[slot] = T(0);
                     cols_out[slot] = -1;
@@ -672,12 +673,19 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     // K5
     m->values = dev_alloc<T>(m, stored_slots);
     m->columns = dev_alloc<int32_t>(m, stored_slots);
+    // x remap (lane-compact only): stored columns index x' = x[perm]
+    uint64_t rp_ends[2] = {0, 0};
+    CUDA_OK(cudaMemcpyAsync(&rp_ends[0], rp, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(&rp_ends[1], rp + N, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+    int32_t* col_map = build_xremap(m, cols + rp_ends[0], rp_ends[1] - rp_ends[0], m->xremap_mode, s);
     if (G > 0 && stored_slots > 0) {
         const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
-        k5_layout<T, TM><<<grid, 256, 0, s>>>(rp, cols, vals, m->groups, tm, assigned, G,
+        k5_layout<T, TM><<<grid, 256, 0, s>>>(rp, cols, vals, m->groups, tm, assigned, col_map, G,
                                              static_cast<T*>(m->values), m->columns);
         LAUNCH_OK("k5_layout");
     }
+    if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
     CUDA_OK(cudaStreamSynchronize(s));
 }
 

@@ -36,7 +36,7 @@ __global__ void k_export_groups(const GroupDesc* __restrict__ desc, const uint64
 template <typename T>
 __global__ void k_expand(const GroupDesc* __restrict__ desc, const uint64_t* __restrict__ ref_off, uint64_t g0,
                          uint64_t g1, uint64_t tpg, const T* __restrict__ vin, const int32_t* __restrict__ cin,
-                         T* __restrict__ vout, int32_t* __restrict__ cout) {
+                         const uint32_t* __restrict__ perm, T* __restrict__ vout, int32_t* __restrict__ cout) {
     const uint64_t base = ref_off[g0];
     for (uint64_t g = g0 + blockIdx.x; g < g1; g += gridDim.x) {
         const GroupDesc d = desc[g];
@@ -46,7 +46,8 @@ __global__ void k_expand(const GroupDesc* __restrict__ desc, const uint64_t* __r
             const uint64_t j = i / tpg, lane = i - j * tpg;
             if (lane < w) {
                 vout[dst + i] = vin[src + j * w + lane];
-                cout[dst + i] = cin[src + j * w + lane];
+                const int32_t c = cin[src + j * w + lane];
+                cout[dst + i] = (perm && c != -1) ? int32_t(perm[c]) : c;
             } else {
                 vout[dst + i] = T(0);
                 cout[dst + i] = -1;
@@ -94,7 +95,8 @@ __global__ void k_row_counts(const GroupDesc* __restrict__ desc, const TM* __res
 template <typename T, typename TM>
 __global__ void k_fill_csr(const GroupDesc* __restrict__ desc, const TM* __restrict__ tm,
                            const int32_t* __restrict__ cols, const T* __restrict__ vals, uint64_t G,
-                           const uint64_t* __restrict__ rp, int32_t* __restrict__ out_cols, T* __restrict__ out_vals) {
+                           const uint64_t* __restrict__ rp, const uint32_t* __restrict__ perm,
+                           int32_t* __restrict__ out_cols, T* __restrict__ out_vals) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < G; g += nw) {
@@ -108,7 +110,7 @@ __global__ void k_fill_csr(const GroupDesc* __restrict__ desc, const TM* __restr
                     const uint64_t slot = d.offset() + uint64_t(j) * d.stride() + c;
                     const int32_t col = cols[slot];
                     if (col == -1) break;
-                    out_cols[o] = col;
+                    out_cols[o] = perm ? int32_t(perm[col]) : col;
                     out_vals[o] = vals[slot];
                     ++o;
                 }
@@ -175,7 +177,7 @@ void expand_to_host(const argcsr_dev* m, const uint64_t* ref_off_dev, T* values,
             Scratch<int32_t> c(n, s);
             k_expand<T><<<grid_for((g1 - g0) * 256, 256), 256, 0, s>>>(m->groups, ref_off_dev, g0, g1, m->tpg,
                                                                         static_cast<const T*>(m->values), m->columns,
-                                                                        v.p, c.p);
+                                                                        m->x_remap ? m->perm : nullptr, v.p, c.p);
             LAUNCH_OK("k_expand");
             if (values) CUDA_OK(cudaMemcpyAsync(values + off[g0], v.p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
             if (columns)
@@ -231,11 +233,13 @@ void to_csr(const argcsr_dev* m, uint64_t* row_pointers, int32_t* columns, void*
     Scratch<unsigned char> ov(nnz * elem_size(m), s);
     if (m->dtype == ARGCSR_F64)
         k_fill_csr<double, uint16_t><<<grid_for(G * 32, 256), 256, 0, s>>>(
-            m->groups, tm, m->columns, static_cast<const double*>(m->values), G, rp.p, oc.p,
+            m->groups, tm, m->columns, static_cast<const double*>(m->values), G, rp.p,
+            m->x_remap ? m->perm : nullptr, oc.p,
             reinterpret_cast<double*>(ov.p));
     else
         k_fill_csr<float, uint16_t><<<grid_for(G * 32, 256), 256, 0, s>>>(
-            m->groups, tm, m->columns, static_cast<const float*>(m->values), G, rp.p, oc.p,
+            m->groups, tm, m->columns, static_cast<const float*>(m->values), G, rp.p,
+            m->x_remap ? m->perm : nullptr, oc.p,
             reinterpret_cast<float*>(ov.p));
     LAUNCH_OK("k_fill_csr");
     CUDA_OK(cudaMemcpyAsync(row_pointers, rp.p, (N + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));

@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "spmv.cuh"
+#include "xremap.cuh"
 
 namespace argcsr_gpu {
 
@@ -535,7 +536,7 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     cfg.numAttrs = 0;
-    const size_t xbytes = m->num_cols * sizeof(T);
+    const size_t xbytes = m->n_used * sizeof(T);  // x, or x' = x[perm] (xremap.cu)
     if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
         // Persist the leading part of x that fits the carve-out (hit ratio 1):
         // all of x for the stencils; the hot low-index columns of R-MAT.
@@ -576,7 +577,7 @@ void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     cfg.numAttrs = 0;
-    const size_t xbytes = m->num_cols * sizeof(T);
+    const size_t xbytes = m->n_used * sizeof(T);  // x, or x' = x[perm] (xremap.cu)
     if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
         const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -673,6 +674,7 @@ void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_beg
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
+    x = xremap_apply(m, x, s);
     if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s);
     else launch_dtype<float>(m, x, x_scale, y, gb, ge, s);
 }

@@ -1,0 +1,19 @@
+// x remap (xremap.cu): device-internal column order that keeps x's working
+// set L2-resident.
+#pragma once
+
+#include "common.cuh"
+
+namespace argcsr_gpu {
+
+// Decides and builds the remap for handle m from the CSR columns (device,
+// nnz entries).  Returns the device array inv (old column -> stored column,
+// num_cols entries, cudaMallocAsync on s; the caller frees it) when the remap
+// is on, else nullptr.
+int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode, cudaStream_t s);
+
+// x as the SpMV kernels read it: x itself, or x' = x[perm] gathered on s into
+// the handle's buffer.
+const void* xremap_apply(const argcsr_dev* m, const void* x, cudaStream_t s);
+
+}  // namespace argcsr_gpu

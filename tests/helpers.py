@@ -70,12 +70,15 @@ def stencil27(n: int) -> Csr:
     return Csr(n**3, n**3, np.cumsum(rp).astype(np.uint64), c.astype(np.int32), v)
 
 
-LAYOUTS = ("compact", "reference")
+# device storage variants every parity case runs through: (layout, x_remap)
+LAYOUTS = (("compact", "auto"), ("reference", "auto"), ("compact", "on"))
 
 
-def to_dev(argcsr, A: Csr, tpg: int, dcs: int, dtype=np.float64, layout: str = "compact"):
+def to_dev(argcsr, A: Csr, tpg: int, dcs: int, dtype=np.float64, layout="compact"):
+    layout, x_remap = (layout, "auto") if isinstance(layout, str) else layout
     return argcsr.argcsr_from_csr(
-        (A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.astype(dtype)), tpg, dcs, layout=layout)
+        (A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.astype(dtype)), tpg, dcs, layout=layout,
+        x_remap=x_remap)
 
 
 def assert_same_layout(dev, ref_m: oracle.ArgCsr, where: str = "") -> None:

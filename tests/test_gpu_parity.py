@@ -131,10 +131,12 @@ def _check_case(argcsr, orc, A, tpg, dcs, where, layouts=LAYOUTS):
     for layout in layouts:
         dev = to_dev(argcsr, A, tpg, dcs, layout=layout)
         w = f"{where} [{layout}]"
-        assert dev.layout == layout
+        assert dev.layout == layout[0]
         assert_same_layout(dev, ref_m, w)
-        if layout == "reference":
-            assert dev.stored_slots == dev.total_slots
+        if layout[0] == "reference":
+            assert dev.stored_slots == dev.total_slots and not dev.x_remap
+        if layout == ("compact", "on") and A.columns.size:
+            assert dev.x_remap and dev.x_used_columns == np.unique(A.columns).size
         else:
             assert dev.stored_slots <= dev.total_slots
         y = argcsr.spmv(dev, x)
@@ -236,12 +238,13 @@ def test_unsorted_columns_copied_in_stored_order(argcsr, orc):
 
 
 # ---------------------------------------------------------------- other APIs
-def test_spmv_groups_writes_only_its_rows(argcsr, orc):
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout):
     import torch
 
     A = powerlaw_csr(20000, 20000, seed=11, heavy_rows=[(100, 8000)])
     ref_m = orc.argcsr_from_csr(A, 128, 1)
-    dev = to_dev(argcsr, A, 128, 1)
+    dev = to_dev(argcsr, A, 128, 1, layout=layout)
     x = np.cos(np.arange(A.num_cols, dtype=np.float64))
     G = dev.num_groups
     for gb, ge in ((0, G), (3, G // 2), (G // 3, G - 1), (5, 6)):

@@ -11,9 +11,12 @@ from test_multigpu_gloo import reference_power_iteration
 pytestmark = pytest.mark.gpu
 
 
-def test_fused_scale_is_bit_identical(argcsr, orc):
+@pytest.mark.parametrize("x_remap", ["auto", "on"])
+def test_fused_scale_is_bit_identical(argcsr, orc, x_remap):
     A = stencil27(16)
-    m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1)
+    m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1,
+                               x_remap=x_remap)
+    assert m.x_remap == (x_remap == "on")
     x = torch.linspace(-3, 3, A.num_cols, dtype=torch.float64, device="cuda")
     s = torch.tensor([1.0 / 7.3], dtype=torch.float64, device="cuda")
     y1 = torch.empty(A.num_rows, dtype=torch.float64, device="cuda")

@@ -209,6 +209,44 @@ ARGCSR_API argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_fo
 
 ARGCSR_API void argcsr_dev_free(argcsr_dev* m);
 
+/* ------------------------------------------------------- import / binary */
+
+/* The reference ArgCsrMatrix (argcsr.hpp:52-63) as host arrays. */
+typedef struct {
+    uint64_t num_rows;
+    uint64_t num_cols;
+    uint64_t threads_per_group;
+    uint64_t num_groups;
+    const uint64_t* groups4;         /* [num_groups * 4]: first_row, size, offset, chunk_size */
+    const uint64_t* threads_mapping; /* [num_rows] */
+    const void* values;              /* [total_slots] f64 (or f32) */
+    const int32_t* columns;          /* [total_slots] */
+    uint64_t total_slots;
+    argcsr_dtype dtype;
+} argcsr_argcsr_view;
+
+/* A device handle from the reference arrays (e.g. a cached conversion),
+ * without re-running the converter: the arrays are checked (groups tile the
+ * rows, reference offsets, threads_mapping increasing per group, free lanes
+ * all padding, padding trailing per lane; ARGCSR_E_FORMAT otherwise) and laid
+ * out as after argcsr_dev_convert_ex(flags).  desired_chunk_size reads 0. */
+ARGCSR_API argcsr_status argcsr_dev_import(const argcsr_argcsr_view* matrix, int device, void* stream,
+                                uint32_t flags, argcsr_dev** out);
+
+/* write_binary(ostream, const ArgCsrMatrix&) (io.cpp:282-298) to a file: the
+ * reference's SPFMTBIN container, byte-identical to the reference writing
+ * argcsr_from_csr of the same input.  fp64 handles only. */
+ARGCSR_API argcsr_status argcsr_dev_write_binary(const argcsr_dev* m, const char* path);
+
+/* read_binary_file (io.cpp:300-366) onto the device: an ARG-CSR container is
+ * imported (argcsr_dev_import); a CSR container is converted with
+ * threads_per_group / desired_chunk_size (argcsr_dev_convert_ex).  Bad magic,
+ * version or tag -> ARGCSR_E_FORMAT; truncation -> ARGCSR_E_PARSE; ELLPACK
+ * containers -> ARGCSR_E_UNSUPPORTED; unreadable file -> ARGCSR_E_IO. */
+ARGCSR_API argcsr_status argcsr_dev_read_binary(const char* path, uint64_t threads_per_group,
+                                     uint64_t desired_chunk_size, int device, void* stream,
+                                     uint32_t flags, argcsr_dev** out);
+
 /* ------------------------------------------------------ multi-GPU row slices */
 
 /* nnz-balanced contiguous row split: row_begin[p] =

@@ -231,6 +231,7 @@ class _Ref:
                                                     f64p]
         L.ref_time_spmv_csr_parallel.argtypes = [vp, f64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, f64p]
         L.ref_write_binary_argcsr.argtypes = [vp, C.c_char_p]
+        L.ref_write_binary_csr.argtypes = [vp, C.c_char_p]
         L.ref_hardware_threads.restype = C.c_uint64
 
     def _check(self, st: int):
@@ -410,6 +411,13 @@ class _Ref:
             self._check(self.lib.ref_write_binary_argcsr(h, path.encode()))
         finally:
             self.lib.ref_argcsr_free(h)
+
+    def write_binary_csr(self, A: Csr, path: str):
+        h = self.csr_handle(A)
+        try:
+            self._check(self.lib.ref_write_binary_csr(h, path.encode()))
+        finally:
+            self.lib.ref_csr_free(h)
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())

@@ -345,6 +345,11 @@ int ref_write_binary_argcsr(const void* h, const char* path) {
     return guarded([&] { write_binary_file(path, *static_cast<const ArgCsrMatrix*>(h)); });
 }
 
+// Binary container, CSR tag (io.cpp:250-257).
+int ref_write_binary_csr(const void* csr, const char* path) {
+    return guarded([&] { write_binary_file(path, *static_cast<const CsrMatrix*>(csr)); });
+}
+
 uint64_t ref_hardware_threads(void) { return std::thread::hardware_concurrency(); }
 
 }  // extern "C"

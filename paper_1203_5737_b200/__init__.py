@@ -124,6 +124,30 @@ def argcsr_from_torch(num_rows: int, num_cols: int, row_pointers, columns, value
         values.contiguous().data_ptr(), dtype, threads_per_group, desired_chunk_size, dev, s.cuda_stream, flags)
 
 
+def write_binary(path: str, matrix: ArgCsrMatrix) -> None:
+    """write_binary(path, matrix) (bindings.cpp:168-171 -> io.cpp:282-298):
+    the reference's SPFMTBIN container, byte-identical to the reference's."""
+    _ext.write_binary(str(path), matrix)
+
+
+def read_binary(path: str, threads_per_group: int = kDefaultThreadsPerGroup,
+                desired_chunk_size: int = kDefaultDesiredChunkSize, device: int = 0, layout: str = "compact",
+                x_remap: str = "auto") -> ArgCsrMatrix:
+    """read_binary(path) (bindings.cpp:172 -> io.cpp:300-366) onto the device:
+    an ARG-CSR container is imported as stored (a cached conversion); a CSR
+    container is converted with threads_per_group / desired_chunk_size."""
+    return _ext.read_binary(str(path), threads_per_group, desired_chunk_size, device, _layout_flags(layout, x_remap))
+
+
+def argcsr_from_reference(num_rows: int, num_cols: int, threads_per_group: int, groups, threads_mapping, values,
+                          columns, device: int = 0, layout: str = "compact", x_remap: str = "auto") -> ArgCsrMatrix:
+    """A device handle from the reference ArgCsrMatrix arrays (groups as a
+    G x 4 array of first_row, size, offset, chunk_size), checked, without
+    re-running the converter."""
+    return _ext.argcsr_from_reference_arrays(num_rows, num_cols, threads_per_group, groups, threads_mapping, values,
+                                             columns, device, _layout_flags(layout, x_remap))
+
+
 def spmv(matrix: ArgCsrMatrix, x):
     """spmv(matrix, x) (bindings.cpp:135 -> spmv_argcsr, argcsr.cpp:219-227).
 

@@ -362,6 +362,66 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         py::arg("matrix"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
         py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);
 
+    m.def(
+        "write_binary",
+        [](const std::string& path, const PyArgCsr& p) {
+            py::gil_scoped_release nogil;
+            check(argcsr_dev_write_binary(p.dev->handle(), path.c_str()));
+        },
+        py::arg("path"), py::arg("matrix"));
+
+    m.def(
+        "read_binary",
+        [](const std::string& path, std::size_t tpg, std::size_t dcs, int device, std::uint32_t flags) {
+            argcsr_dev* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_dev_read_binary(path.c_str(), tpg, dcs, device, nullptr, flags, &h));
+            }
+            return make_handle(h);
+        },
+        py::arg("path"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
+        py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);
+
+    m.def(
+        "argcsr_from_reference_arrays",
+        [](std::uint64_t num_rows, std::uint64_t num_cols, std::uint64_t tpg, py::array groups, py::array tm,
+           py::array values, py::array columns, int device, std::uint32_t flags) {
+            auto g = py::array_t<uint64_t, py::array::c_style | py::array::forcecast>(groups);
+            auto t = py::array_t<uint64_t, py::array::c_style | py::array::forcecast>(tm);
+            auto c = py::array_t<int32_t, py::array::c_style | py::array::forcecast>(columns);
+            py::array v;
+            argcsr_argcsr_view view{};
+            if (py::dtype(values.dtype()).is(py::dtype::of<float>())) {
+                v = py::array_t<float, py::array::c_style | py::array::forcecast>(values);
+                view.dtype = ARGCSR_F32;
+            } else {
+                v = py::array_t<double, py::array::c_style | py::array::forcecast>(values);
+                view.dtype = ARGCSR_F64;
+            }
+            if (g.size() % 4) throw DimensionError("argcsr_from_reference_arrays: groups must be G x 4");
+            if (t.size() != py::ssize_t(num_rows)) throw DimensionError("argcsr_from_reference_arrays: threads_mapping length");
+            if (v.size() != c.size()) throw DimensionError("argcsr_from_reference_arrays: values/columns lengths differ");
+            view.num_rows = num_rows;
+            view.num_cols = num_cols;
+            view.threads_per_group = tpg;
+            view.num_groups = uint64_t(g.size() / 4);
+            view.groups4 = g.data();
+            view.threads_mapping = t.data();
+            view.values = v.data();
+            view.columns = c.data();
+            view.total_slots = uint64_t(c.size());
+            argcsr_dev* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_dev_import(&view, device, nullptr, flags, &h));
+            }
+            return make_handle(h);
+        },
+        py::arg("num_rows"), py::arg("num_cols"), py::arg("threads_per_group"), py::arg("groups"),
+        py::arg("threads_mapping"), py::arg("values"), py::arg("columns"), py::arg("device") = 0,
+        py::arg("flags") = 0u);
+
     m.def("argcsr_from_csr_arrays", &convert_arrays, py::arg("num_rows"), py::arg("num_cols"), py::arg("row_pointers"),
           py::arg("columns"), py::arg("values"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
           py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);

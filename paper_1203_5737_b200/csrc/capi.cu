@@ -2,7 +2,9 @@
 // reference (proj/src/argcsr.cpp:20-26, 220-223, 235-242); every failure is a
 // status code plus a thread-local message, never an exception across the ABI.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -109,6 +111,111 @@ size_t ensure_l2_persist(int device) {
     return granted;
 }
 
+// A fresh handle with the per-handle resources (aux stream, events, L2 window
+// limits); freed by free_handle on any failure of the caller.
+argcsr_dev* new_handle(int device, argcsr_dtype dtype, uint64_t rows, uint64_t cols, uint64_t tpg, uint64_t dcs,
+                       uint32_t flags) {
+    auto* m = new argcsr_dev;
+    m->device = device;
+    m->dtype = dtype;
+    m->num_rows = rows;
+    m->num_cols = cols;
+    m->tpg = tpg;
+    m->dcs = dcs;
+    m->tm16 = true;
+    m->layout = (flags & ARGCSR_LAYOUT_REFERENCE) ? argcsr_gpu::kLayoutReference : argcsr_gpu::kLayoutCompact;
+    m->xremap_mode = (flags & ARGCSR_XREMAP_ON)    ? argcsr_gpu::kXRemapOn
+                     : (flags & ARGCSR_XREMAP_OFF) ? argcsr_gpu::kXRemapOff
+                                                   : argcsr_gpu::kXRemapAuto;
+    try {
+        m->l2_persist_max = ensure_l2_persist(device);
+        CUDA_OK(cudaDeviceGetAttribute(&m->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize, device));
+        CUDA_OK(cudaStreamCreateWithFlags(&m->aux, cudaStreamNonBlocking));
+        CUDA_OK(cudaMalloc(&m->sched, 2 * sizeof(uint32_t)));
+        CUDA_OK(cudaMemset(m->sched, 0, 2 * sizeof(uint32_t)));
+        CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+    } catch (...) {
+        free_handle(m);
+        throw;
+    }
+    return m;
+}
+
+void check_flags(uint32_t flags, const char* who) {
+    if (flags & ~uint32_t(ARGCSR_LAYOUT_REFERENCE | ARGCSR_XREMAP_ON | ARGCSR_XREMAP_OFF))
+        fail(ARGCSR_E_PARAMETER, std::string(who) + ": unknown flags");
+    if ((flags & ARGCSR_XREMAP_ON) && (flags & ARGCSR_XREMAP_OFF))
+        fail(ARGCSR_E_PARAMETER, std::string(who) + ": ARGCSR_XREMAP_ON and ARGCSR_XREMAP_OFF both set");
+}
+
+// ------------------------------------------------------- binary container
+// The reference's SPFMTBIN container (proj/src/io.cpp:17-22, 242-246,
+// 282-298, 300-366): 8-byte magic, u32 version 1, u8 format tag, then
+// little-endian u64 scalars and u64-length-prefixed arrays.
+constexpr char kMagic[8] = {'S', 'P', 'F', 'M', 'T', 'B', 'I', 'N'};
+constexpr uint32_t kVersion = 1;
+constexpr uint8_t kTagCsr = 0, kTagArgCsr = 3;
+
+struct File {
+    std::FILE* f = nullptr;
+    ~File() {
+        if (f) std::fclose(f);
+    }
+};
+
+struct Reader {
+    std::FILE* f;
+    uint64_t left;  // bytes not yet read
+    void bytes(void* p, uint64_t n) {
+        if (n > left || (n && std::fread(p, 1, n, f) != n)) fail(ARGCSR_E_PARSE, "binary stream truncated");
+        left -= n;
+    }
+    uint8_t u8() {
+        uint8_t v;
+        bytes(&v, 1);
+        return v;
+    }
+    uint32_t u32() {
+        unsigned char b[4];
+        bytes(b, 4);
+        return uint32_t(b[0]) | uint32_t(b[1]) << 8 | uint32_t(b[2]) << 16 | uint32_t(b[3]) << 24;
+    }
+    uint64_t u64() {
+        unsigned char b[8];
+        bytes(b, 8);
+        uint64_t v = 0;
+        for (int i = 0; i < 8; ++i) v |= uint64_t(b[i]) << (8 * i);
+        return v;
+    }
+    // u64 length + n elements of `size` bytes; a length beyond the stream is truncation
+    template <typename T>
+    std::vector<T> array() {
+        const uint64_t n = u64();
+        if (n > left / sizeof(T)) fail(ARGCSR_E_PARSE, "binary stream truncated");
+        std::vector<T> a(n);
+        bytes(a.data(), n * sizeof(T));  // little-endian host (x86-64 / aarch64)
+        return a;
+    }
+};
+
+struct Writer {
+    std::FILE* f;
+    void bytes(const void* p, uint64_t n) {
+        if (n && std::fwrite(p, 1, n, f) != n) fail(ARGCSR_E_IO, "binary write failure");
+    }
+    void u8(uint8_t v) { bytes(&v, 1); }
+    void u32(uint32_t v) {
+        const unsigned char b[4] = {uint8_t(v), uint8_t(v >> 8), uint8_t(v >> 16), uint8_t(v >> 24)};
+        bytes(b, 4);
+    }
+    void u64(uint64_t v) {
+        unsigned char b[8];
+        for (int i = 0; i < 8; ++i) b[i] = uint8_t(v >> (8 * i));
+        bytes(b, 8);
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -156,10 +263,7 @@ argcsr_status argcsr_dev_convert_ex(const argcsr_csr_view* csr, uint64_t tpg, ui
                                            std::to_string(argcsr_gpu::kMaxThreadsPerGroup));
         if (csr->num_rows >= 0xFFFFFFFFull)
             fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: num_rows exceeds the device limit 2^32-2");
-        if (flags & ~uint32_t(ARGCSR_LAYOUT_REFERENCE | ARGCSR_XREMAP_ON | ARGCSR_XREMAP_OFF))
-            fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert_ex: unknown flags");
-        if ((flags & ARGCSR_XREMAP_ON) && (flags & ARGCSR_XREMAP_OFF))
-            fail(ARGCSR_E_PARAMETER, "argcsr_dev_convert_ex: ARGCSR_XREMAP_ON and ARGCSR_XREMAP_OFF both set");
+        check_flags(flags, "argcsr_dev_convert_ex");
         if (csr->dtype != ARGCSR_F64 && csr->dtype != ARGCSR_F32)
             fail(ARGCSR_E_PARAMETER, "argcsr_from_csr: unknown dtype");
         if (!csr->row_pointers || (csr->nnz && (!csr->columns || !csr->values)))
@@ -167,26 +271,8 @@ argcsr_status argcsr_dev_convert_ex(const argcsr_csr_view* csr, uint64_t tpg, ui
 
         DeviceScope scope(device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        auto* m = new argcsr_dev;
-        m->device = device;
-        m->dtype = csr->dtype;
-        m->num_rows = csr->num_rows;
-        m->num_cols = csr->num_cols;
-        m->tpg = tpg;
-        m->dcs = dcs;
-        m->tm16 = true;
-        m->layout = (flags & ARGCSR_LAYOUT_REFERENCE) ? argcsr_gpu::kLayoutReference : argcsr_gpu::kLayoutCompact;
-        m->xremap_mode = (flags & ARGCSR_XREMAP_ON)    ? argcsr_gpu::kXRemapOn
-                         : (flags & ARGCSR_XREMAP_OFF) ? argcsr_gpu::kXRemapOff
-                                                       : argcsr_gpu::kXRemapAuto;
+        argcsr_dev* m = new_handle(device, csr->dtype, csr->num_rows, csr->num_cols, tpg, dcs, flags);
         try {
-            m->l2_persist_max = ensure_l2_persist(device);
-            CUDA_OK(cudaDeviceGetAttribute(&m->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize, device));
-            CUDA_OK(cudaStreamCreateWithFlags(&m->aux, cudaStreamNonBlocking));
-            CUDA_OK(cudaMalloc(&m->sched, 2 * sizeof(uint32_t)));
-            CUDA_OK(cudaMemset(m->sched, 0, 2 * sizeof(uint32_t)));
-            CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
-            CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
             const uint64_t N = csr->num_rows, nnz = csr->nnz;
             const size_t es = elem_size(csr->dtype);
             const uint64_t* rp = csr->row_pointers;
@@ -406,6 +492,140 @@ argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_format_stats*
 }
 
 void argcsr_dev_free(argcsr_dev* m) { free_handle(m); }
+
+argcsr_status argcsr_dev_import(const argcsr_argcsr_view* v, int device, void* stream, uint32_t flags,
+                                argcsr_dev** out) {
+    return guarded([&] {
+        if (!v || !out) fail(ARGCSR_E_PARAMETER, "argcsr_dev_import: null argument");
+        *out = nullptr;
+        check_flags(flags, "argcsr_dev_import");
+        if (v->threads_per_group == 0) fail(ARGCSR_E_FORMAT, "argcsr import: threads_per_group is 0");
+        if (v->num_rows == 0) fail(ARGCSR_E_FORMAT, "argcsr import: no rows");
+        if (v->threads_per_group > argcsr_gpu::kMaxThreadsPerGroup)
+            fail(ARGCSR_E_UNSUPPORTED, "argcsr import: threads_per_group " + std::to_string(v->threads_per_group) +
+                                           " exceeds the device limit " +
+                                           std::to_string(argcsr_gpu::kMaxThreadsPerGroup));
+        if (v->num_rows >= 0xFFFFFFFFull) fail(ARGCSR_E_UNSUPPORTED, "argcsr import: num_rows exceeds 2^32-2");
+        if (v->num_groups == 0 || v->num_groups > v->num_rows)
+            fail(ARGCSR_E_FORMAT, "argcsr import: group count out of range");
+        if (v->dtype != ARGCSR_F64 && v->dtype != ARGCSR_F32) fail(ARGCSR_E_PARAMETER, "argcsr import: unknown dtype");
+        if (!v->groups4 || !v->threads_mapping || (v->total_slots && (!v->values || !v->columns)))
+            fail(ARGCSR_E_PARAMETER, "argcsr_dev_import: null array");
+        DeviceScope scope(device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        argcsr_dev* m = new_handle(device, v->dtype, v->num_rows, v->num_cols, v->threads_per_group, 0, flags);
+        try {
+            argcsr_gpu::import_reference(m, v->num_groups, v->groups4, v->threads_mapping, v->values, v->columns,
+                                         v->total_slots, s);
+            CUDA_OK(cudaStreamSynchronize(s));
+        } catch (...) {
+            free_handle(m);
+            throw;
+        }
+        *out = m;
+    });
+}
+
+argcsr_status argcsr_dev_write_binary(const argcsr_dev* m, const char* path) {
+    return guarded([&] {
+        check_handle(m);
+        if (!path) fail(ARGCSR_E_PARAMETER, "argcsr_dev_write_binary: null path");
+        if (m->dtype != ARGCSR_F64)
+            fail(ARGCSR_E_UNSUPPORTED, "write_binary: the container stores fp64 values (io.cpp:282-298)");
+        DeviceScope scope(m->device);
+        const uint64_t G = m->num_groups, N = m->num_rows, S = m->total_slots;
+        std::vector<uint64_t> g4(4 * G), tm(N);
+        std::vector<double> vals(S);
+        std::vector<int32_t> cols(S);
+        argcsr_gpu::export_arrays(m, g4.data(), tm.data(), vals.data(), cols.data(), cudaStreamPerThread);
+        File file;
+        file.f = std::fopen(path, "wb");
+        if (!file.f) fail(ARGCSR_E_IO, std::string("cannot open '") + path + "' for writing");
+        Writer w{file.f};
+        w.bytes(kMagic, sizeof kMagic);  // put_header, io.cpp:242-246
+        w.u32(kVersion);
+        w.u8(kTagArgCsr);
+        w.u64(m->num_rows);  // write_binary(ArgCsrMatrix), io.cpp:282-298
+        w.u64(m->num_cols);
+        w.u64(m->tpg);
+        w.u64(G);
+        w.bytes(g4.data(), g4.size() * sizeof(uint64_t));  // {first_row, size, offset, chunk_size} per group
+        w.u64(N);
+        w.bytes(tm.data(), N * sizeof(uint64_t));
+        w.u64(S);
+        w.bytes(vals.data(), S * sizeof(double));
+        w.u64(S);
+        w.bytes(cols.data(), S * sizeof(int32_t));
+        if (std::fflush(file.f) != 0) fail(ARGCSR_E_IO, "binary write failure");
+    });
+}
+
+argcsr_status argcsr_dev_read_binary(const char* path, uint64_t tpg, uint64_t dcs, int device, void* stream,
+                                     uint32_t flags, argcsr_dev** out) {
+    return guarded([&] {
+        if (!path || !out) fail(ARGCSR_E_PARAMETER, "argcsr_dev_read_binary: null argument");
+        *out = nullptr;
+        check_flags(flags, "argcsr_dev_read_binary");
+        File file;
+        file.f = std::fopen(path, "rb");
+        if (!file.f) fail(ARGCSR_E_IO, std::string("cannot open '") + path + "' for reading");
+        std::fseek(file.f, 0, SEEK_END);
+        const long size = std::ftell(file.f);
+        std::fseek(file.f, 0, SEEK_SET);
+        Reader r{file.f, size < 0 ? 0 : uint64_t(size)};
+        char magic[8];
+        r.bytes(magic, sizeof magic);  // read_binary, io.cpp:300-312
+        if (std::memcmp(magic, kMagic, sizeof magic) != 0) fail(ARGCSR_E_FORMAT, "binary: bad magic");
+        const uint32_t version = r.u32();
+        if (version != kVersion) fail(ARGCSR_E_FORMAT, "binary: unsupported version " + std::to_string(version));
+        const uint8_t tag = r.u8();
+        if (tag == kTagArgCsr) {  // io.cpp:343-363
+            argcsr_argcsr_view v{};
+            v.num_rows = r.u64();
+            v.num_cols = r.u64();
+            v.threads_per_group = r.u64();
+            const uint64_t G = r.u64();
+            if (G > r.left / 32) fail(ARGCSR_E_PARSE, "binary stream truncated");
+            std::vector<uint64_t> g4(4 * G);
+            r.bytes(g4.data(), g4.size() * sizeof(uint64_t));
+            std::vector<uint64_t> tm = r.array<uint64_t>();
+            std::vector<double> vals = r.array<double>();
+            std::vector<int32_t> cols = r.array<int32_t>();
+            if (tm.size() != v.num_rows) fail(ARGCSR_E_FORMAT, "argcsr import: threads_mapping length != num_rows");
+            if (vals.size() != cols.size()) fail(ARGCSR_E_FORMAT, "argcsr import: values/columns lengths differ");
+            v.num_groups = G;
+            v.groups4 = g4.data();
+            v.threads_mapping = tm.data();
+            v.values = vals.data();
+            v.columns = cols.data();
+            v.total_slots = vals.size();
+            v.dtype = ARGCSR_F64;
+            const argcsr_status st = argcsr_dev_import(&v, device, stream, flags, out);
+            if (st != ARGCSR_OK) fail(st, g_last_error);
+        } else if (tag == kTagCsr) {  // io.cpp:313-320: converted on the device
+            argcsr_csr_view v{};
+            v.num_rows = r.u64();
+            v.num_cols = r.u64();
+            std::vector<double> vals = r.array<double>();
+            std::vector<int32_t> cols = r.array<int32_t>();
+            std::vector<uint64_t> rp = r.array<uint64_t>();
+            if (rp.size() != v.num_rows + 1 || vals.size() != cols.size() || rp.back() > vals.size())
+                fail(ARGCSR_E_FORMAT, "binary: inconsistent CSR arrays");
+            v.nnz = rp.back() - rp.front();
+            v.row_pointers = rp.data();
+            v.columns = cols.data();
+            v.values = vals.data();
+            v.dtype = ARGCSR_F64;
+            v.space = ARGCSR_HOST;
+            const argcsr_status st = argcsr_dev_convert_ex(&v, tpg, dcs, device, stream, flags, out);
+            if (st != ARGCSR_OK) fail(st, g_last_error);
+        } else if (tag == 1 || tag == 2) {
+            fail(ARGCSR_E_UNSUPPORTED, "binary: ELLPACK / sliced ELLPACK containers have no device path");
+        } else {
+            fail(ARGCSR_E_FORMAT, "binary: unknown format tag " + std::to_string(tag));
+        }
+    });
+}
 
 argcsr_status argcsr_partition_rows(const uint64_t* row_pointers, uint64_t num_rows, uint32_t parts,
                                     uint64_t* row_begin) {

@@ -459,6 +459,51 @@ __global__ void __launch_bounds__(256) k5_layout(const uint64_t* __restrict__ rp
     }
 }
 
+__device__ __forceinline__ bool is_pos_zero(double v) { return __double_as_longlong(v) == 0; }
+__device__ __forceinline__ bool is_pos_zero(float v) { return __float_as_int(v) == 0; }
+
+// Import (argcsr_dev_import_reference): per group, the reference block
+// (chunk x tpg, argcsr.cpp:99-104) -> the stored block (stride lanes), column
+// indices through the x remap.  Counts explicit entries (cnt[0]) and layout
+// violations (cnt[1]): a free lane (>= assigned) must hold (+0.0, -1) and a
+// lane's padding must trail its entries, as the reference converter writes.
+template <typename T, typename TM>
+__global__ void __launch_bounds__(256) k5_from_reference(const GroupDesc* __restrict__ desc,
+                                                         const uint64_t* __restrict__ ref_off, uint64_t tpg,
+                                                         const TM* __restrict__ assigned, const T* __restrict__ rv,
+                                                         const int32_t* __restrict__ rc,
+                                                         const int32_t* __restrict__ col_map, uint32_t G,
+                                                         T* __restrict__ vals_out, int32_t* __restrict__ cols_out,
+                                                         unsigned long long* __restrict__ cnt) {
+    uint64_t explicit_n = 0, bad = 0;
+    for (uint64_t g = blockIdx.x; g < G; g += gridDim.x) {
+        const GroupDesc d = desc[g];
+        const uint64_t w = d.stride(), off = d.offset(), asg = assigned[g], base = ref_off[g];
+        const uint64_t n = uint64_t(d.chunk) * tpg;
+        for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t j = i / tpg, lane = i - j * tpg;
+            const int32_t c = rc[base + i];
+            const T v = rv[base + i];
+            if (c != -1) {
+                ++explicit_n;
+                if (lane >= asg || (j > 0 && rc[base + i - tpg] == -1)) ++bad;
+            } else if (lane >= asg && !is_pos_zero(v)) {
+                ++bad;
+            }
+            if (lane < w) {
+                vals_out[off + j * w + lane] = v;
+                cols_out[off + j * w + lane] = (c != -1 && col_map) ? col_map[c] : c;
+            }
+        }
+    }
+    explicit_n = warp_sum_u64(explicit_n);
+    bad = warp_sum_u64(bad);
+    if ((threadIdx.x & 31) == 0) {
+        if (explicit_n) atomicAdd(cnt, (unsigned long long)explicit_n);
+        if (bad) atomicAdd(cnt + 1, (unsigned long long)bad);
+    }
+}
+
 // Units per light tile (default kDefaultTileUnits; a tile is one CTA of kTileThreads).
 // ARGCSR_TILE_THREADS (128 .. 2048) sets the units per tile (experiments).
 uint64_t tile_threads_setting() {
@@ -491,6 +536,20 @@ P* dev_alloc(argcsr_dev* m, size_t n) {
     m->device_bytes += std::max<size_t>(n, 1) * sizeof(P);
     return p;
 }
+
+template <typename T>
+struct LayoutSource {
+    const uint64_t* rp = nullptr;  // CSR (converter)
+    const int32_t* cols = nullptr;
+    const T* vals = nullptr;
+    const int32_t* ref_cols = nullptr;  // reference layout (import), ref_slots entries
+    const T* ref_vals = nullptr;
+    uint64_t ref_slots = 0;
+};
+
+template <typename T, typename TM>
+void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, const uint32_t* chunk_p, TM* tm,
+                         TM* assigned, const LayoutSource<T>& src, cudaStream_t s);
 
 template <typename T, typename TM>
 void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const T* vals, cudaStream_t s) {
@@ -544,6 +603,20 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
         LAUNCH_OK("k3_assign");
     }
 
+    layout_and_schedule<T, TM>(m, G, first_row.p, chunk.p, tm, assigned, LayoutSource<T>{rp, cols, vals}, s);
+}
+
+// K4 (offsets, descriptors, SpMV schedule) and K5 (the value/column blocks)
+// for groups given by first_row [G+1] / chunk [G] and tm / assigned, from a
+// CSR matrix (the converter) or from the reference arrays (import).
+template <typename T, typename TM>
+void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, const uint32_t* chunk_p, TM* tm,
+                         TM* assigned, const LayoutSource<T>& src, cudaStream_t s) {
+    const uint64_t N = m->num_rows, tpg = m->tpg;
+    const uint32_t N32 = uint32_t(N);
+    struct {
+        const uint32_t* p;
+    } chunk{chunk_p};
     // K4: offsets (+ total slots), descriptors.  The vector width V of the
     // SpMV also fixes the lane-compact stride granularity.
     const bool compact = m->layout == kLayoutCompact;
@@ -572,7 +645,9 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     if (stored_slots > kOffsetMask)
         fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: more than 2^48 stored slots");
     m->groups = dev_alloc<GroupDesc>(m, uint64_t(G) + 1);
-    k4_fill_desc<TM><<<grid_for(uint64_t(G) + 1, 256), 256, 0, s>>>(first_row.p, chunk.p, offset.p,
+    DevPtr<uint64_t> ref_off(src.ref_cols ? uint64_t(G) + 1 : 1, s);
+    if (src.ref_cols) exclusive_scan(SlotsOf{chunk.p, tpg}, G, ref_off.p, s);
+    k4_fill_desc<TM><<<grid_for(uint64_t(G) + 1, 256), 256, 0, s>>>(first_row, chunk.p, offset.p,
                                                                   compact ? off_heavy.p : nullptr, light_total,
                                                                   heavy_of, G, N32, m->groups);
     LAUNCH_OK("k4_fill_desc");
@@ -673,19 +748,43 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     // K5
     m->values = dev_alloc<T>(m, stored_slots);
     m->columns = dev_alloc<int32_t>(m, stored_slots);
-    // x remap (lane-compact only): stored columns index x' = x[perm]
-    uint64_t rp_ends[2] = {0, 0};
-    CUDA_OK(cudaMemcpyAsync(&rp_ends[0], rp, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaMemcpyAsync(&rp_ends[1], rp + N, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    CUDA_OK(cudaStreamSynchronize(s));
-    int32_t* col_map = build_xremap(m, cols + rp_ends[0], rp_ends[1] - rp_ends[0], m->xremap_mode, s);
-    if (G > 0 && stored_slots > 0) {
-        const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
-        k5_layout<T, TM><<<grid, 256, 0, s>>>(rp, cols, vals, m->groups, tm, assigned, col_map, G,
-                                             static_cast<T*>(m->values), m->columns);
-        LAUNCH_OK("k5_layout");
+    int32_t* col_map = nullptr;
+    if (src.ref_cols) {
+        // import: the reference blocks, checked (free lanes all padding,
+        // sentinels trailing per lane) and compacted
+        col_map = build_xremap(m, src.ref_cols, src.ref_slots, m->xremap_mode, s, true);
+        DevPtr<unsigned long long> cnt(2, s);
+        CUDA_OK(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), s));
+        if (G > 0 && total_slots > 0) {
+            const unsigned grid = unsigned(std::min<uint64_t>(G, 148u * 64u));
+            k5_from_reference<T, TM><<<grid, 256, 0, s>>>(m->groups, ref_off.p, tpg, assigned, src.ref_vals,
+                                                          src.ref_cols, col_map, G, static_cast<T*>(m->values),
+                                                          m->columns, cnt.p);
+            LAUNCH_OK("k5_from_reference");
+        }
+        unsigned long long h[2] = {0, 0};
+        CUDA_OK(cudaMemcpyAsync(h, cnt.p, sizeof h, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
+        if (h[1]) fail(ARGCSR_E_FORMAT, "argcsr import: " + std::to_string(h[1]) +
+                                            " slots break the ARG-CSR layout (free lanes must hold (0.0, -1) and "
+                                            "padding must trail each lane)");
+        m->nnz = h[0];
+    } else {
+        // x remap (lane-compact only): stored columns index x' = x[perm]
+        uint64_t rp_ends[2] = {0, 0};
+        CUDA_OK(cudaMemcpyAsync(&rp_ends[0], src.rp, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(&rp_ends[1], src.rp + N, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        col_map = build_xremap(m, src.cols + rp_ends[0], rp_ends[1] - rp_ends[0], m->xremap_mode, s, false);
+        if (G > 0 && stored_slots > 0) {
+            const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
+            k5_layout<T, TM><<<grid, 256, 0, s>>>(src.rp, src.cols, src.vals, m->groups, tm, assigned, col_map, G,
+                                                 static_cast<T*>(m->values), m->columns);
+            LAUNCH_OK("k5_layout");
+        }
+        if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
     }
-    if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
     CUDA_OK(cudaStreamSynchronize(s));
 }
 
@@ -702,6 +801,77 @@ __global__ void __launch_bounds__(1024) scan_partials_kernel(uint64_t* partial, 
         carry += tot;
     }
     if (threadIdx.x == 0) *total = carry;
+}
+
+namespace {
+
+// Import of the reference arrays (argcsr_dev_import): structural checks on the
+// host (groups tile the rows in order, reference offsets, threads_mapping
+// increasing within each group and <= threads_per_group), then the device
+// layout and SpMV schedule exactly as after a conversion.
+template <typename T>
+void import_typed(argcsr_dev* m, uint64_t G, const uint64_t* g4, const uint64_t* tm64, const T* vals,
+                  const int32_t* cols, uint64_t S, cudaStream_t s) {
+    const uint64_t N = m->num_rows, tpg = m->tpg;
+    std::vector<uint32_t> first(G + 1), chunk(G);
+    std::vector<uint16_t> tm(N), asg(G);
+    uint64_t row = 0, off = 0;
+    for (uint64_t g = 0; g < G; ++g) {
+        const uint64_t fr = g4[4 * g], size = g4[4 * g + 1], offset = g4[4 * g + 2], ch = g4[4 * g + 3];
+        const std::string at = " (group " + std::to_string(g) + ")";
+        if (fr != row || size == 0 || size > tpg || size > N - row)
+            fail(ARGCSR_E_FORMAT, "argcsr import: groups must tile the rows in order" + at);
+        if (offset != off) fail(ARGCSR_E_FORMAT, "argcsr import: offset is not threads_per_group * sum(chunk)" + at);
+        if (ch > 0xFFFFFFFFull || (ch && tpg > (S - off) / ch))
+            fail(ARGCSR_E_FORMAT, "argcsr import: chunk_size exceeds the value array" + at);
+        uint64_t prev = 0;
+        for (uint64_t r = fr; r < fr + size; ++r) {
+            if (tm64[r] <= prev || tm64[r] > tpg)
+                fail(ARGCSR_E_FORMAT, "argcsr import: threads_mapping must increase within a group and stay <= "
+                                      "threads_per_group" + at);
+            prev = tm64[r];
+            tm[r] = uint16_t(prev);
+        }
+        first[g] = uint32_t(fr);
+        chunk[g] = uint32_t(ch);
+        asg[g] = uint16_t(prev);
+        row += size;
+        off += ch * tpg;
+    }
+    if (row != N) fail(ARGCSR_E_FORMAT, "argcsr import: groups cover " + std::to_string(row) + " of " +
+                                            std::to_string(N) + " rows");
+    if (off != S) fail(ARGCSR_E_FORMAT, "argcsr import: value/column arrays hold " + std::to_string(S) +
+                                            " slots, the groups " + std::to_string(off));
+    first[G] = uint32_t(N);
+    m->num_groups = G;
+    DevPtr<uint32_t> d_first(G + 1, s), d_chunk(G, s);
+    DevPtr<int32_t> d_cols(S, s);
+    DevPtr<T> d_vals(S, s);
+    uint16_t* d_tm = dev_alloc<uint16_t>(m, N);
+    uint16_t* d_asg = dev_alloc<uint16_t>(m, G);
+    m->tm = d_tm;
+    m->assigned = d_asg;
+    CUDA_OK(cudaMemcpyAsync(d_first.p, first.data(), (G + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(d_chunk.p, chunk.data(), G * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(d_tm, tm.data(), N * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaMemcpyAsync(d_asg, asg.data(), G * sizeof(uint16_t), cudaMemcpyHostToDevice, s));
+    if (S) {
+        CUDA_OK(cudaMemcpyAsync(d_cols.p, cols, S * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        CUDA_OK(cudaMemcpyAsync(d_vals.p, vals, S * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    LayoutSource<T> src;
+    src.ref_cols = d_cols.p;
+    src.ref_vals = d_vals.p;
+    src.ref_slots = S;
+    layout_and_schedule<T, uint16_t>(m, uint32_t(G), d_first.p, d_chunk.p, d_tm, d_asg, src, s);
+}
+
+}  // namespace
+
+void import_reference(argcsr_dev* m, uint64_t G, const uint64_t* groups4, const uint64_t* tm, const void* vals,
+                      const int32_t* cols, uint64_t S, cudaStream_t s) {
+    if (m->dtype == ARGCSR_F64) import_typed<double>(m, G, groups4, tm, static_cast<const double*>(vals), cols, S, s);
+    else import_typed<float>(m, G, groups4, tm, static_cast<const float*>(vals), cols, S, s);
 }
 
 // threads_mapping and per-group assigned counts are u16 on the device

@@ -10,4 +10,10 @@ namespace argcsr_gpu {
 void convert_device_csr(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const void* vals,
                         cudaStream_t s);
 
+// Device handle from the reference arrays (host memory): groups as
+// {first_row, size, offset, chunk_size} x G, threads_mapping [num_rows],
+// values / columns [S].  m carries rows, cols, tpg, dtype, layout.
+void import_reference(argcsr_dev* m, uint64_t G, const uint64_t* groups4, const uint64_t* tm, const void* vals,
+                      const int32_t* cols, uint64_t S, cudaStream_t s);
+
 }  // namespace argcsr_gpu

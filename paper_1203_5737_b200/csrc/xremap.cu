@@ -35,10 +35,11 @@ unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
     return unsigned(std::max<uint64_t>(1, std::min<uint64_t>(b, cap)));
 }
 
-__global__ void k_col_hist(const int32_t* __restrict__ cols, uint64_t n, uint64_t num_cols,
+__global__ void k_col_hist(const int32_t* __restrict__ cols, uint64_t n, uint64_t num_cols, bool sentinels,
                            uint32_t* __restrict__ count, unsigned int* __restrict__ bad) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const int32_t c = cols[i];
+        if (sentinels && c == -1) continue;
         if (c < 0 || uint64_t(c) >= num_cols) {
             *bad = 1u;  // the converter does not validate (argcsr.cpp:107-117): no remap then
             continue;
@@ -50,20 +51,24 @@ __global__ void k_col_hist(const int32_t* __restrict__ cols, uint64_t n, uint64_
 // key: popularity octave, most-used first; unused columns last (255).
 __global__ void k_col_keys(const uint32_t* __restrict__ count, uint64_t n, uint8_t* __restrict__ key,
                            uint32_t* __restrict__ idx, unsigned long long* __restrict__ used,
-                           unsigned long long* __restrict__ lead_nnz, uint64_t K) {
-    uint64_t u = 0, lead = 0;
+                           unsigned long long* __restrict__ lead_nnz, unsigned long long* __restrict__ total,
+                           uint64_t K) {
+    uint64_t u = 0, lead = 0, tot = 0;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t c = count[i];
         key[i] = c == 0 ? uint8_t(255) : uint8_t(__clz(c));  // __clz(c) = 31 - floor(log2 c)
         idx[i] = uint32_t(i);
         u += c != 0;
+        tot += c;
         if (i < K) lead += c;
     }
     u = warp_sum_u64(u);
     lead = warp_sum_u64(lead);
+    tot = warp_sum_u64(tot);
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(used, (unsigned long long)u);
         atomicAdd(lead_nnz, (unsigned long long)lead);
+        atomicAdd(total, (unsigned long long)tot);
     }
 }
 
@@ -101,7 +106,7 @@ struct Tmp {
 
 }  // namespace
 
-int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode, cudaStream_t s) {
+int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode, cudaStream_t s, bool sentinels) {
     m->x_remap = false;
     m->n_used = m->num_cols;
     if (mode == kXRemapOff || m->layout != kLayoutCompact || m->num_cols == 0 || nnz == 0) return nullptr;
@@ -114,11 +119,11 @@ int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode
 
     Tmp<uint32_t> count(C, s);
     Tmp<unsigned int> bad(1, s);
-    Tmp<unsigned long long> acc(3, s);  // used, lead nnz, top nnz
+    Tmp<unsigned long long> acc(4, s);  // used, lead nnz, top nnz, total nnz
     CUDA_OK(cudaMemsetAsync(count.p, 0, C * sizeof(uint32_t), s));
     CUDA_OK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned int), s));
-    CUDA_OK(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), s));
-    k_col_hist<<<grid_for(nnz, 256), 256, 0, s>>>(cols, nnz, C, count.p, bad.p);
+    CUDA_OK(cudaMemsetAsync(acc.p, 0, 4 * sizeof(unsigned long long), s));
+    k_col_hist<<<grid_for(nnz, 256), 256, 0, s>>>(cols, nnz, C, sentinels, count.p, bad.p);
     LAUNCH_OK("k_col_hist");
     Tmp<uint8_t> key(C, s), key_sorted(C, s);
     Tmp<uint32_t> idx(C, s);
@@ -131,7 +136,7 @@ int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode
             if (!keep && p) cudaFree(p), p = nullptr;
         }
     } guard{perm};
-    k_col_keys<<<grid_for(C, 256), 256, 0, s>>>(count.p, C, key.p, idx.p, acc.p, acc.p + 1, K);
+    k_col_keys<<<grid_for(C, 256), 256, 0, s>>>(count.p, C, key.p, idx.p, acc.p, acc.p + 1, acc.p + 3, K);
     LAUNCH_OK("k_col_keys");
     size_t tmp_bytes = 0;
     CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key.p, key_sorted.p, idx.p, perm, int(C), 0, 8, s));
@@ -140,13 +145,14 @@ int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode
     k_top_nnz<<<grid_for(std::min<uint64_t>(K, C), 256), 256, 0, s>>>(perm, count.p, std::min<uint64_t>(K, C),
                                                                       acc.p + 2);
     LAUNCH_OK("k_top_nnz");
-    unsigned long long h[3] = {0, 0, 0};
+    unsigned long long h[4] = {0, 0, 0, 0};
     unsigned int hbad = 0;
     CUDA_OK(cudaMemcpyAsync(h, acc.p, sizeof h, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaMemcpyAsync(&hbad, bad.p, sizeof hbad, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaStreamSynchronize(s));
     if (hbad) return nullptr;
-    const double lead = double(h[1]) / double(nnz), top = double(h[2]) / double(nnz);
+    if (h[3] == 0) return nullptr;
+    const double lead = double(h[1]) / double(h[3]), top = double(h[2]) / double(h[3]);
     if (mode == kXRemapAuto && top < lead + 0.05) return nullptr;
 
     const uint64_t n_used = h[0];

@@ -6,11 +6,11 @@
 
 namespace argcsr_gpu {
 
-// Decides and builds the remap for handle m from the CSR columns (device,
-// nnz entries).  Returns the device array inv (old column -> stored column,
+// Decides and builds the remap for handle m from the column indices (device,
+// n entries; with `sentinels`, -1 entries are padding and skipped).  Returns the device array inv (old column -> stored column,
 // num_cols entries, cudaMallocAsync on s; the caller frees it) when the remap
 // is on, else nullptr.
-int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode, cudaStream_t s);
+int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t n, int mode, cudaStream_t s, bool sentinels);
 
 // x as the SpMV kernels read it: x itself, or x' = x[perm] gathered on s into
 // the handle's buffer.

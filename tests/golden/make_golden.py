@@ -14,6 +14,9 @@ Writes, next to this script:
                        conversion arrays and spmv_argcsr(probe_vector)
   corpus_digests.json  for all 500 corpus matrices, a digest of the reference
                        conversion + SpMV over the full GRID (checksum of checksums)
+  *.spfmt              the reference's binary container (io.cpp:242-298) as
+                       written by write_binary_file: e8 at (12, 2) and corpus[3]
+                       at (32, 4) as ARG-CSR, e8 as CSR
 """
 import hashlib
 import json
@@ -53,8 +56,11 @@ def main():
         out[f"values_{k}"], out[f"columns_{k}"] = M.values, M.columns
         out[f"y_{k}"] = ref.spmv_argcsr(M, x8)
     np.savez_compressed(HERE / "e8.npz", **out)
+    ref.write_binary(ref.argcsr_from_csr(A, 12, 2), str(HERE / "e8_argcsr_12_2.spfmt"))
+    ref.write_binary_csr(A, str(HERE / "e8_csr.spfmt"))
 
     corpus = ref.corpus(500)
+    ref.write_binary(ref.argcsr_from_csr(corpus[3], 32, 4), str(HERE / "corpus3_argcsr_32_4.spfmt"))
     c40 = {}
     for i, A in enumerate(corpus[:40]):
         c40[f"{i}_shape"] = np.array([A.num_rows, A.num_cols], np.uint64)

@@ -339,11 +339,12 @@ def run_b200(args):
             if args.power_iteration:
                 D.step(bufs[it[0] % 2], bufs[(it[0] + 1) % 2], pscale, ps2)
             else:
-                D.spmv_gather(bufs[it[0] % 2], bufs[(it[0] + 1) % 2])
+                D.spmv_gather(bufs[it[0] % 2], bufs[(it[0] + 1) % 2], wait=False)
             it[0] += 1
 
         for _ in range(args.warmup):
             step()
+        D.wait_gather()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -352,6 +353,7 @@ def run_b200(args):
         e0.record()
         for _ in range(args.steps):
             step()
+        D.wait_gather()  # the last all-gather is part of the timed region
         e1.record()
         torch.cuda.synchronize()
         if world > 1:

@@ -172,6 +172,15 @@ ARGCSR_API argcsr_status argcsr_dev_spmv_scaled(const argcsr_dev* m, const void*
 ARGCSR_API argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_t group_begin,
                                      uint64_t group_end, void* y, void* stream);
 
+/* The general form: rows of groups [group_begin, group_end) of y = A (s x),
+ * s = *x_scale on the device (NULL: 1).  ARGCSR_SPMV_REUSE_X lets a handle
+ * with the x remap on skip its x' gather and reuse the previous launch's x'
+ * (the multi-GPU step runs interior then boundary groups on the same x). */
+#define ARGCSR_SPMV_REUSE_X 1u
+ARGCSR_API argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, const double* x_scale,
+                                 uint64_t group_begin, uint64_t group_end, void* y, uint32_t flags,
+                                 void* stream);
+
 /* Host-buffer form of spmv_argcsr (argcsr.cpp:219-227): checks x_len ==
  * num_cols (DimensionError, same message shape), copies x in, multiplies,
  * copies y (num_rows entries) out, synchronises. */

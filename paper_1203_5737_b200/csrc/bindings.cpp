@@ -284,6 +284,15 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
                                               reinterpret_cast<void*>(stream)));
              },
              py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
+        .def("spmv_ex_device",
+             [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uint64_t gb, std::uint64_t ge,
+                std::uintptr_t y, std::uint32_t flags, std::uintptr_t stream) {
+                 check(argcsr_dev_spmv_ex(p.dev->handle(), reinterpret_cast<const void*>(x),
+                                          reinterpret_cast<const double*>(scale), gb, ge, reinterpret_cast<void*>(y),
+                                          flags, reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("group_begin"), py::arg("group_end"), py::arg("y_ptr"),
+             py::arg("flags") = 0u, py::arg("stream") = 0)
         .def("spmv_groups_device",
              [](const PyArgCsr& p, std::uintptr_t x, std::uint64_t gb, std::uint64_t ge, std::uintptr_t y,
                 std::uintptr_t stream) {

@@ -378,6 +378,18 @@ argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_
     });
 }
 
+argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, const double* x_scale, uint64_t group_begin,
+                                 uint64_t group_end, void* y, uint32_t flags, void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_ex: null vector");
+        if (flags & ~uint32_t(ARGCSR_SPMV_REUSE_X)) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_ex: unknown flags");
+        DeviceScope scope(m->device);
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream), x_scale,
+                                (flags & ARGCSR_SPMV_REUSE_X) != 0);
+    });
+}
+
 argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x, uint64_t x_len, void* y) {
     return guarded([&] {
         check_handle(m);

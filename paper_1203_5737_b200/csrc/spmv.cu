@@ -670,11 +670,11 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
 }  // namespace
 
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale) {
+                 cudaStream_t s, const double* x_scale, bool reuse_x) {
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
-    x = xremap_apply(m, x, s);
+    x = reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
     if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s);
     else launch_dtype<float>(m, x, x_scale, y, gb, ge, s);
 }

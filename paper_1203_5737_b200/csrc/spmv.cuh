@@ -10,7 +10,9 @@ namespace argcsr_gpu {
 // y = A (s * x), s = *x_scale (a device scalar, read by the kernel; NULL:
 // 1.0).  The scale is applied per gather (fl(s * x[c])), bit-identical to
 // scaling x first; 1.0 is an exact no-op.
+// reuse_x: an x remap handle skips its x' gather and reuses the x' of the
+// previous launch on this handle (same x, stream-ordered after it).
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale = nullptr);
+                 cudaStream_t s, const double* x_scale = nullptr, bool reuse_x = false);
 
 }  // namespace argcsr_gpu

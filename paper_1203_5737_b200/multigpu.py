@@ -17,6 +17,15 @@ y_k = A x_k.  The scaling of step k is fused into the gathers of SpMV k+1
 (argcsr_dev_spmv_scaled, bit-identical to scaling x first), and
 ||y_k||^2 is one 8-byte all-reduce of the per-rank partial sums.
 
+Overlap.  Each rank finds the longest run of its groups whose
+rows reference only columns it owns (interior groups; on a stencil slice all
+but the first and last ~n^2 rows).  A step computes the interior groups first
+(their x entries are the rank's own y from the previous step), then waits for
+the previous step's all-gather -- which ran on NCCL's stream meanwhile -- and
+computes the boundary groups; y is written straight into the rank's chunk of
+the next x buffer and the in-place all-gather of step k overlaps the interior
+SpMV of step k+1.
+
 The collectives and the per-rank engine are separable so the host logic runs
 on CPU with the gloo backend in tests (tests/test_multigpu_gloo.py), where a
 test-only engine (the oracle) stands in for the device.
@@ -66,6 +75,29 @@ class CsrSlice:
         return self.row_end - self.row_begin
 
 
+def interior_group_range(row_pointers, columns, first_rows, r0: int, r1: int) -> tuple[int, int]:
+    """Longest run [ga, gb) of groups whose rows reference only columns in
+    [r0, r1).  `first_rows` has G + 1 entries (the last one is num_rows);
+    row_pointers / columns are the slice's (rebased) arrays; works on numpy
+    arrays or torch tensors (device-side for the big ones)."""
+    t = torch.as_tensor(np.asarray(columns) if isinstance(columns, np.ndarray) else columns)
+    rp = torch.as_tensor(np.asarray(row_pointers, dtype=np.int64) if isinstance(row_pointers, np.ndarray)
+                         else row_pointers.to(torch.int64)).to(t.device)
+    bad = ((t < r0) | (t >= r1)).to(torch.int64)
+    cbad = torch.cat([torch.zeros(1, dtype=torch.int64, device=t.device), torch.cumsum(bad, 0)])
+    row_bad = (cbad[rp[1:]] - cbad[rp[:-1]] > 0).to(torch.int64)
+    rbad = torch.cat([torch.zeros(1, dtype=torch.int64, device=t.device), torch.cumsum(row_bad, 0)])
+    fr = torch.as_tensor(np.asarray(first_rows, dtype=np.int64)).to(t.device)
+    good = ~(rbad[fr[1:]] - rbad[fr[:-1]] > 0)
+    g = np.concatenate([[False], good.cpu().numpy(), [False]]).astype(np.int8)
+    edges = np.flatnonzero(np.diff(g))  # run starts and ends alternate
+    if edges.size == 0:
+        return 0, 0
+    starts, ends = edges[0::2], edges[1::2]
+    k = int(np.argmax(ends - starts))
+    return int(starts[k]), int(ends[k])
+
+
 def slice_rows(row_pointers, columns, values, num_cols: int, r0: int, r1: int) -> CsrSlice:
     a, b = int(row_pointers[r0]), int(row_pointers[r1])
     return CsrSlice(r0, r1, num_cols, row_pointers[r0:r1 + 1] - row_pointers[r0], columns[a:b], values[a:b])
@@ -95,6 +127,22 @@ class DeviceEngine:
         self.m.spmv_scaled_device(x.data_ptr(), 0 if x_scale is None else x_scale.data_ptr(), y.data_ptr(),
                                   self.stream.cuda_stream)
 
+    def spmv_range(self, x: torch.Tensor, y: torch.Tensor, g0: int, g1: int, x_scale: Optional[torch.Tensor] = None,
+                   reuse_x: bool = False) -> None:
+        """Rows of groups [g0, g1) of y = A (s * x) (argcsr_dev_spmv_ex)."""
+        if g1 <= g0:
+            return
+        self.m.spmv_ex_device(x.data_ptr(), 0 if x_scale is None else x_scale.data_ptr(), g0, g1, y.data_ptr(),
+                              1 if reuse_x else 0, self.stream.cuda_stream)
+
+    @property
+    def num_groups(self) -> int:
+        return self.m.num_groups
+
+    def group_first_rows(self) -> np.ndarray:
+        g = self.m.groups_array
+        return np.concatenate([g[:, 0], [self.m.num_rows]]).astype(np.int64)
+
 
 class DistributedArgCsr:
     """A row-partitioned ARG-CSR matrix across the ranks of `group`
@@ -103,7 +151,7 @@ class DistributedArgCsr:
     def __init__(self, num_rows: int, num_cols: int, row_pointers, columns, values, tpg: int = 128, dcs: int = 1,
                  group=None, device: Optional[torch.device] = None,
                  engine_factory: Optional[Callable[[CsrSlice], object]] = None, dtype=torch.float64,
-                 layout: str = "compact"):
+                 layout: str = "compact", overlap: bool = True):
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized()
         self.world = dist.get_world_size(group) if self.distributed else 1
@@ -124,6 +172,13 @@ class DistributedArgCsr:
         self.device = self.engine.device
         self.dtype = dtype
         self.y = torch.empty(self.slice.num_rows, dtype=dtype, device=self.device)
+        self.r0, self.r1 = r0, r1
+        self.overlap = overlap and self.world > 1
+        self.interior = (0, 0)
+        self._pending = []  # outstanding async gather works (overlap mode)
+        if self.overlap:
+            self.interior = interior_group_range(self.slice.row_pointers, self.slice.columns,
+                                                 self.engine.group_first_rows(), r0, r1)
 
     # ------------------------------------------------------------ collectives
     def gather(self, y_local: torch.Tensor, x_full: torch.Tensor) -> None:
@@ -143,16 +198,56 @@ class DistributedArgCsr:
                            group=self.group)
             off += n
 
+    def gather_async(self, x_full: torch.Tensor) -> None:
+        """In-place all-gather: this rank's chunk x_full[r0:r1] already holds
+        its y slice; the works complete on the collective stream."""
+        if len(set(self.counts)) == 1:
+            self._pending.append(dist.all_gather_into_tensor(x_full, x_full[self.r0:self.r1], group=self.group,
+                                                             async_op=True))
+            return
+        off = 0
+        for p, n in enumerate(self.counts):
+            src = dist.get_global_rank(self.group, p) if self.group is not None else p
+            self._pending.append(dist.broadcast(x_full[off:off + n], src=src, group=self.group, async_op=True))
+            off += n
+
+    def wait_gather(self) -> None:
+        """Stream-order (NCCL) or complete (gloo) the outstanding gathers."""
+        for w in self._pending:
+            w.wait()
+        self._pending = []
+
+    def _spmv_overlapped(self, xin: torch.Tensor, xout: torch.Tensor, x_scale: Optional[torch.Tensor]) -> torch.Tensor:
+        """Interior groups, wait for xin's gather, boundary groups; y into
+        xout's own chunk (returned as a view)."""
+        y = xout[self.r0:self.r1]
+        ga, gb = self.interior
+        G = self.engine.num_groups
+        self.engine.spmv_range(xin, y, ga, gb, x_scale)
+        self.wait_gather()
+        self.engine.spmv_range(xin, y, 0, ga, x_scale)
+        self.engine.spmv_range(xin, y, gb, G, x_scale, reuse_x=ga > 0)
+        return y
+
     def allreduce_sum(self, v: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
             dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
         return v
 
     # ------------------------------------------------------------------ steps
-    def spmv_gather(self, x_full: torch.Tensor, out_full: torch.Tensor, x_scale: Optional[torch.Tensor] = None) -> None:
-        """out = A (x_scale * x) assembled on every rank (iterated-SpMV step)."""
-        self.engine.spmv(x_full, self.y, x_scale)
-        self.gather(self.y, out_full)
+    def spmv_gather(self, x_full: torch.Tensor, out_full: torch.Tensor, x_scale: Optional[torch.Tensor] = None,
+                    wait: bool = True) -> None:
+        """out = A (x_scale * x) assembled on every rank (iterated-SpMV step).
+        In overlap mode the gather is left in flight unless `wait`; the next
+        spmv_gather on `out_full` (or wait_gather) orders it."""
+        if not self.overlap:
+            self.engine.spmv(x_full, self.y, x_scale)
+            self.gather(self.y, out_full)
+            return
+        self._spmv_overlapped(x_full, out_full, x_scale)
+        self.gather_async(out_full)
+        if wait:
+            self.wait_gather()
 
     def power_iteration(self, x0: torch.Tensor, iters: int):
         """`iters` steps of x <- A x / ||A x||; returns (lambda, x) with
@@ -162,6 +257,7 @@ class DistributedArgCsr:
         s2 = torch.zeros(1, dtype=torch.float64, device=self.device)
         for k in range(iters):
             self.step(buf[k % 2], buf[(k + 1) % 2], scale, s2)
+        self.wait_gather()
         lam = float(torch.sqrt(s2).item())  # the only host synchronisation
         x = buf[iters % 2] * scale  # materialise the last normalisation
         return lam, x
@@ -169,9 +265,16 @@ class DistributedArgCsr:
     def step(self, xin: torch.Tensor, xout: torch.Tensor, scale: torch.Tensor, s2: torch.Tensor) -> None:
         """One power-iteration step, device-side only: y = A (scale * xin);
         s2 = ||y||^2 (all-reduced); xout = all-gather(y); scale = 1/sqrt(s2)."""
-        self.engine.spmv(xin, self.y, scale)
-        y64 = self.y.to(torch.float64)
+        if self.overlap:
+            y = self._spmv_overlapped(xin, xout, scale)
+        else:
+            y = self.y
+            self.engine.spmv(xin, y, scale)
+        y64 = y.to(torch.float64)
         s2.copy_(torch.dot(y64, y64).reshape(1))
         self.allreduce_sum(s2)
-        self.gather(self.y, xout)
+        if self.overlap:
+            self.gather_async(xout)  # in flight under the next step's interior groups
+        else:
+            self.gather(y, xout)
         torch.reciprocal(torch.sqrt(s2), out=scale)

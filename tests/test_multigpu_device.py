@@ -40,3 +40,29 @@ def test_power_iteration_single_rank(tpg, dcs):
     lam_ref, x_ref = reference_power_iteration(A, x0, 30, tpg, dcs)
     assert abs(lam - lam_ref) <= 1e-10 * abs(lam_ref)
     assert np.max(np.abs(x.cpu().numpy() - x_ref)) <= 1e-9
+
+
+@pytest.mark.parametrize("x_remap", ["auto", "on"])
+def test_interior_boundary_split_is_bit_identical(argcsr, x_remap):
+    """The overlapped multi-GPU step computes interior groups, then the two
+    boundary ranges (the last one reusing x'); together they equal one SpMV."""
+    from paper_1203_5737_b200.multigpu import DeviceEngine, interior_group_range, slice_rows
+
+    A = stencil27(18)
+    sl = slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, 0, A.num_rows)
+    eng = DeviceEngine(sl, 128, 1, torch.device("cuda", 0))
+    if x_remap == "on":
+        eng.m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1,
+                                       x_remap="on")
+    r0, r1 = A.num_rows // 3, 2 * A.num_rows // 3  # pretend this rank owns the middle third of x
+    ga, gb = interior_group_range(A.row_pointers, A.columns, eng.group_first_rows(), r0, r1)
+    assert 0 < ga < gb < eng.num_groups
+    x = torch.linspace(-2, 2, A.num_cols, dtype=torch.float64, device="cuda")
+    s = torch.tensor([0.37], dtype=torch.float64, device="cuda")
+    y_full = torch.empty(A.num_rows, dtype=torch.float64, device="cuda")
+    eng.spmv(x, y_full, s)
+    y = torch.full_like(y_full, float("nan"))
+    eng.spmv_range(x, y, ga, gb, s)
+    eng.spmv_range(x, y, 0, ga, s)
+    eng.spmv_range(x, y, gb, eng.num_groups, s, reuse_x=True)
+    assert bits(y.cpu().numpy()) == bits(y_full.cpu().numpy())

@@ -36,6 +36,25 @@ class OracleEngine:
             xv = xv * x_scale.numpy()[0]
         y.copy_(torch.from_numpy(self.orc.spmv_argcsr(self.m, xv)))
 
+    @property
+    def num_groups(self):
+        return int(self.m.groups.shape[0])
+
+    def group_first_rows(self):
+        return np.concatenate([self.m.groups[:, 0], [self.m.num_rows]]).astype(np.int64)
+
+    def spmv_range(self, x, y, g0, g1, x_scale=None, reuse_x=False):
+        """Rows of groups [g0, g1) only (spmv_argcsr_groups semantics)."""
+        if g1 <= g0:
+            return
+        xv = x.numpy()
+        if x_scale is not None:
+            xv = xv * x_scale.numpy()[0]
+        full = self.orc.spmv_argcsr(self.m, xv)
+        a = int(self.m.groups[g0, 0])
+        b = int(self.m.groups[g1, 0]) if g1 < self.num_groups else self.m.num_rows
+        y[a:b] = torch.from_numpy(full[a:b])
+
 
 def reference_power_iteration(A, x0, iters, tpg, dcs):
     """Single-process CPU run of the same algorithm (oracle SpMV, sequential norm)."""
@@ -63,7 +82,7 @@ def _matrix(kind):
     return powerlaw_csr(3001, 3001, seed=4, heavy_rows=[(7, 2000)])
 
 
-def _worker(rank, world, port, kind, tpg, dcs, iters, out):
+def _worker(rank, world, port, kind, tpg, dcs, iters, out, overlap):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, str(ROOT))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -73,7 +92,7 @@ def _worker(rank, world, port, kind, tpg, dcs, iters, out):
 
         A = _matrix(kind)
         D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values, tpg, dcs,
-                              engine_factory=lambda sl: OracleEngine(sl, tpg, dcs))
+                              engine_factory=lambda sl: OracleEngine(sl, tpg, dcs), overlap=overlap)
         # the slice's conversion equals the reference conversion of the slice
         sl = D.slice
         want = oracle.orc().argcsr_from_csr(D.engine.csr, tpg, dcs)
@@ -84,19 +103,21 @@ def _worker(rank, world, port, kind, tpg, dcs, iters, out):
         D.spmv_gather(x0, out_full)
         lam, x = D.power_iteration(x0, iters)
         res = dict(rank=rank, bounds=D.bounds.tolist(), counts=D.counts, r0=sl.row_begin, r1=sl.row_end,
-                   y1=out_full.numpy().copy(), lam=lam, x=x.numpy().copy())
+                   y1=out_full.numpy().copy(), lam=lam, x=x.numpy().copy(), interior=D.interior,
+                   groups=D.engine.num_groups)
         torch.save(res, out / f"rank{rank}.pt")
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,tpg,dcs", [("stencil", 128, 1), ("stencil8", 128, 32), ("powerlaw", 32, 4)])
-def test_two_rank_power_iteration_gloo(tmp_path, kind, tpg, dcs):
+@pytest.mark.parametrize("kind,tpg,dcs,overlap", [("stencil", 128, 1, True), ("stencil8", 128, 32, True),
+                                                  ("powerlaw", 32, 4, True), ("stencil", 128, 1, False)])
+def test_two_rank_power_iteration_gloo(tmp_path, kind, tpg, dcs, overlap):
     import oracle
 
     port = 29500 + (os.getpid() % 1000)
     iters = 12
-    mp.start_processes(_worker, args=(2, port, kind, tpg, dcs, iters, tmp_path), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, port, kind, tpg, dcs, iters, tmp_path, overlap), nprocs=2, join=True,
                        start_method="spawn")
     res = [torch.load(tmp_path / f"rank{r}.pt", weights_only=False) for r in range(2)]
     A = _matrix(kind)
@@ -115,6 +136,11 @@ def test_two_rank_power_iteration_gloo(tmp_path, kind, tpg, dcs):
     for r in res:
         assert np.all(np.abs(r["y1"] - y_full) <= 1e-12 * absrow)
         assert np.array_equal(r["y1"], res[0]["y1"])  # every rank holds the same gathered y
+    if overlap and kind.startswith("stencil"):
+        for r in res:  # a stencil slice: interior groups between its boundary layers (none at the matrix ends)
+            ga, gb = r["interior"]
+            assert ga < gb
+            assert (ga > 0) == (r["r0"] > 0) and (gb < r["groups"]) == (r["r1"] < A.num_rows)
     lam_ref, x_ref = reference_power_iteration(A, x0, iters, tpg, dcs)
     for r in res:
         assert abs(r["lam"] - lam_ref) <= 1e-10 * abs(lam_ref)

@@ -324,7 +324,7 @@ def run_b200(args):
             total_ms = sum(spmv_times)
             step_ms = total_ms / args.steps
         sampler.mark_end()
-        launches = args.steps * ((1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0))
+        launches = args.steps * ((1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0) + (1 if m.x_remap else 0))
     else:
         bufs = [x, xg]
         it = [0]

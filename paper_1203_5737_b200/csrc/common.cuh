@@ -118,6 +118,7 @@ struct argcsr_dev {
     void* xbuf = nullptr;                 // [n_used] x' (one SpMV in flight per handle)
     uint64_t n_used = 0;                  // columns with at least one entry (remap on) or num_cols
     double x_cover_lead = 0, x_cover_top = 0;  // nnz share of the window: leading columns / remapped
+    double run_pairs_orig = 0, run_pairs_remap = 0;  // long rows: share of consecutive column pairs
 
     // x residency (L2 persisting window) — queried, not hard-coded.
     size_t l2_persist_max = 0;

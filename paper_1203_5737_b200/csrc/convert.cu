@@ -776,7 +776,8 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         CUDA_OK(cudaMemcpyAsync(&rp_ends[0], src.rp, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaMemcpyAsync(&rp_ends[1], src.rp + N, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
-        col_map = build_xremap(m, src.cols + rp_ends[0], rp_ends[1] - rp_ends[0], m->xremap_mode, s, false);
+        col_map = build_xremap(m, src.cols + rp_ends[0], rp_ends[1] - rp_ends[0], m->xremap_mode, s, false, src.rp,
+                               src.cols);
         if (G > 0 && stored_slots > 0) {
             const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
             k5_layout<T, TM><<<grid, 256, 0, s>>>(src.rp, src.cols, src.vals, m->groups, tm, assigned, col_map, G,

@@ -123,12 +123,66 @@ __device__ __forceinline__ double ld_x(const float* p, uint64_t pol) {
     return double(v);
 }
 
+// x runs: 2 or 4 consecutive x entries in one 16-/32-byte load (one L1
+// wavefront instead of 2 or 4 for a warp whose lanes are far apart).
+__device__ __forceinline__ void ld_x2(const double* p, double (&v)[2], uint64_t pol) {
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_x2(const float* p, double (&v)[2], uint64_t pol) {
+    float a, b;
+    asm("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(a), "=f"(b) : "l"(p), "l"(pol));
+    v[0] = a, v[1] = b;
+}
+__device__ __forceinline__ void ld_x4(const double* p, double (&v)[4], uint64_t pol) {
+    asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_x4(const float* p, double (&v)[4], uint64_t pol) {
+    float a, b, c, d;
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(p), "l"(pol));
+    v[0] = a, v[1] = b, v[2] = c, v[3] = d;
+}
+
+// x of U consecutive element steps of ONE lane (V = 1: the heavy path).  A
+// lane holds a contiguous run of its row's entries, so when the columns of 4
+// (2) steps are consecutive and the first is 4- (2-) element aligned, one
+// vector load replaces 4 (2) gathers.  Same values, so bit-identical.
+template <typename T, int U>
+__device__ __forceinline__ void gather_lane_runs(const T* x, const int (&c)[U][1], double (&xv)[U][1], uint64_t pol) {
+#pragma unroll
+    for (int q = 0; q < U / 4; ++q) {
+        const int c0 = c[4 * q][0];
+        const bool run4 = c0 >= 0 && (c0 & 3) == 0 && c[4 * q + 1][0] == c0 + 1 && c[4 * q + 2][0] == c0 + 2 &&
+                          c[4 * q + 3][0] == c0 + 3;
+        if (run4) {
+            double t[4];
+            ld_x4(x + c0, t, pol);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) xv[4 * q + k][0] = t[k];
+            continue;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int a = c[4 * q + 2 * h][0], b = c[4 * q + 2 * h + 1][0];
+            if (a >= 0 && (a & 1) == 0 && b == a + 1) {
+                double t[2];
+                ld_x2(x + a, t, pol);
+                xv[4 * q + 2 * h][0] = t[0], xv[4 * q + 2 * h + 1][0] = t[1];
+            } else {
+                xv[4 * q + 2 * h][0] = a != -1 ? ld_x(x + a, pol) : 0.0;
+                xv[4 * q + 2 * h + 1][0] = b != -1 ? ld_x(x + b, pol) : 0.0;
+            }
+        }
+    }
+}
+
 // Phase 1 (argcsr.cpp:193-203) for V adjacent lanes starting at slot0: per
 // lane, sum += v * x[c] over j ascending until the first sentinel.  Columns
 // and values of U element steps are issued together (values of a fully
 // finished vector are skipped when PRED); the layout keeps sentinels
 // trailing, so "skip sentinel" == "stop at the first sentinel".
-template <typename T, int V, int U, bool PRED>
+template <typename T, int V, int U, bool PRED, bool HEAVY_RUNS = false>
 __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, uint64_t stride,
                                        double (&s)[V], uint64_t pol_stream, uint64_t pol_x, double xs,
                                        uint32_t jstart = 0) {
@@ -167,11 +221,15 @@ __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uin
             }
         }
         double xv[U][V];
+        if constexpr (V == 1 && U % 4 == 0 && HEAVY_RUNS) {
+            gather_lane_runs<T, U>(a.x, c, xv, pol_x);
+        } else {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int l = 0; l < V; ++l)
-                xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
+                for (int l = 0; l < V; ++l)
+                    xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
+        }
         if (a.x_scale) {  // uniform: fused normalisation of the power iteration
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -213,7 +271,7 @@ __device__ __forceinline__ uint32_t find_le(const uint32_t* arr, uint32_t n, uin
 
 // Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
 // order, one lane per thread.
-template <typename T, int UH>
+template <typename T, int UH, bool RUNS>
 __global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -244,7 +302,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvA
         if (g < a.g_begin || g >= a.g_end) continue;
         const GroupDesc d = a.groups[g];
         double s[1];
-        phase1<T, 1, UH, false>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream, pol_x, xs);
+        phase1<T, 1, UH, false, RUNS>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream, pol_x,
+                                      xs);
         s_part[l] = s[0];
     }
     __syncthreads();
@@ -512,8 +571,9 @@ int variant_id() {
         const char* e = std::getenv("ARGCSR_SPMV_VARIANT");
         if (!e) return -1;
         const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
-                               "-", "-", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "LPD4P0B4", "LPD2P0B6"};
-        for (int i = 0; i < 15; ++i)
+                               "U8P0B2", "U8P0B3", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "LPD4P0B4", "LPD2P0B6",
+                               "U6P0B3"};
+        for (int i = 0; i < 16; ++i)
             if (!std::strcmp(e, names[i])) return i;
         return -1;
     }();
@@ -617,6 +677,9 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
         case 5: launch_light<T, V, 8, true, 2>(m, a, s); break;
         case 6: launch_light<T, V, 4, true, 4>(m, a, s); break;
         case 7: launch_light<T, V, 2, true, 8>(m, a, s); break;
+        case 8: launch_light<T, V, 8, false, 2>(m, a, s); break;
+        case 9: launch_light<T, V, 8, false, 3>(m, a, s); break;
+        case 15: launch_light<T, V, 6, false, 3>(m, a, s); break;
         default: launch_light<T, V, 4, true, 4>(m, a, s); break;
     }
 }
@@ -654,7 +717,22 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     }
     if (m->heavy_ctas > 0) {
         const size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
-        launch(spmv_heavy_kernel<T, 16>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
+        // vector x loads where the long rows' stored columns run consecutively
+        // (measured per matrix by the converter, xremap.cu)
+        double runs = m->x_remap ? m->run_pairs_remap : m->run_pairs_orig;
+        if (const char* e = std::getenv("ARGCSR_HEAVY_RUNS")) runs = e[0] == '1' ? 1.0 : 0.0;  // experiments
+        // (the run-loading kernel holds more registers: 8 steps in flight
+        // per lane measured best for it, 16 for the scalar one)
+        const char* uh = std::getenv("ARGCSR_HEAVY_U");  // experiments: 8 | 16
+        if (runs >= 0.5 && sizeof(T) == sizeof(double)) {
+            if (uh && uh[0] == '1')
+                launch(spmv_heavy_kernel<T, 16, true>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
+            else
+                launch(spmv_heavy_kernel<T, 8, true>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
+        } else if (uh && uh[0] == '8')
+            launch(spmv_heavy_kernel<T, 8, false>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
+        else
+            launch(spmv_heavy_kernel<T, 16, false>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
     }
     switch (m->lanes_per_unit) {
         case 4: launch_v<T, 4>(m, a, s); break;

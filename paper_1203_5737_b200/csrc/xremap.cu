@@ -13,10 +13,12 @@
 // reference's.
 //
 // It is applied only where it pays (auto mode): x larger than the window AND
-// the window, filled popularity-first, covers >= 5% more of the nnz than the
-// window over the leading columns.  R-MAT qualifies (leading 90% vs 100% at
-// 2^22); stencils on one GPU do not; a row slice of a stencil on one of P GPUs
-// does (it touches ~1/P of x).
+// the window, filled popularity-first, covers >= 25 points more of the nnz
+// than the window over the leading columns.  A row slice of a stencil on one
+// of P GPUs qualifies (it touches ~1/P of x, often none of the leading
+// columns); R-MAT 2^24 does not (leading 90% vs 100%: measured, the x' gather
+// costs more than the misses it saves); stencils on one GPU do
+// not.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -81,6 +83,41 @@ __global__ void k_top_nnz(const uint32_t* __restrict__ perm, const uint32_t* __r
     if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)t);
 }
 
+// Consecutive-column pairs inside long rows (>= kLongRow entries; they form
+// the heavy groups): in the input order and in the remapped order.  A lane of
+// a heavy group holds a contiguous run of its row, so consecutive stored
+// columns let the heavy kernel load x in 16/32-byte runs (spmv.cu).
+constexpr uint64_t kLongRow = 256;
+__global__ void k_long_row_runs(const uint64_t* __restrict__ rp, uint64_t N, const int32_t* __restrict__ cols,
+                                const int32_t* __restrict__ inv, uint64_t num_cols,
+                                unsigned long long* __restrict__ acc /* long nnz, pairs, orig, remapped */) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    uint64_t ln = 0, pairs = 0, orig = 0, rem = 0;
+    for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < N; r += nw) {
+        const uint64_t b = rp[r], e = rp[r + 1];
+        if (e - b < kLongRow) continue;
+        if (lane == 0) ln += e - b;
+        for (uint64_t k = b + lane; k + 1 < e; k += 32) {
+            const int32_t c0 = cols[k], c1 = cols[k + 1];
+            if (c0 < 0 || c1 < 0 || uint64_t(c0) >= num_cols || uint64_t(c1) >= num_cols) continue;
+            ++pairs;
+            orig += c1 == c0 + 1;
+            rem += inv[c1] == inv[c0] + 1;
+        }
+    }
+    ln = warp_sum_u64(ln);
+    pairs = warp_sum_u64(pairs);
+    orig = warp_sum_u64(orig);
+    rem = warp_sum_u64(rem);
+    if (lane == 0) {
+        atomicAdd(acc, (unsigned long long)ln);
+        atomicAdd(acc + 1, (unsigned long long)pairs);
+        atomicAdd(acc + 2, (unsigned long long)orig);
+        atomicAdd(acc + 3, (unsigned long long)rem);
+    }
+}
+
 __global__ void k_inverse(const uint32_t* __restrict__ perm, uint64_t n_used, int32_t* __restrict__ inv) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_used;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -106,7 +143,8 @@ struct Tmp {
 
 }  // namespace
 
-int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode, cudaStream_t s, bool sentinels) {
+int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode, cudaStream_t s, bool sentinels,
+                      const uint64_t* rp, const int32_t* cols_abs) {
     m->x_remap = false;
     m->n_used = m->num_cols;
     if (mode == kXRemapOff || m->layout != kLayoutCompact || m->num_cols == 0 || nnz == 0) return nullptr;
@@ -115,7 +153,8 @@ int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode
     const size_t sv = m->dtype == ARGCSR_F64 ? sizeof(double) : sizeof(float);
     const size_t win = std::min<size_t>(size_t(m->l2_window_max), m->l2_persist_max);
     const uint64_t K = win / sv;  // x elements the window holds
-    if (mode == kXRemapAuto && (win == 0 || C <= K)) return nullptr;
+    const bool fits = win == 0 || C <= K;
+    if (mode == kXRemapAuto && fits && !rp) return nullptr;
 
     Tmp<uint32_t> count(C, s);
     Tmp<unsigned int> bad(1, s);
@@ -153,13 +192,36 @@ int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode
     if (hbad) return nullptr;
     if (h[3] == 0) return nullptr;
     const double lead = double(h[1]) / double(h[3]), top = double(h[2]) / double(h[3]);
-    if (mode == kXRemapAuto && top < lead + 0.05) return nullptr;
-
     const uint64_t n_used = h[0];
     int32_t* inv = nullptr;
     CUDA_OK(cudaMallocAsync(&inv, C * sizeof(int32_t), s));
+    struct InvGuard {
+        int32_t*& p;
+        cudaStream_t s;
+        bool keep = false;
+        ~InvGuard() {
+            if (!keep && p) cudaFreeAsync(p, s), p = nullptr;
+        }
+    } inv_guard{inv, s};
     k_inverse<<<grid_for(n_used, 256), 256, 0, s>>>(perm, n_used, inv);
     LAUNCH_OK("k_inverse");
+    bool on = mode == kXRemapOn || (!fits && top >= lead + 0.25);
+    if (!on && rp && m->dtype == ARGCSR_F64) {
+        // the second reason: long rows whose columns become consecutive (fp64:
+        // measured on C4; an fp32 handle's heavy kernel loses)
+        Tmp<unsigned long long> runs(4, s);
+        CUDA_OK(cudaMemsetAsync(runs.p, 0, 4 * sizeof(unsigned long long), s));
+        k_long_row_runs<<<grid_for(m->num_rows * 32, 256), 256, 0, s>>>(rp, m->num_rows, cols_abs, inv, C, runs.p);
+        LAUNCH_OK("k_long_row_runs");
+        unsigned long long r[4] = {0, 0, 0, 0};
+        CUDA_OK(cudaMemcpyAsync(r, runs.p, sizeof r, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        on = r[1] > 0 && double(r[0]) >= 0.2 * double(h[3]) && double(r[3]) - double(r[2]) >= 0.5 * double(r[1]);
+        m->run_pairs_orig = r[1] ? double(r[2]) / double(r[1]) : 0.0;
+        m->run_pairs_remap = r[1] ? double(r[3]) / double(r[1]) : 0.0;
+    }
+    if (!on) return nullptr;
+    inv_guard.keep = true;
     guard.keep = true;
     m->perm = perm;
     m->device_bytes += C * sizeof(uint32_t);

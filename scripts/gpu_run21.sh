@@ -1,0 +1,5 @@
+for c in C4f32 C4; do timeout 600 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --no-variants > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "$c rc=$?"; python -c "
+import json; d=json.load(open('gpurun_out/bench_$c.json'))
+print('$c', d['value'], 'frac', d['roofline']['frac'], 'remap', d['format']['x_remap'], 'conv', d['conversion_ms'])
+"; done
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,l1tex__throughput.avg.pct_of_peak_sustained_active -k regex:spmv_ -s 10 -c 2 --csv python bench.py --config C4 --steps 5 --warmup 5 --no-variants --no-cpu-baseline 2>/dev/null | grep -v "^==" | cut -d, -f5,13- | tail -6

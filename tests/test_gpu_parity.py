@@ -332,3 +332,39 @@ def test_torch_device_path(argcsr, orc):
     assert bits(y.cpu().numpy()) == bits(orc.spmv_argcsr(orc.argcsr_from_csr(A, 128, 1), x.cpu().numpy()))
     with pytest.raises(argcsr.DimensionError):
         argcsr.spmv_torch(dev, x[:-1])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_dense_rows_vector_x_runs(argcsr, orc, dtype, layout):
+    """Long rows whose columns run consecutively (directly, or after the x
+    remap for strided dense rows) take the heavy kernel's vector x loads;
+    results stay bit-identical (fp32: one rounding of the fp64 sum)."""
+    rng = np.random.default_rng(3)
+    n = 6000
+    rows, cols = [], []
+    for r in range(n):
+        if r % 1500 == 7:
+            c = np.arange(0, n, 3) if r % 3000 == 7 else np.arange(r % 11, n - 5)  # strided / consecutive dense rows
+        else:
+            c = np.unique(np.clip(r + rng.integers(-3, 4, 3), 0, n - 1))
+        rows.append(np.full(c.size, r))
+        cols.append(c)
+    r_ = np.concatenate(rows)
+    c_ = np.concatenate(cols).astype(np.int32)
+    rp = np.zeros(n + 1, np.uint64)
+    np.add.at(rp, r_ + 1, 1)
+    vals = rng.uniform(-1, 1, c_.size)
+    if dtype == np.float32:
+        vals = vals.astype(np.float32).astype(np.float64)
+    A = Csr(n, n, np.cumsum(rp).astype(np.uint64), c_, vals)
+    ref_m = orc.argcsr_from_csr(A, 128, 1)
+    dev = to_dev(argcsr, A, 128, 1, dtype=dtype, layout=layout)
+    assert dev.heavy_groups > 0
+    x = np.sin(np.arange(n)).astype(dtype)
+    y = argcsr.spmv(dev, x)
+    y_ref = orc.spmv_argcsr(ref_m, x.astype(np.float64))
+    if dtype == np.float64:
+        assert bits(y) == bits(y_ref)
+    else:
+        assert np.array_equal(y, y_ref.astype(np.float32))

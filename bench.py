@@ -367,7 +367,11 @@ def run_b200(args):
         if args.power_iteration:
             pi_lambda = float(torch.sqrt(ps2).item())
         step_ms = total_ms / args.steps
-        launches = args.steps * ((1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0))
+        per_call = (1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0)
+        if D.overlap:  # interior + two boundary ranges; the last reuses the x' gather
+            launches = args.steps * (3 * per_call + (2 if m.x_remap else 0))
+        else:
+            launches = args.steps * (per_call + (1 if m.x_remap else 0))
     sampler.stop()
     clocks = sampler.summary()
 

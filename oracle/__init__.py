@@ -412,6 +412,31 @@ class _Ref:
         finally:
             self.lib.ref_argcsr_free(h)
 
+    def read_matrix_market(self, path: str) -> Csr:
+        """The reference's read_matrix_market_file, run in a helper process
+        (_ref/ref_mm_tool) that writes the CsrMatrix as the reference's CSR
+        container; parsed here (io.cpp:250-257, 313-320)."""
+        import struct
+        import subprocess
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as d:
+            out = Path(d) / "a.spfmt"
+            r = subprocess.run([str(REF_SO.parent / "ref_mm_tool"), str(path), str(out)], capture_output=True,
+                               text=True)
+            if r.returncode:
+                raise OracleError(-1, r.stdout.strip() or r.stderr.strip())
+            raw = out.read_bytes()
+        assert raw[:8] == b"SPFMTBIN" and raw[12] == 0
+        nr, nc = struct.unpack_from("<2Q", raw, 13)
+        pos, arrs = 29, []
+        for dt in ("<f8", "<i4", "<u8"):
+            (n,) = struct.unpack_from("<Q", raw, pos)
+            arrs.append(np.frombuffer(raw, dt, n, pos + 8).copy())
+            pos += 8 + n * np.dtype(dt).itemsize
+        vals, cols, rp = arrs
+        return Csr(nr, nc, rp, cols, vals)
+
     def write_binary_csr(self, A: Csr, path: str):
         h = self.csr_handle(A)
         try:

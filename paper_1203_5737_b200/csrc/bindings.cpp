@@ -9,7 +9,11 @@
 #include <pybind11/stl.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cstring>
+#include <fstream>
+#include <iomanip>
+#include <sstream>
 #include <memory>
 #include <optional>
 #include <tuple>
@@ -54,6 +58,88 @@ CsrMatrix csr_from_triplets(std::size_t num_rows, std::size_t num_cols, std::vec
     }
     for (std::size_t r = 0; r < num_rows; ++r) A.row_pointers[r + 1] += A.row_pointers[r];
     return A;
+}
+
+// ---------------------------------------------------------------- Matrix Market
+// read_matrix_market / write_matrix_market (proj/src/io.cpp:42-160): the
+// coordinate format, real / integer / pattern fields, general / symmetric /
+// skew-symmetric symmetry (mirrored off-diagonal entries, negated for skew),
+// 1-based indices, duplicates summed by csr_from_triplets; the same error
+// classes and messages.
+std::string lower(std::string s) {
+    for (char& c : s) c = char(std::tolower(static_cast<unsigned char>(c)));
+    return s;
+}
+
+bool next_data_line(std::istream& in, std::string& line) {
+    while (std::getline(in, line)) {
+        std::size_t i = 0;
+        while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+        if (i == line.size() || line[i] == '%') continue;
+        return true;
+    }
+    return false;
+}
+
+CsrMatrix read_matrix_market(std::istream& in) {
+    std::string banner;
+    if (!std::getline(in, banner)) throw ParseError("matrix market: empty stream");
+    std::istringstream hs(banner);
+    std::string tag, object, format, field, symmetry;
+    hs >> tag >> object >> format >> field >> symmetry;
+    if (lower(tag) != "%%matrixmarket" || !hs) throw ParseError("matrix market: malformed header line");
+    object = lower(object), format = lower(format), field = lower(field), symmetry = lower(symmetry);
+    if (object != "matrix") throw UnsupportedError("matrix market: object '" + object + "' not supported");
+    if (format != "coordinate") {
+        if (format == "array") throw UnsupportedError("matrix market: array format not supported");
+        throw ParseError("matrix market: unknown format '" + format + "'");
+    }
+    const bool pattern = field == "pattern";
+    if (!pattern && field != "real" && field != "integer") {
+        if (field == "complex") throw UnsupportedError("matrix market: complex field not supported");
+        throw ParseError("matrix market: unknown field '" + field + "'");
+    }
+    const bool symmetric = symmetry == "symmetric", skew = symmetry == "skew-symmetric";
+    if (!symmetric && !skew && symmetry != "general") {
+        if (symmetry == "hermitian") throw UnsupportedError("matrix market: hermitian symmetry not supported");
+        throw ParseError("matrix market: unknown symmetry '" + symmetry + "'");
+    }
+    std::string line;
+    if (!next_data_line(in, line)) throw ParseError("matrix market: missing size line");
+    std::istringstream ss(line);
+    long long rows = 0, cols = 0, entries = 0;
+    if (!(ss >> rows >> cols >> entries) || rows < 0 || cols < 0 || entries < 0)
+        throw ParseError("matrix market: malformed size line '" + line + "'");
+    if (rows == 0 || cols == 0) throw ParseError("matrix market: matrix dimensions must be positive");
+    std::vector<Triplet> triplets;
+    triplets.reserve(std::size_t(entries) * (symmetric || skew ? 2 : 1));
+    for (long long k = 0; k < entries; ++k) {
+        if (!next_data_line(in, line))
+            throw ParseError("matrix market: expected " + std::to_string(entries) + " entries, got " +
+                             std::to_string(k));
+        std::istringstream es(line);
+        long long i = 0, j = 0;
+        double v = 1.0;
+        if (!(es >> i >> j)) throw ParseError("matrix market: malformed entry '" + line + "'");
+        if (!pattern && !(es >> v)) throw ParseError("matrix market: entry missing value '" + line + "'");
+        if (i < 1 || i > rows || j < 1 || j > cols)
+            throw BoundsError("matrix market: entry (" + std::to_string(i) + ", " + std::to_string(j) + ") outside " +
+                              std::to_string(rows) + "x" + std::to_string(cols));
+        const std::size_t r = std::size_t(i - 1), c = std::size_t(j - 1);
+        triplets.push_back({r, c, v});
+        if ((symmetric || skew) && r != c) triplets.push_back({c, r, skew ? -v : v});
+    }
+    return csr_from_triplets(std::size_t(rows), std::size_t(cols), std::move(triplets));
+}
+
+void write_matrix_market(std::ostream& out, const CsrMatrix& A) {
+    out << "%%MatrixMarket matrix coordinate real general\n";
+    out << A.num_rows << ' ' << A.num_cols << ' ' << A.nnz() << '\n';
+    out << std::setprecision(17);
+    for (std::size_t r = 0; r < A.num_rows; ++r)
+        for (std::size_t k = A.row_pointers[r]; k < A.row_pointers[r + 1]; ++k)
+            out << (r + 1) << ' ' << (A.columns[k] + 1) << ' ' << A.values[k] << '\n';
+    if (!out) throw IoError("matrix market: write failure");
 }
 
 template <typename T>
@@ -370,6 +456,23 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         },
         py::arg("matrix"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
         py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);
+
+    m.def(
+        "read_matrix_market",
+        [](const std::string& path) {
+            std::ifstream in(path);
+            if (!in) throw IoError("cannot open '" + path + "' for reading");
+            return read_matrix_market(in);
+        },
+        py::arg("path"));
+    m.def(
+        "write_matrix_market",
+        [](const std::string& path, const CsrMatrix& A) {
+            std::ofstream out(path);
+            if (!out) throw IoError("cannot open '" + path + "' for writing");
+            write_matrix_market(out, A);
+        },
+        py::arg("path"), py::arg("matrix"));
 
     m.def(
         "write_binary",

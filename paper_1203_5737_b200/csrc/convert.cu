@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) k5_from_reference(const GroupDesc* __rest
 uint64_t tile_threads_setting() {
     const char* e = std::getenv("ARGCSR_TILE_THREADS");
     const long v = e ? std::atol(e) : 0;
-    return (v == 128 || v == 256 || v == 512 || v == 1024 || v == 2048) ? uint64_t(v) : uint64_t(kDefaultTileUnits);
+    return (v >= 128 && v <= 2048 && v % 128 == 0) ? uint64_t(v) : uint64_t(kDefaultTileUnits);
 }
 
 unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {

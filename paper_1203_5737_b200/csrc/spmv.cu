@@ -572,8 +572,8 @@ int variant_id() {
         if (!e) return -1;
         const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
                                "U8P0B2", "U8P0B3", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "LPD4P0B4", "LPD2P0B6",
-                               "U6P0B3"};
-        for (int i = 0; i < 16; ++i)
+                               "U6P0B3", "U4P0B5", "U3P0B5", "U4P0B6"};
+        for (int i = 0; i < 19; ++i)
             if (!std::strcmp(e, names[i])) return i;
         return -1;
     }();
@@ -656,9 +656,10 @@ template <typename T, int V>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     int vid = variant_id();
     if (vid < 0) {
-        // Default: hardware-dispatched tiles, unpredicated value loads
-        // (measured best on C1-C4 with the lane-compact layout, scripts/sweep.sh).
-        vid = 2;
+        // Default: hardware-dispatched tiles, unpredicated value loads, 5 CTAs
+        // per SM (measured best on C2-C4 with the lane-compact layout,
+        // scripts/sweep.sh).
+        vid = 16;
     }
     switch (vid) {
         case 0: launch_lightp<T, V, 4, true, 4, false>(m, a, s); return;
@@ -680,6 +681,9 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
         case 8: launch_light<T, V, 8, false, 2>(m, a, s); break;
         case 9: launch_light<T, V, 8, false, 3>(m, a, s); break;
         case 15: launch_light<T, V, 6, false, 3>(m, a, s); break;
+        case 16: launch_light<T, V, 4, false, 5>(m, a, s); break;
+        case 17: launch_light<T, V, 3, false, 5>(m, a, s); break;
+        case 18: launch_light<T, V, 4, false, 6>(m, a, s); break;
         default: launch_light<T, V, 4, true, 4>(m, a, s); break;
     }
 }

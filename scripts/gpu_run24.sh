@@ -1,0 +1,3 @@
+V="U4P0B5 U4P0B6 U4P0B4"
+CONFIGS="C2:1 C2:32 C3:1 C4:1 C4f32:1 C1:1" LAYOUTS="compact" VARIANTS="$V" STEPS=50 timeout 1500 bash scripts/sweep.sh > /dev/null 2>&1
+cat gpurun_out/sweep.txt

@@ -469,6 +469,25 @@ def variants(args, A, x, tdtype, sv, stream, spmv_fn, x_remap=False):
                     "total_slots": m2.total_slots, "stored_slots": m2.stored_slots, "groups": m2.num_groups})
         m2.free()
         del m2
+    # the paper's comparison formats on the device (csrc/ellpack.cu)
+    for name, slice_size in (("sliced_ellpack_32", 32), ("ellpack", 0)):
+        try:
+            E = argcsr._ext.sell_from_device_csr(
+                A.num_rows, A.num_cols, A.nnz, A.row_pointers.data_ptr(), A.columns.data_ptr(),
+                A.values.to(tdtype).contiguous().data_ptr(), "float64" if sv == 8 else "float32", slice_size,
+                x.device.index, stream.cuda_stream)
+
+            def ell(_m, xx, yy, st, E=E):
+                E.spmv_device(xx.data_ptr(), yy.data_ptr(), st.cuda_stream)
+
+            ts = time_spmv(None, x, y, min(args.steps, 50), args.warmup, stream, ell)
+            ms = statistics.median(ts)
+            res.append({"impl": name, "ms": ms, "gflops": 2 * A.nnz / ms / 1e6, "eff_GBps": ab / ms / 1e6,
+                        "total_slots": E.total_slots})
+            del E
+        except Exception as e:  # ELLPACK pads every row to the widest: power-law rows do not fit
+            res.append({"impl": name, "error": str(e)[:160]})
+        torch.cuda.empty_cache()
     try:
         csr = torch.sparse_csr_tensor(A.row_pointers, A.columns.to(torch.int64), A.values.to(tdtype),
                                       size=(A.num_rows, A.num_cols))

@@ -218,6 +218,43 @@ ARGCSR_API argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_fo
 
 ARGCSR_API void argcsr_dev_free(argcsr_dev* m);
 
+/* ------------------------------------------- ELLPACK / Sliced ELLPACK */
+
+/* The paper's comparison formats (proj/include/argcsr/ellpack.hpp): an
+ * opaque device matrix in the reference layout -- slice s is a columnwise
+ * block, slot j of local row r at slice_offsets[s] + j * rows_in_slice + r,
+ * padding (0.0, -1) trailing; ELLPACK is one slice of all rows. */
+typedef struct argcsr_sell argcsr_sell;
+
+typedef struct {
+    uint64_t num_rows;
+    uint64_t num_cols;
+    uint64_t slice_size;   /* num_rows for ELLPACK */
+    uint64_t num_slices;
+    uint64_t total_slots;
+    uint64_t width;        /* widest slice (EllpackMatrix::width) */
+    uint64_t device_bytes;
+    int32_t device;
+    argcsr_dtype dtype;
+    uint32_t ellpack;      /* 1: made by argcsr_ell_convert */
+} argcsr_sell_info_t;
+
+/* ellpack_from_csr (ellpack.cpp:7-24) on the device. */
+ARGCSR_API argcsr_status argcsr_ell_convert(const argcsr_csr_view* csr, int device, void* stream, argcsr_sell** out);
+/* sliced_from_csr(A, slice_size = 32) (ellpack.cpp:26-60); slice_size 0 -> ParameterError. */
+ARGCSR_API argcsr_status argcsr_sell_convert(const argcsr_csr_view* csr, uint64_t slice_size, int device,
+                                  void* stream, argcsr_sell** out);
+ARGCSR_API argcsr_status argcsr_sell_info(const argcsr_sell* m, argcsr_sell_info_t* info);
+/* Host copies of the reference fields; any pointer may be NULL. */
+ARGCSR_API argcsr_status argcsr_sell_export(const argcsr_sell* m, uint64_t* slice_widths, uint64_t* slice_offsets,
+                                 void* values, int32_t* columns);
+/* spmv_ellpack / spmv_sliced (ellpack.cpp:121-176), bit-identical fp64; device
+ * pointers, stream-ordered. */
+ARGCSR_API argcsr_status argcsr_sell_spmv(const argcsr_sell* m, const void* x, void* y, void* stream);
+/* Host vectors, synchronous; x_len != num_cols -> DimensionError (ellpack.cpp:135-139). */
+ARGCSR_API argcsr_status argcsr_sell_spmv_host(const argcsr_sell* m, const void* x, uint64_t x_len, void* y);
+ARGCSR_API void argcsr_sell_free(argcsr_sell* m);
+
 /* ------------------------------------------------------- import / binary */
 
 /* The reference ArgCsrMatrix (argcsr.hpp:52-63) as host arrays. */

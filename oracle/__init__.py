@@ -232,6 +232,15 @@ class _Ref:
         L.ref_time_spmv_csr_parallel.argtypes = [vp, f64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, f64p]
         L.ref_write_binary_argcsr.argtypes = [vp, C.c_char_p]
         L.ref_write_binary_csr.argtypes = [vp, C.c_char_p]
+        L.ref_ellpack_from_csr.restype = vp
+        L.ref_ellpack_from_csr.argtypes = [vp]
+        L.ref_sliced_from_csr.argtypes = [vp, C.c_uint64, C.POINTER(vp)]
+        L.ref_ell_fields.argtypes = [vp, u64p, u64p, f64p, i32p]
+        L.ref_sell_fields.argtypes = [vp, u64p, u64p, u64p, u64p, f64p, i32p]
+        L.ref_spmv_ellpack.argtypes = [vp, f64p, C.c_uint64, f64p]
+        L.ref_spmv_sliced.argtypes = [vp, f64p, C.c_uint64, f64p]
+        L.ref_ell_free.argtypes = [vp]
+        L.ref_sell_free.argtypes = [vp]
         L.ref_hardware_threads.restype = C.c_uint64
 
     def _check(self, st: int):
@@ -436,6 +445,49 @@ class _Ref:
             pos += 8 + n * np.dtype(dt).itemsize
         vals, cols, rp = arrs
         return Csr(nr, nc, rp, cols, vals)
+
+    def ellpack(self, A: Csr, x=None):
+        """ellpack_from_csr(A) fields (width, values, columns) and, with x, spmv_ellpack(M, x)."""
+        h = self.csr_handle(A)
+        e = self.lib.ref_ellpack_from_csr(h)
+        self.lib.ref_csr_free(h)
+        try:
+            w, n = C.c_uint64(), C.c_uint64()
+            self.lib.ref_ell_fields(e, C.byref(w), C.byref(n), None, None)
+            vals, cols = np.zeros(n.value), np.zeros(n.value, np.int32)
+            self.lib.ref_ell_fields(e, C.byref(w), C.byref(n), _p(vals, f64p), _p(cols, i32p))
+            y = None
+            if x is not None:
+                x = np.ascontiguousarray(x, np.float64)
+                y = np.zeros(A.num_rows)
+                self._check(self.lib.ref_spmv_ellpack(e, _p(x, f64p), x.size, _p(y, f64p)))
+            return w.value, vals, cols, y
+        finally:
+            self.lib.ref_ell_free(e)
+
+    def sliced(self, A: Csr, slice_size: int, x=None):
+        """sliced_from_csr(A, slice_size) fields and, with x, spmv_sliced(M, x)."""
+        h = self.csr_handle(A)
+        out = C.c_void_p()
+        st = self.lib.ref_sliced_from_csr(h, slice_size, C.byref(out))
+        self.lib.ref_csr_free(h)
+        self._check(st)
+        e = out.value
+        try:
+            ns, n = C.c_uint64(), C.c_uint64()
+            self.lib.ref_sell_fields(e, C.byref(ns), C.byref(n), None, None, None, None)
+            w, o = np.zeros(ns.value, np.uint64), np.zeros(ns.value, np.uint64)
+            vals, cols = np.zeros(n.value), np.zeros(n.value, np.int32)
+            self.lib.ref_sell_fields(e, C.byref(ns), C.byref(n), _p(w, u64p), _p(o, u64p), _p(vals, f64p),
+                                     _p(cols, i32p))
+            y = None
+            if x is not None:
+                x = np.ascontiguousarray(x, np.float64)
+                y = np.zeros(A.num_rows)
+                self._check(self.lib.ref_spmv_sliced(e, _p(x, f64p), x.size, _p(y, f64p)))
+            return w, o, vals, cols, y
+        finally:
+            self.lib.ref_sell_free(e)
 
     def write_binary_csr(self, A: Csr, path: str):
         h = self.csr_handle(A)

@@ -22,6 +22,7 @@
 
 #include "argcsr/analysis.hpp"
 #include "argcsr/argcsr.hpp"
+#include "argcsr/ellpack.hpp"
 #include "argcsr/bench.hpp"
 #include "argcsr/core.hpp"
 #include "argcsr/io.hpp"
@@ -349,6 +350,45 @@ int ref_write_binary_argcsr(const void* h, const char* path) {
 int ref_write_binary_csr(const void* csr, const char* path) {
     return guarded([&] { write_binary_file(path, *static_cast<const CsrMatrix*>(csr)); });
 }
+
+// ELLPACK / Sliced ELLPACK (ellpack.cpp): conversions, fields, SpMV.
+void* ref_ellpack_from_csr(const void* csr) {
+    return new EllpackMatrix(ellpack_from_csr(*static_cast<const CsrMatrix*>(csr)));
+}
+int ref_sliced_from_csr(const void* csr, uint64_t slice_size, void** out) {
+    return guarded([&] { *out = new SlicedEllpackMatrix(sliced_from_csr(*static_cast<const CsrMatrix*>(csr), slice_size)); });
+}
+void ref_ell_fields(const void* h, uint64_t* width, uint64_t* slots, double* vals, int32_t* cols) {
+    const auto* M = static_cast<const EllpackMatrix*>(h);
+    *width = M->width;
+    *slots = M->values.size();
+    if (vals) std::copy(M->values.begin(), M->values.end(), vals);
+    if (cols) std::copy(M->columns.begin(), M->columns.end(), cols);
+}
+void ref_sell_fields(const void* h, uint64_t* nslices, uint64_t* slots, uint64_t* widths, uint64_t* offsets, double* vals,
+                     int32_t* cols) {
+    const auto* M = static_cast<const SlicedEllpackMatrix*>(h);
+    *nslices = M->num_slices();
+    *slots = M->values.size();
+    if (widths) std::copy(M->slice_widths.begin(), M->slice_widths.end(), widths);
+    if (offsets) std::copy(M->slice_offsets.begin(), M->slice_offsets.end(), offsets);
+    if (vals) std::copy(M->values.begin(), M->values.end(), vals);
+    if (cols) std::copy(M->columns.begin(), M->columns.end(), cols);
+}
+int ref_spmv_ellpack(const void* h, const double* x, uint64_t nx, double* y) {
+    return guarded([&] {
+        const DenseVector r = spmv_ellpack(*static_cast<const EllpackMatrix*>(h), DenseVector(x, x + nx));
+        std::copy(r.begin(), r.end(), y);
+    });
+}
+int ref_spmv_sliced(const void* h, const double* x, uint64_t nx, double* y) {
+    return guarded([&] {
+        const DenseVector r = spmv_sliced(*static_cast<const SlicedEllpackMatrix*>(h), DenseVector(x, x + nx));
+        std::copy(r.begin(), r.end(), y);
+    });
+}
+void ref_ell_free(void* h) { delete static_cast<EllpackMatrix*>(h); }
+void ref_sell_free(void* h) { delete static_cast<SlicedEllpackMatrix*>(h); }
 
 uint64_t ref_hardware_threads(void) { return std::thread::hardware_concurrency(); }
 

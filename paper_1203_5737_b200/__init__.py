@@ -47,6 +47,12 @@ CsrMatrix = _ext.CsrMatrix
 GroupInfo = _ext.GroupInfo
 FormatStats = _ext.FormatStats
 ArgCsrMatrix = _ext.ArgCsrMatrix
+EllpackMatrix = _ext.EllpackMatrix
+SlicedEllpackMatrix = _ext.SlicedEllpackMatrix
+ellpack_from_csr = _ext.ellpack_from_csr
+sliced_from_csr = _ext.sliced_from_csr
+csr_from_ellpack = _ext.csr_from_ellpack
+csr_from_sliced = _ext.csr_from_sliced
 
 kDefaultThreadsPerGroup = _ext.kDefaultThreadsPerGroup
 kDefaultDesiredChunkSize = _ext.kDefaultDesiredChunkSize
@@ -157,8 +163,16 @@ def spmv(matrix: ArgCsrMatrix, x):
     numpy array, a torch CUDA tensor gives a torch CUDA tensor (stream-ordered
     on the current stream).  A wrong length raises DimensionError.
     """
+    if isinstance(matrix, (EllpackMatrix, SlicedEllpackMatrix)):  # ellpack.cpp:132-176
+        host = _ext.spmv_ellpack_host if isinstance(matrix, EllpackMatrix) else _ext.spmv_sliced_host
+        if type(x).__module__.startswith("torch"):
+            return spmv_torch(matrix, x)
+        if isinstance(x, _np.ndarray):
+            return host(matrix, x)
+        return host(matrix, _np.asarray(x, dtype=_np.float64)).tolist()
     if not isinstance(matrix, ArgCsrMatrix):
-        raise UnsupportedError("spmv: only ArgCsrMatrix runs on the device path; convert with argcsr_from_csr")
+        raise UnsupportedError("spmv: only the device formats (ARG-CSR, ELLPACK, sliced ELLPACK) run here; "
+                               "convert with argcsr_from_csr")
     mod = type(x).__module__
     if mod.startswith("torch"):
         return spmv_torch(matrix, x)
@@ -171,7 +185,7 @@ def spmv_torch(matrix: ArgCsrMatrix, x, out=None, stream=None):
     """y = A x for torch CUDA tensors, launched on `stream` (default: current)."""
     import torch
 
-    want = torch.float64 if matrix.dtype == "float64" else torch.float32
+    want = torch.float64 if getattr(matrix, "dtype", "float64") == "float64" else torch.float32
     if not x.is_cuda or x.dtype != want:
         raise ParameterError(f"spmv: x must be a CUDA {want} tensor")
     if x.numel() != matrix.num_cols:

@@ -18,8 +18,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 
-CUDA_SOURCES = ["capi.cu", "convert.cu", "spmv.cu", "inverse.cu", "xremap.cu"]
-CUDA_HEADERS = ["common.cuh", "scan.cuh", "convert.cuh", "spmv.cuh", "inverse.cuh", "xremap.cuh"]
+CUDA_SOURCES = ["capi.cu", "convert.cu", "spmv.cu", "inverse.cu", "xremap.cu", "ellpack.cu"]
+CUDA_HEADERS = ["common.cuh", "scan.cuh", "convert.cuh", "spmv.cuh", "inverse.cuh", "xremap.cuh", "ellpack.cuh"]
 LIB = PKG / "libargcsr_gpu.so"
 EXT = PKG / ("_argcsr_gpu" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 

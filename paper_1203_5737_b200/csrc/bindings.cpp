@@ -185,6 +185,102 @@ struct PyArgCsr {
     }
 };
 
+// ELLPACK / Sliced ELLPACK device matrices (argcsr_sell*); the two Python
+// classes share one handle type, like the reference's two structs share a
+// layout (ellpack.hpp:13-45).
+struct SellHandle {
+    argcsr_sell* h = nullptr;
+    argcsr_sell_info_t info{};
+    explicit SellHandle(argcsr_sell* p) : h(p) { check(argcsr_sell_info(h, &info)); }
+    ~SellHandle() { argcsr_sell_free(h); }
+    SellHandle(const SellHandle&) = delete;
+    SellHandle& operator=(const SellHandle&) = delete;
+};
+struct PySellBase {
+    std::shared_ptr<SellHandle> s;
+    const argcsr_sell_info_t& info() const { return s->info; }
+    py::array values() const {
+        const bool f64 = info().dtype == ARGCSR_F64;
+        py::array v = f64 ? py::array(py::array_t<double>(py::ssize_t(info().total_slots)))
+                          : py::array(py::array_t<float>(py::ssize_t(info().total_slots)));
+        check(argcsr_sell_export(s->h, nullptr, nullptr, v.mutable_data(), nullptr));
+        return v;
+    }
+    py::array_t<int32_t> columns() const {
+        py::array_t<int32_t> c(py::ssize_t(info().total_slots));
+        check(argcsr_sell_export(s->h, nullptr, nullptr, nullptr, c.mutable_data()));
+        return c;
+    }
+    std::vector<uint64_t> widths() const {
+        std::vector<uint64_t> w(info().num_slices);
+        check(argcsr_sell_export(s->h, w.data(), nullptr, nullptr, nullptr));
+        return w;
+    }
+    std::vector<uint64_t> offsets() const {
+        std::vector<uint64_t> o(info().num_slices);
+        check(argcsr_sell_export(s->h, nullptr, o.data(), nullptr, nullptr));
+        return o;
+    }
+    // csr_from_ellpack / csr_from_sliced (ellpack.cpp:62-119): read each row's
+    // slots up to the first padding, in slot order.
+    CsrMatrix to_csr() const {
+        if (info().dtype != ARGCSR_F64) throw UnsupportedError("csr_from_sliced: fp32 matrix");
+        const uint64_t N = info().num_rows, S = info().slice_size;
+        std::vector<double> v(info().total_slots);
+        std::vector<int32_t> c(info().total_slots);
+        std::vector<uint64_t> w = widths(), o = offsets();
+        check(argcsr_sell_export(s->h, nullptr, nullptr, v.data(), c.data()));
+        CsrMatrix A;
+        A.num_rows = N;
+        A.num_cols = info().num_cols;
+        A.row_pointers.assign(N + 1, 0);
+        for (uint64_t sl = 0; sl < w.size(); ++sl) {
+            const uint64_t first = sl * S, rows = std::min(first + S, N) - first;
+            for (uint64_t local = 0; local < rows; ++local)
+                for (uint64_t j = 0; j < w[sl]; ++j) {
+                    const uint64_t slot = o[sl] + j * rows + local;
+                    if (c[slot] == -1) break;
+                    A.values.push_back(v[slot]);
+                    A.columns.push_back(c[slot]);
+                    A.row_pointers[first + local + 1] += 1;
+                }
+        }
+        for (uint64_t r = 0; r < N; ++r) A.row_pointers[r + 1] += A.row_pointers[r];
+        return A;
+    }
+};
+struct PyEllpack : PySellBase {};
+struct PySliced : PySellBase {};
+
+argcsr_csr_view host_view(const CsrMatrix& A) {
+    argcsr_csr_view v{};
+    v.num_rows = A.num_rows;
+    v.num_cols = A.num_cols;
+    v.nnz = A.nnz();
+    v.row_pointers = reinterpret_cast<const uint64_t*>(A.row_pointers.data());
+    v.columns = A.columns.data();
+    v.values = A.values.data();
+    v.dtype = ARGCSR_F64;
+    v.space = ARGCSR_HOST;
+    return v;
+}
+
+template <typename P>
+py::array sell_spmv_host(const P& p, py::array x) {
+    const bool f64 = p.info().dtype == ARGCSR_F64;
+    py::array xc = f64 ? py::array(py::array_t<double, py::array::c_style | py::array::forcecast>(x))
+                       : py::array(py::array_t<float, py::array::c_style | py::array::forcecast>(x));
+    py::array y = new_array(f64, p.info().num_rows);
+    const void* xp = xc.data();
+    void* yp = y.mutable_data();
+    const uint64_t n = uint64_t(xc.size());
+    {
+        py::gil_scoped_release nogil;
+        check(argcsr_sell_spmv_host(p.s->h, xp, n, yp));
+    }
+    return y;
+}
+
 PyArgCsr make_handle(argcsr_dev* h) {
     PyArgCsr p;
     p.dev = std::make_shared<DeviceArgCsr>(h);
@@ -456,6 +552,101 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         },
         py::arg("matrix"), py::arg("threads_per_group") = kDefaultThreadsPerGroup,
         py::arg("desired_chunk_size") = kDefaultDesiredChunkSize, py::arg("device") = 0, py::arg("flags") = 0u);
+
+    py::class_<PyEllpack>(m, "EllpackMatrix")
+        .def_property_readonly("num_rows", [](const PyEllpack& p) { return p.info().num_rows; })
+        .def_property_readonly("dtype", [](const PyEllpack& p) { return p.info().dtype == ARGCSR_F64 ? "float64" : "float32"; })
+        .def_property_readonly("num_cols", [](const PyEllpack& p) { return p.info().num_cols; })
+        .def_property_readonly("width", [](const PyEllpack& p) { return p.info().width; })
+        .def_property_readonly("total_slots", [](const PyEllpack& p) { return p.info().total_slots; })
+        .def_property_readonly("device_bytes", [](const PyEllpack& p) { return p.info().device_bytes; })
+        .def_property_readonly("values", [](const PyEllpack& p) { return p.values(); })
+        .def_property_readonly("columns", [](const PyEllpack& p) { return p.columns(); })
+        .def("spmv_device", [](const PyEllpack& p, std::uintptr_t x, std::uintptr_t y, std::uintptr_t stream) {
+            check(argcsr_sell_spmv(p.s->h, reinterpret_cast<const void*>(x), reinterpret_cast<void*>(y),
+                                   reinterpret_cast<void*>(stream)));
+        }, py::arg("x_ptr"), py::arg("y_ptr"), py::arg("stream") = 0);
+    py::class_<PySliced>(m, "SlicedEllpackMatrix")
+        .def_property_readonly("num_rows", [](const PySliced& p) { return p.info().num_rows; })
+        .def_property_readonly("dtype", [](const PySliced& p) { return p.info().dtype == ARGCSR_F64 ? "float64" : "float32"; })
+        .def_property_readonly("num_cols", [](const PySliced& p) { return p.info().num_cols; })
+        .def_property_readonly("slice_size", [](const PySliced& p) { return p.info().slice_size; })
+        .def_property_readonly("total_slots", [](const PySliced& p) { return p.info().total_slots; })
+        .def_property_readonly("device_bytes", [](const PySliced& p) { return p.info().device_bytes; })
+        .def("num_slices", [](const PySliced& p) { return p.info().num_slices; })
+        .def_property_readonly("slice_widths", [](const PySliced& p) { return p.widths(); })
+        .def_property_readonly("slice_offsets", [](const PySliced& p) { return p.offsets(); })
+        .def_property_readonly("values", [](const PySliced& p) { return p.values(); })
+        .def_property_readonly("columns", [](const PySliced& p) { return p.columns(); })
+        .def("spmv_device", [](const PySliced& p, std::uintptr_t x, std::uintptr_t y, std::uintptr_t stream) {
+            check(argcsr_sell_spmv(p.s->h, reinterpret_cast<const void*>(x), reinterpret_cast<void*>(y),
+                                   reinterpret_cast<void*>(stream)));
+        }, py::arg("x_ptr"), py::arg("y_ptr"), py::arg("stream") = 0);
+
+    m.def(
+        "ellpack_from_csr",
+        [](const CsrMatrix& A, int device) {
+            const argcsr_csr_view v = host_view(A);
+            argcsr_sell* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_ell_convert(&v, device, nullptr, &h));
+            }
+            PyEllpack p;
+            p.s = std::make_shared<SellHandle>(h);
+            return p;
+        },
+        py::arg("matrix"), py::arg("device") = 0);
+    m.def(
+        "sliced_from_csr",
+        [](const CsrMatrix& A, std::size_t slice_size, int device) {
+            const argcsr_csr_view v = host_view(A);
+            argcsr_sell* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                check(argcsr_sell_convert(&v, slice_size, device, nullptr, &h));
+            }
+            PySliced p;
+            p.s = std::make_shared<SellHandle>(h);
+            return p;
+        },
+        py::arg("matrix"), py::arg("slice_size") = 32, py::arg("device") = 0);
+    m.def(
+        "sell_from_device_csr",
+        [](std::uint64_t num_rows, std::uint64_t num_cols, std::uint64_t nnz, std::uintptr_t rp, std::uintptr_t cols,
+           std::uintptr_t vals, const std::string& dtype, std::size_t slice_size, int device, std::uintptr_t stream) {
+            argcsr_csr_view v{};
+            v.num_rows = num_rows;
+            v.num_cols = num_cols;
+            v.nnz = nnz;
+            v.row_pointers = reinterpret_cast<const uint64_t*>(rp);
+            v.columns = reinterpret_cast<const int32_t*>(cols);
+            v.values = reinterpret_cast<const void*>(vals);
+            v.dtype = dtype == "float32" ? ARGCSR_F32 : ARGCSR_F64;
+            v.space = ARGCSR_DEVICE;
+            argcsr_sell* h = nullptr;
+            {
+                py::gil_scoped_release nogil;
+                if (slice_size == 0) check(argcsr_ell_convert(&v, device, reinterpret_cast<void*>(stream), &h));
+                else check(argcsr_sell_convert(&v, slice_size, device, reinterpret_cast<void*>(stream), &h));
+            }
+            auto hs = std::make_shared<SellHandle>(h);
+            if (slice_size == 0) {
+                PyEllpack p;
+                p.s = hs;
+                return py::cast(p);
+            }
+            PySliced p;
+            p.s = hs;
+            return py::cast(p);
+        },
+        py::arg("num_rows"), py::arg("num_cols"), py::arg("nnz"), py::arg("row_pointers_ptr"), py::arg("columns_ptr"),
+        py::arg("values_ptr"), py::arg("dtype") = "float64", py::arg("slice_size") = 0, py::arg("device") = 0,
+        py::arg("stream") = 0);
+    m.def("csr_from_ellpack", [](const PyEllpack& p) { return p.to_csr(); }, py::arg("matrix"));
+    m.def("csr_from_sliced", [](const PySliced& p) { return p.to_csr(); }, py::arg("matrix"));
+    m.def("spmv_ellpack_host", &sell_spmv_host<PyEllpack>, py::arg("matrix"), py::arg("x"));
+    m.def("spmv_sliced_host", &sell_spmv_host<PySliced>, py::arg("matrix"), py::arg("x"));
 
     m.def(
         "read_matrix_market",

@@ -13,6 +13,7 @@
 #include "argcsr_gpu.h"
 #include "common.cuh"
 #include "convert.cuh"
+#include "ellpack.cuh"
 #include "inverse.cuh"
 #include "spmv.cuh"
 
@@ -504,6 +505,159 @@ argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_format_stats*
 }
 
 void argcsr_dev_free(argcsr_dev* m) { free_handle(m); }
+
+// ------------------------------------------------- ELLPACK / Sliced ELLPACK
+namespace {
+void free_sell(argcsr_sell* m) {
+    if (!m) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    cudaFree(m->width);
+    cudaFree(m->offset);
+    cudaFree(m->values);
+    cudaFree(m->columns);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete m;
+}
+
+argcsr_status sell_convert_common(const argcsr_csr_view* csr, uint64_t slice_size, bool ellpack, int device,
+                                  void* stream, argcsr_sell** out) {
+    return guarded([&] {
+        const char* who = ellpack ? "ellpack_from_csr" : "sliced_from_csr";
+        if (!csr || !out) fail(ARGCSR_E_PARAMETER, std::string(who) + ": null argument");
+        *out = nullptr;
+        if (!ellpack && slice_size == 0) fail(ARGCSR_E_PARAMETER, "sliced_from_csr: slice_size must be at least 1");
+        if (csr->dtype != ARGCSR_F64 && csr->dtype != ARGCSR_F32) fail(ARGCSR_E_PARAMETER, std::string(who) + ": unknown dtype");
+        if (!csr->row_pointers || (csr->nnz && (!csr->columns || !csr->values)))
+            fail(ARGCSR_E_PARAMETER, std::string(who) + ": null CSR array");
+        DeviceScope scope(device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto* m = new argcsr_sell;
+        m->device = device;
+        m->dtype = csr->dtype;
+        m->ellpack = ellpack;
+        m->num_rows = csr->num_rows;
+        m->num_cols = csr->num_cols;
+        m->nnz = csr->nnz;
+        m->slice_size = ellpack ? std::max<uint64_t>(csr->num_rows, 1) : slice_size;
+        try {
+            const size_t es = elem_size(csr->dtype);
+            const uint64_t N = csr->num_rows, nnz = csr->nnz;
+            const uint64_t* rp = csr->row_pointers;
+            const int32_t* cols = csr->columns;
+            const void* vals = csr->values;
+            void* staged[3] = {nullptr, nullptr, nullptr};
+            struct Release {
+                void** p;
+                cudaStream_t s;
+                ~Release() {
+                    for (int i = 0; i < 3; ++i)
+                        if (p[i]) cudaFreeAsync(p[i], s);
+                }
+            } release{staged, s};
+            if (csr->space == ARGCSR_HOST) {
+                CUDA_OK(cudaMallocAsync(&staged[0], (N + 1) * sizeof(uint64_t), s));
+                CUDA_OK(cudaMallocAsync(&staged[1], std::max<uint64_t>(nnz, 1) * sizeof(int32_t), s));
+                CUDA_OK(cudaMallocAsync(&staged[2], std::max<uint64_t>(nnz, 1) * es, s));
+                CUDA_OK(cudaMemcpyAsync(staged[0], rp, (N + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+                if (nnz) {
+                    CUDA_OK(cudaMemcpyAsync(staged[1], cols, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+                    CUDA_OK(cudaMemcpyAsync(staged[2], vals, nnz * es, cudaMemcpyHostToDevice, s));
+                }
+                rp = static_cast<const uint64_t*>(staged[0]);
+                cols = static_cast<const int32_t*>(staged[1]);
+                vals = staged[2];
+            }
+            argcsr_gpu::sell_convert(m, rp, cols, vals, s);
+        } catch (...) {
+            free_sell(m);
+            throw;
+        }
+        *out = m;
+    });
+}
+}  // namespace
+
+argcsr_status argcsr_ell_convert(const argcsr_csr_view* csr, int device, void* stream, argcsr_sell** out) {
+    return sell_convert_common(csr, 0, true, device, stream, out);
+}
+
+argcsr_status argcsr_sell_convert(const argcsr_csr_view* csr, uint64_t slice_size, int device, void* stream,
+                                  argcsr_sell** out) {
+    return sell_convert_common(csr, slice_size, false, device, stream, out);
+}
+
+argcsr_status argcsr_sell_info(const argcsr_sell* m, argcsr_sell_info_t* info) {
+    return guarded([&] {
+        if (!m || !info) fail(ARGCSR_E_PARAMETER, "argcsr_sell_info: null argument");
+        DeviceScope scope(m->device);
+        info->num_rows = m->num_rows;
+        info->num_cols = m->num_cols;
+        info->slice_size = m->slice_size;
+        info->num_slices = m->num_slices;
+        info->total_slots = m->total_slots;
+        std::vector<uint64_t> w(m->num_slices);
+        if (m->num_slices)
+            CUDA_OK(cudaMemcpy(w.data(), m->width, m->num_slices * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        info->width = w.empty() ? 0 : *std::max_element(w.begin(), w.end());
+        info->device_bytes = m->device_bytes;
+        info->device = m->device;
+        info->dtype = m->dtype;
+        info->ellpack = m->ellpack ? 1u : 0u;
+    });
+}
+
+argcsr_status argcsr_sell_export(const argcsr_sell* m, uint64_t* slice_widths, uint64_t* slice_offsets, void* values,
+                                 int32_t* columns) {
+    return guarded([&] {
+        if (!m) fail(ARGCSR_E_PARAMETER, "argcsr_sell_export: null handle");
+        DeviceScope scope(m->device);
+        cudaStream_t s = cudaStreamPerThread;
+        if (slice_widths && m->num_slices)
+            CUDA_OK(cudaMemcpyAsync(slice_widths, m->width, m->num_slices * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        if (slice_offsets && m->num_slices)
+            CUDA_OK(cudaMemcpyAsync(slice_offsets, m->offset, m->num_slices * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        if (values && m->total_slots)
+            CUDA_OK(cudaMemcpyAsync(values, m->values, m->total_slots * elem_size(m->dtype), cudaMemcpyDeviceToHost, s));
+        if (columns && m->total_slots)
+            CUDA_OK(cudaMemcpyAsync(columns, m->columns, m->total_slots * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    });
+}
+
+argcsr_status argcsr_sell_spmv(const argcsr_sell* m, const void* x, void* y, void* stream) {
+    return guarded([&] {
+        if (!m) fail(ARGCSR_E_PARAMETER, "argcsr_sell_spmv: null handle");
+        if ((!x && m->num_cols) || (!y && m->num_rows)) fail(ARGCSR_E_PARAMETER, "argcsr_sell_spmv: null vector");
+        DeviceScope scope(m->device);
+        argcsr_gpu::sell_spmv(m, x, y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+argcsr_status argcsr_sell_spmv_host(const argcsr_sell* m, const void* x, uint64_t x_len, void* y) {
+    return guarded([&] {
+        if (!m) fail(ARGCSR_E_PARAMETER, "argcsr_sell_spmv_host: null handle");
+        const char* who = m->ellpack ? "spmv_ellpack" : "spmv_sliced";  // ellpack.cpp:135-139, 169-173
+        if (x_len != m->num_cols)
+            fail(ARGCSR_E_DIMENSION, std::string(who) + ": vector length " + std::to_string(x_len) +
+                                         " does not match " + std::to_string(m->num_cols) + " columns");
+        DeviceScope scope(m->device);
+        cudaStream_t s = cudaStreamPerThread;
+        const size_t es = elem_size(m->dtype);
+        void *dx = nullptr, *dy = nullptr;
+        CUDA_OK(cudaMallocAsync(&dx, std::max<uint64_t>(x_len, 1) * es, s));
+        CUDA_OK(cudaMallocAsync(&dy, std::max<uint64_t>(m->num_rows, 1) * es, s));
+        if (x_len) CUDA_OK(cudaMemcpyAsync(dx, x, x_len * es, cudaMemcpyHostToDevice, s));
+        argcsr_gpu::sell_spmv(m, dx, dy, s);
+        if (m->num_rows) CUDA_OK(cudaMemcpyAsync(y, dy, m->num_rows * es, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaFreeAsync(dx, s));
+        CUDA_OK(cudaFreeAsync(dy, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    });
+}
+
+void argcsr_sell_free(argcsr_sell* m) { free_sell(m); }
 
 argcsr_status argcsr_dev_import(const argcsr_argcsr_view* v, int device, void* stream, uint32_t flags,
                                 argcsr_dev** out) {

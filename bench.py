@@ -401,7 +401,8 @@ def run_b200(args):
                    "l2": ("flushed between steps (working set < 4x L2)" if flush_buf is not None else
                           f"inputs larger than L2 (ARG-CSR arrays {m.stored_slots * (sv + 4) / 1e9:.2f} GB); "
                           "x kept L2-resident by design (access-policy window)"),
-                   "parallelism": f"rows nnz-balanced over {world} GPU(s)" if world > 1 else "single GPU"},
+                   "parallelism": (f"rows nnz-balanced over {world} GPU(s), {D.exchange} x exchange overlapped "
+                                   f"with the interior groups" if world > 1 else "single GPU")},
         "eff_GBps": round(eff_gbs, 1), "pct_of_8TBps": round(100 * eff_gbs / NOMINAL_HBM_GBS, 2),
         "pct_of_measured": round(100 * eff_gbs / peak, 2),
         "roofline": {"bound": "hbm", "achieved": round(eff_gbs, 1), "peak": peak, "unit": "GB/s",

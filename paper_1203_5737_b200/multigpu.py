@@ -151,7 +151,7 @@ class DistributedArgCsr:
     def __init__(self, num_rows: int, num_cols: int, row_pointers, columns, values, tpg: int = 128, dcs: int = 1,
                  group=None, device: Optional[torch.device] = None,
                  engine_factory: Optional[Callable[[CsrSlice], object]] = None, dtype=torch.float64,
-                 layout: str = "compact", overlap: bool = True):
+                 layout: str = "compact", overlap: bool = True, exchange: str = "auto"):
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized()
         self.world = dist.get_world_size(group) if self.distributed else 1
@@ -179,6 +179,39 @@ class DistributedArgCsr:
         if self.overlap:
             self.interior = interior_group_range(self.slice.row_pointers, self.slice.columns,
                                                  self.engine.group_first_rows(), r0, r1)
+        # x exchange between steps: the all-gather of every y slice, or only
+        # the halo -- the x entries of other ranks this rank's columns use
+        # (auto: halo when it moves < 1/4 of the all-gather's volume)
+        if exchange not in ("auto", "allgather", "halo"):
+            raise ValueError("exchange must be 'auto', 'allgather' or 'halo'")
+        self.halo = None
+        if self.overlap and exchange != "allgather":
+            self.halo = self._build_halo()
+            total = int(self.halo["recv_total"].item())
+            if exchange == "auto" and total * 4 >= self.num_rows:
+                self.halo = None
+        self.exchange = "halo" if self.halo is not None else ("allgather" if self.world > 1 else "none")
+
+    def _build_halo(self) -> dict:
+        """Halo plan: per peer, the global rows this rank needs (recv) and the
+        global rows it must send (learned with two all-to-alls)."""
+        cols = self.slice.columns
+        c = torch.as_tensor(np.asarray(cols) if isinstance(cols, np.ndarray) else cols).to(self.device, torch.int64)
+        need = torch.unique(c[(c < self.r0) | (c >= self.r1)])  # sorted
+        b = torch.as_tensor(self.bounds.astype(np.int64), device=self.device)
+        cuts = torch.searchsorted(need, b)
+        recv_counts = (cuts[1:] - cuts[:-1]).to(torch.int64)
+        dev_cc = self.device if self.device.type == "cuda" else torch.device("cpu")
+        sc = torch.empty(self.world, dtype=torch.int64, device=dev_cc)
+        dist.all_to_all_single(sc, recv_counts.to(dev_cc), group=self.group)
+        rc_l, sc_l = recv_counts.cpu().tolist(), sc.cpu().tolist()
+        send_rows = torch.empty(sum(sc_l), dtype=torch.int64, device=dev_cc)
+        dist.all_to_all_single(send_rows, need.to(dev_cc), output_split_sizes=sc_l, input_split_sizes=rc_l,
+                               group=self.group)
+        return {"recv_rows": need, "recv_counts": rc_l, "send_local": (send_rows.to(self.device) - self.r0),
+                "send_counts": sc_l, "recv_total": torch.tensor(sum(rc_l)),
+                "recv_buf": torch.empty(sum(rc_l), dtype=self.dtype, device=self.device),
+                "send_buf": torch.empty(sum(sc_l), dtype=self.dtype, device=self.device)}
 
     # ------------------------------------------------------------ collectives
     def gather(self, y_local: torch.Tensor, x_full: torch.Tensor) -> None:
@@ -211,11 +244,38 @@ class DistributedArgCsr:
             self._pending.append(dist.broadcast(x_full[off:off + n], src=src, group=self.group, async_op=True))
             off += n
 
+    def halo_async(self, x_full: torch.Tensor) -> None:
+        """Send the rows peers need from this rank's chunk x_full[r0:r1] and
+        receive this rank's halo; the scatter into x_full follows the wait."""
+        h = self.halo
+        torch.index_select(x_full[self.r0:self.r1], 0, h["send_local"], out=h["send_buf"])
+        self._pending.append(dist.all_to_all_single(h["recv_buf"], h["send_buf"],
+                                                    output_split_sizes=h["recv_counts"],
+                                                    input_split_sizes=h["send_counts"], group=self.group,
+                                                    async_op=True))
+        self._halo_target = x_full
+
+    def exchange_async(self, x_full: torch.Tensor) -> None:
+        if self.halo is not None:
+            self.halo_async(x_full)
+        else:
+            self.gather_async(x_full)
+
     def wait_gather(self) -> None:
-        """Stream-order (NCCL) or complete (gloo) the outstanding gathers."""
+        """Stream-order (NCCL) or complete (gloo) the outstanding exchange."""
         for w in self._pending:
             w.wait()
+        if self._pending and self.halo is not None:
+            self._halo_target.index_copy_(0, self.halo["recv_rows"], self.halo["recv_buf"])
         self._pending = []
+
+    def assemble(self, x_full: torch.Tensor) -> None:
+        """All-gather every rank's chunk of x_full (after a halo-only step,
+        the other ranks' rows of x_full are stale)."""
+        self.wait_gather()
+        if self.world > 1:
+            y = x_full[self.r0:self.r1].clone()
+            self.gather(y, x_full)
 
     def _spmv_overlapped(self, xin: torch.Tensor, xout: torch.Tensor, x_scale: Optional[torch.Tensor]) -> torch.Tensor:
         """Interior groups, wait for xin's gather, boundary groups; y into
@@ -245,9 +305,11 @@ class DistributedArgCsr:
             self.gather(self.y, out_full)
             return
         self._spmv_overlapped(x_full, out_full, x_scale)
-        self.gather_async(out_full)
+        self.exchange_async(out_full)
         if wait:
             self.wait_gather()
+            if self.halo is not None:
+                self.assemble(out_full)
 
     def power_iteration(self, x0: torch.Tensor, iters: int):
         """`iters` steps of x <- A x / ||A x||; returns (lambda, x) with
@@ -258,6 +320,8 @@ class DistributedArgCsr:
         for k in range(iters):
             self.step(buf[k % 2], buf[(k + 1) % 2], scale, s2)
         self.wait_gather()
+        if self.halo is not None:
+            self.assemble(buf[iters % 2])
         lam = float(torch.sqrt(s2).item())  # the only host synchronisation
         x = buf[iters % 2] * scale  # materialise the last normalisation
         return lam, x
@@ -274,7 +338,7 @@ class DistributedArgCsr:
         s2.copy_(torch.dot(y64, y64).reshape(1))
         self.allreduce_sum(s2)
         if self.overlap:
-            self.gather_async(xout)  # in flight under the next step's interior groups
+            self.exchange_async(xout)  # in flight under the next step's interior groups
         else:
             self.gather(y, xout)
         torch.reciprocal(torch.sqrt(s2), out=scale)

@@ -82,7 +82,7 @@ def _matrix(kind):
     return powerlaw_csr(3001, 3001, seed=4, heavy_rows=[(7, 2000)])
 
 
-def _worker(rank, world, port, kind, tpg, dcs, iters, out, overlap):
+def _worker(rank, world, port, kind, tpg, dcs, iters, out, overlap, exchange="auto"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, str(ROOT))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -92,7 +92,8 @@ def _worker(rank, world, port, kind, tpg, dcs, iters, out, overlap):
 
         A = _matrix(kind)
         D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values, tpg, dcs,
-                              engine_factory=lambda sl: OracleEngine(sl, tpg, dcs), overlap=overlap)
+                              engine_factory=lambda sl: OracleEngine(sl, tpg, dcs), overlap=overlap,
+                              exchange=exchange)
         # the slice's conversion equals the reference conversion of the slice
         sl = D.slice
         want = oracle.orc().argcsr_from_csr(D.engine.csr, tpg, dcs)
@@ -104,20 +105,22 @@ def _worker(rank, world, port, kind, tpg, dcs, iters, out, overlap):
         lam, x = D.power_iteration(x0, iters)
         res = dict(rank=rank, bounds=D.bounds.tolist(), counts=D.counts, r0=sl.row_begin, r1=sl.row_end,
                    y1=out_full.numpy().copy(), lam=lam, x=x.numpy().copy(), interior=D.interior,
-                   groups=D.engine.num_groups)
+                   groups=D.engine.num_groups, exchange=D.exchange)
         torch.save(res, out / f"rank{rank}.pt")
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,tpg,dcs,overlap", [("stencil", 128, 1, True), ("stencil8", 128, 32, True),
-                                                  ("powerlaw", 32, 4, True), ("stencil", 128, 1, False)])
-def test_two_rank_power_iteration_gloo(tmp_path, kind, tpg, dcs, overlap):
+@pytest.mark.parametrize("kind,tpg,dcs,overlap,exchange", [
+    ("stencil", 128, 1, True, "auto"), ("stencil8", 128, 32, True, "allgather"), ("stencil8", 128, 1, True, "halo"),
+    ("powerlaw", 32, 4, True, "auto"), ("powerlaw", 32, 4, True, "halo"), ("stencil", 128, 1, False, "auto")])
+def test_two_rank_power_iteration_gloo(tmp_path, kind, tpg, dcs, overlap, exchange):
     import oracle
 
     port = 29500 + (os.getpid() % 1000)
     iters = 12
-    mp.start_processes(_worker, args=(2, port, kind, tpg, dcs, iters, tmp_path, overlap), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, port, kind, tpg, dcs, iters, tmp_path, overlap, exchange), nprocs=2,
+                       join=True,
                        start_method="spawn")
     res = [torch.load(tmp_path / f"rank{r}.pt", weights_only=False) for r in range(2)]
     A = _matrix(kind)
@@ -136,6 +139,10 @@ def test_two_rank_power_iteration_gloo(tmp_path, kind, tpg, dcs, overlap):
     for r in res:
         assert np.all(np.abs(r["y1"] - y_full) <= 1e-12 * absrow)
         assert np.array_equal(r["y1"], res[0]["y1"])  # every rank holds the same gathered y
+    if exchange == "halo" or (overlap and exchange == "auto" and kind.startswith("stencil")):
+        assert all(r["exchange"] == "halo" for r in res)
+    if not overlap or exchange == "allgather":
+        assert all(r["exchange"] == "allgather" for r in res)
     if overlap and kind.startswith("stencil"):
         for r in res:  # a stencil slice: interior groups between its boundary layers (none at the matrix ends)
             ga, gb = r["interior"]

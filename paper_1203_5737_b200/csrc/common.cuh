@@ -100,6 +100,8 @@ struct argcsr_dev {
     uint32_t num_tiles = 0, num_heavy = 0, heavy_ctas = 0;
     uint64_t heavy_max_lanes = 0;         // lanes of the fullest heavy CTA
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
+    uint32_t max_tile_rows = 0;
+    uint64_t total_units = 0;             // light units (+1 per heavy group) of the schedule           // rows of the largest light tile (heavy groups' rows included)
     uint64_t tile_span = 0;               // units between consecutive tile keys
     uint32_t tile_threads = 256;          // tiles were built for this CTA size
     uint64_t max_tile_units = 0;          // tile_span + ceil(tpg / V) - 1

@@ -366,14 +366,21 @@ __global__ void k4_tiles(const uint64_t* __restrict__ unit_base, uint32_t G, uin
     }
 }
 
+// Largest tile: groups (out[0]) and rows (out[1]).
 __global__ void k4_max_tile_groups(const uint32_t* __restrict__ tiles, uint32_t ntiles,
-                                   unsigned long long* __restrict__ out) {
-    uint64_t m = 0;
+                                   const GroupDesc* __restrict__ desc, unsigned long long* __restrict__ out) {
+    uint64_t m = 0, mr = 0;
     for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < ntiles;
-         k += uint64_t(gridDim.x) * blockDim.x)
+         k += uint64_t(gridDim.x) * blockDim.x) {
         m = max(m, uint64_t(tiles[k + 1] - tiles[k]));
+        mr = max(mr, uint64_t(desc[tiles[k + 1]].first_row - desc[tiles[k]].first_row));
+    }
     m = warp_max_u64(m);
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+    mr = warp_max_u64(mr);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, (unsigned long long)m);
+        atomicMax(out + 1, (unsigned long long)mr);
+    }
 }
 
 __global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, unsigned long long* __restrict__ out) {
@@ -725,6 +732,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     const uint64_t span = maxu <= tt / 2 ? tt - maxu + 1 : tt;
     m->tile_span = span;
     m->tile_threads = uint32_t(tt);
+    m->total_units = total_units;
     const uint64_t ntiles = (total_units + span - 1) / span;
     if (ntiles > 0x7fffffffull) fail(ARGCSR_E_UNSUPPORTED, "argcsr_from_csr: matrix too large for the tile schedule");
     m->num_tiles = uint32_t(ntiles);
@@ -732,16 +740,17 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     k4_tiles<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(m->unit_base, G, uint32_t(ntiles), span, m->tiles);
     LAUNCH_OK("k4_tiles");
     {
-        DevPtr<unsigned long long> mx(1, s);
-        CUDA_OK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), s));
+        DevPtr<unsigned long long> mx(2, s);
+        CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
         if (ntiles) {
-            k4_max_tile_groups<<<grid_for(ntiles, 256), 256, 0, s>>>(m->tiles, uint32_t(ntiles), mx.p);
+            k4_max_tile_groups<<<grid_for(ntiles, 256), 256, 0, s>>>(m->tiles, uint32_t(ntiles), m->groups, mx.p);
             LAUNCH_OK("k4_max_tile_groups");
         }
-        unsigned long long mg = 0;
-        CUDA_OK(cudaMemcpyAsync(&mg, mx.p, sizeof mg, cudaMemcpyDeviceToHost, s));
+        unsigned long long mg[2] = {0, 0};
+        CUDA_OK(cudaMemcpyAsync(mg, mx.p, sizeof mg, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
-        m->max_tile_groups = uint32_t(mg);
+        m->max_tile_groups = uint32_t(mg[0]);
+        m->max_tile_rows = uint32_t(mg[1]);
         m->max_tile_units = span + maxu - 1;
     }
 

@@ -51,6 +51,7 @@ struct SpmvArgs {
     uint32_t heavy_ctas;
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
     uint32_t max_tile_groups;
+    uint32_t max_tile_rows;
     uint32_t max_tile_units;
     const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
@@ -319,7 +320,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvA
 }
 
 // Light tile kt: consecutive short-chunk groups, V-lane units, one unit per thread.
-template <typename T, int V, int U, bool PRED, int MINB>
+// MAP: every unit and row of the tile gets its group index in shared memory
+// while the metadata loads (one thread per group, so only for small groups);
+// otherwise both phases binary-search the tile's group table.
+template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -333,30 +337,40 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     const uint32_t ng = ge - gs;
     const uint32_t cap = a.max_tile_groups;
     // smem: s_part[max_tile_units * V] | s_off[cap] | s_ub[cap+1] | s_first[cap+1] | s_chunk[cap]
+    //       | s_ugrp[max_tile_units] | s_rgrp[max_tile_rows]  (unit / row -> group in tile)
     uint64_t* s_off = reinterpret_cast<uint64_t*>(s_part + size_t(a.max_tile_units) * V);
     uint32_t* s_ub = reinterpret_cast<uint32_t*>(s_off + cap);
     uint32_t* s_first = s_ub + cap + 1;
     uint32_t* s_chunk = s_first + cap + 1;
+    uint16_t* s_ugrp = reinterpret_cast<uint16_t*>(s_chunk + cap);
+    uint16_t* s_rgrp = s_ugrp + a.max_tile_units;
 
     const uint64_t ub0 = a.unit_base[gs];
+    const uint32_t row0 = MAP ? a.groups[gs].first_row : 0u;
     for (uint32_t i = threadIdx.x; i <= ng; i += blockDim.x) {
         const GroupDesc d = a.groups[gs + i];
+        const uint32_t ub = uint32_t(a.unit_base[gs + i] - ub0);
         s_first[i] = d.first_row;
-        s_ub[i] = uint32_t(a.unit_base[gs + i] - ub0);
+        s_ub[i] = ub;
         if (i < ng) {
             s_off[i] = d.off_stride;
             s_chunk[i] = d.chunk;
+            if constexpr (MAP) {
+                const uint32_t ue = uint32_t(a.unit_base[gs + i + 1] - ub0), re = a.groups[gs + i + 1].first_row;
+                for (uint32_t u = ub; u < ue; ++u) s_ugrp[u] = uint16_t(i);
+                for (uint32_t r = d.first_row; r < re; ++r) s_rgrp[r - row0] = uint16_t(i);
+            }
         }
     }
     __syncthreads();
 
     // Phase-2 metadata of this thread's first row, fetched under phase 1.
-    const uint32_t row0 = s_first[0], row_end = s_first[ng];
-    const uint32_t pr = row0 + threadIdx.x;
+    const uint32_t row_end = s_first[ng];
+    const uint32_t pr = (MAP ? row0 : s_first[0]) + threadIdx.x;
     uint32_t pgi = 0, pb = 0, pe = 0;
     bool pvalid = false;
     if (pr < row_end) {
-        pgi = find_le(s_first, ng, pr);
+        pgi = MAP ? s_rgrp[pr - row0] : find_le(s_first, ng, pr);
         const uint32_t g = gs + pgi;
         pvalid = !(s_off[pgi] & kHeavyBit) && g >= a.g_begin && g < a.g_end;
         if (pvalid) {
@@ -367,7 +381,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
 
     const uint32_t nunits = s_ub[ng];
     for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) {
-        const uint32_t gi = find_le(s_ub, ng, u);
+        const uint32_t gi = MAP ? s_ugrp[u] : find_le(s_ub, ng, u);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         double s[V];
@@ -381,7 +395,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
 
     if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
     for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
-        const uint32_t gi = find_le(s_first, ng, r);
+        const uint32_t gi = MAP ? s_rgrp[r - row0] : find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
@@ -551,9 +565,10 @@ template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
 void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s);
 
 
-size_t light_smem_bytes(const argcsr_dev* m, int V) {
+size_t light_smem_bytes(const argcsr_dev* m, int V, bool map = false) {
     const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
-    return size_t(m->max_tile_units) * V * sizeof(double) + cap * sizeof(uint64_t) + (cap + 1) * 4 * 2 + cap * 4;
+    return size_t(m->max_tile_units) * V * sizeof(double) + cap * sizeof(uint64_t) + (cap + 1) * 4 * 2 + cap * 4 +
+           (map ? (size_t(m->max_tile_units) + m->max_tile_rows) * sizeof(uint16_t) : 0);
 }
 
 bool l2_window_enabled() {
@@ -615,7 +630,13 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
 
 template <typename T, int V, int U, bool PRED, int MINB>
 void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    launch(spmv_light_kernel<T, V, U, PRED, MINB>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
+    // small groups (units + rows per group, on average): fill the maps, else search
+    const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
+    const char* e = std::getenv("ARGCSR_MAP");  // experiments: force 1 / 0
+    if (e ? e[0] == '1' : per_group <= 24.0)
+        launch(spmv_light_kernel<T, V, U, PRED, MINB, true>, m->num_tiles, light_smem_bytes(m, V, true), m, a, s);
+    else
+        launch(spmv_light_kernel<T, V, U, PRED, MINB, false>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
 }
 
 template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
@@ -708,6 +729,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.g_begin = gb;
     a.g_end = ge;
     a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
+    a.max_tile_rows = m->max_tile_rows;
     a.max_tile_units = uint32_t(m->max_tile_units);
     a.x_evict_last = env_flag("ARGCSR_XPOL", 1);
     a.stream_evict_first = env_flag("ARGCSR_SPOL", m->num_heavy > 0 ? 1 : 0);

@@ -12,7 +12,7 @@ for cfg in ${CONFIGS:-C2:1 C2:32 C3:1 C4:1}; do
       # pol "d" = the library defaults; "x<0|1>s<0|1>" forces the x / stream L2 policies
       if [ "$pol" = d ]; then unset ARGCSR_XPOL ARGCSR_SPOL; else export ARGCSR_XPOL=${pol:1:1} ARGCSR_SPOL=${pol:3:1}; fi
       # variant "K=V,K2=V2" = the default kernel with those environment settings
-      unset ARGCSR_TILE_THREADS ARGCSR_SPMV_VARIANT
+      for v_ in $(env | grep -o '^ARGCSR_[A-Z_0-9]*' | grep -v -e ARGCSR_XPOL -e ARGCSR_SPOL); do unset $v_; done
       vv=$v
       case $v in *=*) for kv in ${v//,/ }; do export "$kv"; done; vv=${ARGCSR_SPMV_VARIANT:-default};; esac
       r=$(ARGCSR_SPMV_VARIANT=$vv timeout 300 python bench.py --config $c --dcs $d --layout $lay --steps ${STEPS:-50} --warmup 5 --no-variants --no-cpu-baseline 2>/dev/null)

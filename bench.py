@@ -432,7 +432,9 @@ def run_b200(args):
         out["e2e"] = {"value": round(2.0 * nnz_total / e2e_s / 1e9, 3), "unit": "GFLOP/s",
                       "h2d_bytes_per_step": A.num_cols * sv, "d2h_bytes_per_step": A.num_rows * sv,
                       "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
-                      "path": "argcsr_dev_spmv_host_staged (pinned host x -> H2D -> SpMV -> D2H y -> sync)"}
+                      "path": "argcsr_dev_spmv_host_staged: pinned host x -> H2D in 8 pieces (copy engine 1) -> "
+                              "light-tile chunks launched as their x window lands -> D2H of y chunks (copy "
+                              "engine 2) -> sync; one-shot when the matrix has heavy groups or the x remap"}
         out["gpu_launches"] = launches
 
         if not args.no_variants:

@@ -80,6 +80,12 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->perm);
     cudaFree(m->xbuf);
     if (m->aux) cudaStreamDestroy(m->aux);
+    if (m->h2d) cudaStreamDestroy(m->h2d);
+    if (m->d2h) cudaStreamDestroy(m->d2h);
+    for (int i = 0; i < 8; ++i) {
+        if (m->ev_x[i]) cudaEventDestroy(m->ev_x[i]);
+        if (m->ev_c[i]) cudaEventDestroy(m->ev_c[i]);
+    }
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (prev >= 0) cudaSetDevice(prev);
@@ -136,6 +142,12 @@ argcsr_dev* new_handle(int device, argcsr_dtype dtype, uint64_t rows, uint64_t c
         CUDA_OK(cudaMemset(m->sched, 0, 2 * sizeof(uint32_t)));
         CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+        CUDA_OK(cudaStreamCreateWithFlags(&m->h2d, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&m->d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 8; ++i) {
+            CUDA_OK(cudaEventCreateWithFlags(&m->ev_x[i], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&m->ev_c[i], cudaEventDisableTiming));
+        }
     } catch (...) {
         free_handle(m);
         throw;
@@ -430,9 +442,46 @@ argcsr_status argcsr_dev_spmv_host_staged(const argcsr_dev* m, const void* x_hos
         DeviceScope scope(m->device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t es = elem_size(m->dtype);
-        CUDA_OK(cudaMemcpyAsync(x_dev, x_host, m->num_cols * es, cudaMemcpyHostToDevice, s));
-        argcsr_gpu::spmv_launch(m, x_dev, y_dev, 0, m->num_groups, s);
-        CUDA_OK(cudaMemcpyAsync(y_host, y_dev, m->num_rows * es, cudaMemcpyDeviceToHost, s));
+        if (m->tile_cmax.empty() || m->lanes_per_unit != 4 || m->num_cols == 0) {
+            CUDA_OK(cudaMemcpyAsync(x_dev, x_host, m->num_cols * es, cudaMemcpyHostToDevice, s));
+            argcsr_gpu::spmv_launch(m, x_dev, y_dev, 0, m->num_groups, s);
+            CUDA_OK(cudaMemcpyAsync(y_host, y_dev, m->num_rows * es, cudaMemcpyDeviceToHost, s));
+            CUDA_OK(cudaStreamSynchronize(s));
+            return;
+        }
+        // Pipelined: x goes up in 8 pieces on one copy engine, y comes down in
+        // 8 row chunks on the other (PCIe is full duplex), and each chunk of
+        // light tiles starts as soon as x is resident up to the largest
+        // column it reads (banded matrices: long before all of x arrives).
+        constexpr int K = 8;
+        const uint64_t C = m->num_cols, N = m->num_rows;
+        const uint32_t nt = m->num_tiles;
+        CUDA_OK(cudaEventRecord(m->ev_fork, s));  // order after the caller's prior work on s
+        CUDA_OK(cudaStreamWaitEvent(m->h2d, m->ev_fork, 0));
+        CUDA_OK(cudaStreamWaitEvent(m->d2h, m->ev_fork, 0));
+        for (int j = 0; j < K; ++j) {
+            const uint64_t c0 = C * j / K, c1 = C * (j + 1) / K;
+            if (c1 > c0)
+                CUDA_OK(cudaMemcpyAsync(static_cast<char*>(x_dev) + c0 * es, static_cast<const char*>(x_host) + c0 * es,
+                                        (c1 - c0) * es, cudaMemcpyHostToDevice, m->h2d));
+            CUDA_OK(cudaEventRecord(m->ev_x[j], m->h2d));
+        }
+        for (int k = 0; k < K; ++k) {
+            const uint32_t t0 = uint32_t(uint64_t(nt) * k / K), t1 = uint32_t(uint64_t(nt) * (k + 1) / K);
+            if (t1 > t0) {
+                const uint64_t reach = m->tile_cmax[t1 - 1];  // columns 0..reach are read by tiles < t1
+                const int j = int(std::min<uint64_t>(K - 1, ((reach + 1) * K + C - 1) / C - 1));
+                CUDA_OK(cudaStreamWaitEvent(s, m->ev_x[std::max(j, 0)], 0));
+                argcsr_gpu::spmv_launch_tiles(m, x_dev, y_dev, t0, t1, s);
+            }
+            CUDA_OK(cudaEventRecord(m->ev_c[k], s));
+            CUDA_OK(cudaStreamWaitEvent(m->d2h, m->ev_c[k], 0));
+            const uint64_t r0 = t0 < nt ? m->tile_row[t0] : N, r1 = m->tile_row[t1];
+            if (r1 > r0)
+                CUDA_OK(cudaMemcpyAsync(static_cast<char*>(y_host) + r0 * es, static_cast<const char*>(y_dev) + r0 * es,
+                                        (r1 - r0) * es, cudaMemcpyDeviceToHost, m->d2h));
+        }
+        CUDA_OK(cudaStreamSynchronize(m->d2h));
         CUDA_OK(cudaStreamSynchronize(s));
     });
 }

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "argcsr_gpu.h"
 
@@ -101,7 +102,12 @@ struct argcsr_dev {
     uint64_t heavy_max_lanes = 0;         // lanes of the fullest heavy CTA
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
     uint32_t max_tile_rows = 0;
-    uint64_t total_units = 0;             // light units (+1 per heavy group) of the schedule           // rows of the largest light tile (heavy groups' rows included)
+    uint64_t total_units = 0;             // light units (+1 per heavy group) of the schedule
+    // pipelined host path (argcsr_dev_spmv_host_staged): per light tile, the
+    // largest stored column used by tiles 0..t (running max) and its first row
+    std::vector<uint32_t> tile_cmax, tile_row;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_x[8] = {}, ev_c[8] = {};           // rows of the largest light tile (heavy groups' rows included)
     uint64_t tile_span = 0;               // units between consecutive tile keys
     uint32_t tile_threads = 256;          // tiles were built for this CTA size
     uint64_t max_tile_units = 0;          // tile_span + ceil(tpg / V) - 1

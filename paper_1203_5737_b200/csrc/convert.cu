@@ -392,6 +392,29 @@ __global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, uns
     if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
 }
 
+// Largest column each light tile reads (padding -1 ignored): for the
+// pipelined host path, a tile may start once x is copied up to it.
+__global__ void k_tile_cmax(const uint32_t* __restrict__ tiles, uint32_t ntiles, const GroupDesc* __restrict__ desc,
+                            const int32_t* __restrict__ cols, uint32_t* __restrict__ cmax,
+                            uint32_t* __restrict__ first_row) {
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t b = desc[tiles[t]].offset(), e = desc[tiles[t + 1]].offset();
+        int32_t mx = 0;
+        for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) mx = max(mx, cols[i]);
+        mx = int32_t(warp_max_u64(uint64_t(uint32_t(mx))));
+        __shared__ int32_t s_mx[32];
+        if ((threadIdx.x & 31) == 0) s_mx[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int32_t m = 0;
+            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) m = max(m, s_mx[w]);
+            cmax[t] = uint32_t(m);
+            first_row[t] = desc[tiles[t]].first_row;
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------- K5
 // Gather form of layout_group: lane l of group g belongs to the row whose
 // threads_mapping range holds l; its chunk c holds the row's elements
@@ -796,6 +819,20 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
     }
     CUDA_OK(cudaStreamSynchronize(s));
+    // pipelined host path: tile column reach (light tiles only; no heavy groups, no remap)
+    if (m->num_heavy == 0 && !m->x_remap && m->num_tiles >= 16) {
+        const uint32_t nt = m->num_tiles;
+        DevPtr<uint32_t> cm(nt, s), fr(nt, s);
+        k_tile_cmax<<<std::min<uint32_t>(nt, 148u * 16u), 256, 0, s>>>(m->tiles, nt, m->groups, m->columns, cm.p, fr.p);
+        LAUNCH_OK("k_tile_cmax");
+        m->tile_cmax.resize(nt);
+        m->tile_row.resize(nt + 1);
+        CUDA_OK(cudaMemcpyAsync(m->tile_cmax.data(), cm.p, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaMemcpyAsync(m->tile_row.data(), fr.p, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        for (uint32_t t = 1; t < nt; ++t) m->tile_cmax[t] = std::max(m->tile_cmax[t], m->tile_cmax[t - 1]);
+        m->tile_row[nt] = uint32_t(N);
+    }
 }
 
 }  // namespace

@@ -52,6 +52,7 @@ struct SpmvArgs {
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
     uint32_t max_tile_groups;
     uint32_t max_tile_rows;
+    uint32_t tile0;  // light tiles [tile0, tile0 + gridDim.x) of this launch (spmv_launch_tiles)
     uint32_t max_tile_units;
     const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
     const double xs = a.x_scale ? *a.x_scale : 1.0;
 
-    const uint32_t kt = blockIdx.x;
+    const uint32_t kt = a.tile0 + blockIdx.x;
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
     if (ge <= a.g_begin || gs >= a.g_end || gs == ge) return;
     const uint32_t ng = ge - gs;
@@ -730,6 +731,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.g_end = ge;
     a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
     a.max_tile_rows = m->max_tile_rows;
+    a.tile0 = 0;
     a.max_tile_units = uint32_t(m->max_tile_units);
     a.x_evict_last = env_flag("ARGCSR_XPOL", 1);
     a.stream_evict_first = env_flag("ARGCSR_SPOL", m->num_heavy > 0 ? 1 : 0);
@@ -771,7 +773,48 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     }
 }
 
+// Light tiles [t0, t1) only, default kernel (the pipelined host path; the
+// handle has no heavy groups and no x remap).
+template <typename T>
+void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0, uint32_t t1, cudaStream_t s) {
+    SpmvArgs<T> a{};
+    a.vals = static_cast<const T*>(m->values);
+    a.cols = m->columns;
+    a.groups = m->groups;
+    a.tm = static_cast<const uint16_t*>(m->tm);
+    a.assigned = static_cast<const uint16_t*>(m->assigned);
+    a.unit_base = m->unit_base;
+    a.tiles = m->tiles;
+    a.heavy = m->heavy;
+    a.heavy_ptr = m->heavy_ptr;
+    a.x = static_cast<const T*>(x);
+    a.y = static_cast<T*>(y);
+    a.heavy_ctas = 0;
+    a.g_begin = 0;
+    a.g_end = uint32_t(m->num_groups);
+    a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
+    a.max_tile_rows = m->max_tile_rows;
+    a.max_tile_units = uint32_t(m->max_tile_units);
+    a.x_scale = nullptr;
+    a.x_evict_last = 1;
+    a.stream_evict_first = 0;
+    a.tile0 = t0;
+    const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
+    const unsigned grid = t1 - t0;
+    if (m->lanes_per_unit != 4) fail(ARGCSR_E_INTERNAL, "spmv_launch_tiles: V = 4 handles only");
+    if (per_group <= 24.0)
+        launch(spmv_light_kernel<T, 4, 4, false, 5, true>, grid, light_smem_bytes(m, 4, true), m, a, s);
+    else
+        launch(spmv_light_kernel<T, 4, 4, false, 5, false>, grid, light_smem_bytes(m, 4), m, a, s);
+}
+
 }  // namespace
+
+void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0, uint32_t t1, cudaStream_t s) {
+    if (t1 <= t0) return;
+    if (m->dtype == ARGCSR_F64) launch_tiles_dtype<double>(m, x, y, t0, t1, s);
+    else launch_tiles_dtype<float>(m, x, y, t0, t1, s);
+}
 
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
                  cudaStream_t s, const double* x_scale, bool reuse_x) {

@@ -15,4 +15,8 @@ namespace argcsr_gpu {
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
                  cudaStream_t s, const double* x_scale = nullptr, bool reuse_x = false);
 
+// Light tiles [t0, t1) only (handles without heavy groups or x remap): the
+// pipelined host path launches the tiles whose x window has arrived.
+void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0, uint32_t t1, cudaStream_t s);
+
 }  // namespace argcsr_gpu

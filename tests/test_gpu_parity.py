@@ -368,3 +368,23 @@ def test_dense_rows_vector_x_runs(argcsr, orc, dtype, layout):
         assert bits(y) == bits(y_ref)
     else:
         assert np.array_equal(y, y_ref.astype(np.float32))
+
+
+@pytest.mark.parametrize("kind", ["stencil", "powerlaw"])
+def test_host_staged_pipeline(argcsr, orc, kind):
+    """argcsr_dev_spmv_host_staged (the e2e path): x up in pieces, tiles as
+    soon as their columns have arrived, y down in chunks (banded matrices);
+    one-shot otherwise.  Bit-identical to the reference either way."""
+    import torch
+
+    A = stencil27(30) if kind == "stencil" else powerlaw_csr(30000, 30000, seed=12, heavy_rows=[(5, 9000)])
+    dev = to_dev(argcsr, A, 128, 1)
+    x = np.sin(np.arange(A.num_cols, dtype=np.float64))
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty(A.num_rows, dtype=torch.float64).pin_memory()
+    xd = torch.empty(A.num_cols, dtype=torch.float64, device="cuda")
+    yd = torch.empty(A.num_rows, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    for _ in range(2):
+        dev.spmv_host_staged(xh.data_ptr(), xd.data_ptr(), yd.data_ptr(), yh.data_ptr(), s.cuda_stream)
+        assert bits(yh.numpy()) == bits(orc.spmv_argcsr(orc.argcsr_from_csr(A, 128, 1), x))

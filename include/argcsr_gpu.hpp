@@ -240,4 +240,43 @@ inline FormatStats padding_stats(const DeviceArgCsr& M) {
     return {s.explicit_nnz, s.assigned_padded_slots, s.total_allocated_slots, s.padding_ratio, s.estimated_bytes};
 }
 
+// io.hpp:37-43 — the reference's binary container, byte-identical.
+inline void write_binary_file(const std::string& path, const DeviceArgCsr& M) {
+    check(argcsr_dev_write_binary(M.handle(), path.c_str()));
+}
+
+// An ARG-CSR container is imported as stored (a cached conversion); a CSR
+// container is converted with threads_per_group / desired_chunk_size.
+inline DeviceArgCsr read_binary_file(const std::string& path, std::size_t threads_per_group = kDefaultThreadsPerGroup,
+                                     std::size_t desired_chunk_size = kDefaultDesiredChunkSize, int device = 0) {
+    argcsr_dev* h = nullptr;
+    check(argcsr_dev_read_binary(path.c_str(), threads_per_group, desired_chunk_size, device, nullptr, 0u, &h));
+    return DeviceArgCsr(h);
+}
+
+// A device handle from a host ArgCsrMatrix without re-running the converter.
+inline DeviceArgCsr device_from_host(const ArgCsrMatrix& M, int device = 0) {
+    std::vector<uint64_t> g4(4 * M.groups.size());
+    for (std::size_t g = 0; g < M.groups.size(); ++g) {
+        g4[4 * g] = M.groups[g].first_row;
+        g4[4 * g + 1] = M.groups[g].size;
+        g4[4 * g + 2] = M.groups[g].offset;
+        g4[4 * g + 3] = M.groups[g].chunk_size;
+    }
+    argcsr_argcsr_view v{};
+    v.num_rows = M.num_rows;
+    v.num_cols = M.num_cols;
+    v.threads_per_group = M.threads_per_group;
+    v.num_groups = M.groups.size();
+    v.groups4 = g4.data();
+    v.threads_mapping = reinterpret_cast<const uint64_t*>(M.threads_mapping.data());
+    v.values = M.values.data();
+    v.columns = M.columns.data();
+    v.total_slots = M.values.size();
+    v.dtype = ARGCSR_F64;
+    argcsr_dev* h = nullptr;
+    check(argcsr_dev_import(&v, device, nullptr, 0u, &h));
+    return DeviceArgCsr(h);
+}
+
 }  // namespace argcsr_b200

@@ -124,3 +124,39 @@ def test_partition_rows_nnz_balanced(argcsr):
         assert b[0] == 0 and b[-1] == 9 and np.all(np.diff(b.astype(np.int64)) >= 1)
     b = argcsr.partition_rows(rp, 2)
     assert b[1] == np.searchsorted(rp, 50)
+
+
+def _build_example(tmp_path):
+    import subprocess
+
+    root = Path(__file__).resolve().parent.parent
+    exe = tmp_path / "spmv_example"
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{root / 'include'}", str(root / "examples" / "spmv_example.cpp"),
+           f"-L{root / 'paper_1203_5737_b200'}", "-largcsr_gpu", f"-Wl,-rpath,{root / 'paper_1203_5737_b200'}",
+           "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_cpp_example_builds_and_fails_loudly_without_a_device(tmp_path):
+    """include/argcsr_gpu.hpp is a usable C++ API over the C-ABI library; with
+    no CUDA device the product path raises (no CPU fallback)."""
+    import subprocess
+
+    import torch
+
+    exe = _build_example(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("a device is present (tests/test_gpu_parity.py runs the example)")
+    r = subprocess.run([str(exe), "16"], capture_output=True, text=True)
+    assert r.returncode == 2 and "no CUDA device" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_example_runs_on_the_device(tmp_path):
+    import subprocess
+
+    exe = _build_example(tmp_path)
+    r = subprocess.run([str(exe), "300", str(tmp_path / "a.spfmt")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "lossless=1" in r.stdout

@@ -45,6 +45,8 @@ def parse_args():
     p.add_argument("--dcs", type=int, default=1)
     p.add_argument("--layout", default="compact", choices=["compact", "reference"],
                    help="device storage of the value/column blocks (include/argcsr_gpu.h ARGCSR_LAYOUT_REFERENCE)")
+    p.add_argument("--x-remap", default="auto", choices=["auto", "on", "off"],
+                   help="device column order (single-GPU path): library decision, or forced")
     p.add_argument("--no-variants", action="store_true", help="skip the tuned-dcs and cuSPARSE side runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-steps", type=int, default=20)
@@ -279,7 +281,7 @@ def run_b200(args):
             S = A
             m = argcsr.argcsr_from_torch(A.num_rows, A.num_cols, A.row_pointers.contiguous(), A.columns.contiguous(),
                                          A.values.to(tdtype).contiguous(), args.tpg, args.dcs, stream=stream,
-                                         layout=args.layout)
+                                         layout=args.layout, x_remap=args.x_remap)
         ce1.record(stream)
     torch.cuda.synchronize()
     conv_ms = ce0.elapsed_time(ce1)
@@ -385,7 +387,7 @@ def run_b200(args):
 
     peak, peak_src = measured_peak()
     info = {"layout": m.layout, "groups": m.num_groups, "total_slots": m.total_slots,
-            "stored_slots": m.stored_slots, "x_remap": m.x_remap, "x_used_columns": m.x_used_columns,
+            "stored_slots": m.stored_slots, "x_remap": m.x_remap, "x_used_columns": m.x_used_columns, "unit_len_bytes": m.unit_len_bytes,
             "heavy_groups": m.heavy_groups,
             "light_tiles": m.light_tiles, "max_chunk": m.max_chunk_size, "device_bytes": m.device_bytes,
             "heavy_ctas": m.heavy_ctas, "l2_persist_bytes": m.l2_persist_bytes}

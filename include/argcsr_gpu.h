@@ -100,6 +100,7 @@ typedef struct {
     uint32_t layout;           /* 0 = lane-compact (default), ARGCSR_LAYOUT_REFERENCE */
     uint32_t x_remap;          /* 1: stored columns index x' = x[perm] (see ARGCSR_XREMAP_ON) */
     uint64_t x_used_columns;   /* columns with an entry (x_remap) or num_cols */
+    uint64_t unit_len_bytes;   /* per-unit step counts the SpMV stops at (0: not kept, reads to chunk_size) */
 } argcsr_dev_info_t;
 
 /* Device layout of the value/column blocks (argcsr_dev_convert_ex flags).

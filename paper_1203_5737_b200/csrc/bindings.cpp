@@ -413,6 +413,7 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         .def_property_readonly("stored_slots", [](const PyArgCsr& p) { return p.info().stored_slots; })
         .def_property_readonly("x_remap", [](const PyArgCsr& p) { return p.info().x_remap != 0; })
         .def_property_readonly("x_used_columns", [](const PyArgCsr& p) { return p.info().x_used_columns; })
+        .def_property_readonly("unit_len_bytes", [](const PyArgCsr& p) { return p.info().unit_len_bytes; })
         .def_property_readonly("layout", [](const PyArgCsr& p) {
             return p.info().layout == ARGCSR_LAYOUT_REFERENCE ? "reference" : "compact";
         })

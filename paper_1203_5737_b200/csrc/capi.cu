@@ -74,6 +74,7 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->assigned);
     cudaFree(m->unit_base);
     cudaFree(m->tiles);
+    cudaFree(m->ulen);
     cudaFree(m->heavy);
     cudaFree(m->heavy_ptr);
     cudaFree(m->sched);
@@ -341,6 +342,7 @@ argcsr_status argcsr_dev_info(const argcsr_dev* m, argcsr_dev_info_t* info) {
         info->layout = m->layout == argcsr_gpu::kLayoutReference ? ARGCSR_LAYOUT_REFERENCE : 0u;
         info->x_remap = m->x_remap ? 1u : 0u;
         info->x_used_columns = m->n_used;
+        info->unit_len_bytes = m->ulen ? m->total_units : 0;
         info->nnz = m->nnz;
         info->heavy_groups = m->num_heavy;
         info->heavy_ctas = m->heavy_ctas;

@@ -103,6 +103,8 @@ struct argcsr_dev {
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
     uint32_t max_tile_rows = 0;
     uint64_t total_units = 0;             // light units (+1 per heavy group) of the schedule
+    uint8_t* ulen = nullptr;              // [total_units] light unit lengths (steps with an entry), or null
+    uint64_t unit_len_saved = 0;          // stream bytes per SpMV the lengths save (measured at conversion)
     // pipelined host path (argcsr_dev_spmv_host_staged): per light tile, the
     // largest stored column used by tiles 0..t (running max) and its first row
     std::vector<uint32_t> tile_cmax, tile_row;

@@ -415,6 +415,45 @@ __global__ void k_tile_cmax(const uint32_t* __restrict__ tiles, uint32_t ntiles,
     }
 }
 
+// Per light unit (V adjacent lanes of a group), the number of element steps
+// holding an entry: 1 + the last step with a non-sentinel column in any of its
+// lanes (sentinels trail per lane).  One warp per group, lanes over units,
+// scanning down from the last step.  Also sums, over the light units, the
+// slots the SpMV reads with and without the lengths (stop at the length vs.
+// at the first U-step batch ending in an all-sentinel step), so the converter
+// keeps the lengths only when they save more traffic than they cost.
+__global__ void k6_unit_len(const GroupDesc* __restrict__ desc, const uint64_t* __restrict__ unit_base, uint32_t G,
+                            uint32_t V, uint32_t U, const int32_t* __restrict__ cols, uint8_t* __restrict__ ulen,
+                            unsigned long long* __restrict__ reads) {
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long with_len = 0, without = 0;
+    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < G;
+         g += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const GroupDesc d = desc[g];
+        if (d.heavy()) continue;
+        const uint64_t ub = unit_base[g], ue = unit_base[g + 1];
+        const uint64_t stride = d.stride();
+        for (uint64_t u = ub + lane; u < ue; u += 32) {
+            const uint64_t slot0 = d.offset() + (u - ub) * V;
+            uint32_t len = d.chunk;
+            for (; len > 0; --len) {
+                bool any = false;
+                for (uint32_t l = 0; l < V; ++l) any |= cols[slot0 + uint64_t(len - 1) * stride + l] != -1;
+                if (any) break;
+            }
+            ulen[u] = uint8_t(len);
+            with_len += uint64_t(len) * V;
+            without += uint64_t(min(d.chunk, U * (len / U + 1))) * V;
+        }
+    }
+    with_len = warp_sum_u64(with_len);
+    without = warp_sum_u64(without);
+    if (lane == 0) {
+        atomicAdd(reads, with_len);
+        atomicAdd(reads + 1, without);
+    }
+}
+
 // ------------------------------------------------------------------- K5
 // Gather form of layout_group: lane l of group g belongs to the row whose
 // threads_mapping range holds l; its chunk c holds the row's elements
@@ -819,6 +858,28 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
     }
     CUDA_OK(cudaStreamSynchronize(s));
+    // Light unit lengths (u8, light chunks <= kHeavyChunk): kept when the
+    // padding steps they let the SpMV skip outweigh their own reads.
+    if (G > 0 && total_units > 0 && stored_slots > 0) {
+        m->ulen = dev_alloc<uint8_t>(m, total_units);
+        CUDA_OK(cudaMemsetAsync(m->ulen, 0, total_units, s));
+        DevPtr<unsigned long long> rd(2, s);
+        CUDA_OK(cudaMemsetAsync(rd.p, 0, 2 * sizeof(unsigned long long), s));
+        k6_unit_len<<<grid_for(uint64_t(G) * 32, 256), 256, 0, s>>>(m->groups, m->unit_base, G, V, 4, m->columns,
+                                                                    m->ulen, rd.p);
+        LAUNCH_OK("k6_unit_len");
+        unsigned long long r[2] = {0, 0};
+        CUDA_OK(cudaMemcpyAsync(r, rd.p, sizeof r, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        m->unit_len_saved = (r[1] - r[0]) * (sizeof(T) + sizeof(int32_t));
+        const char* e = std::getenv("ARGCSR_ULEN");  // experiments: force 1 / 0
+        const bool keep = e ? e[0] == '1' : m->unit_len_saved > 4 * total_units;
+        if (!keep) {
+            CUDA_OK(cudaFree(m->ulen));
+            m->device_bytes -= total_units;
+            m->ulen = nullptr;
+        }
+    }
     // pipelined host path: tile column reach (light tiles only; no heavy groups, no remap)
     if (m->num_heavy == 0 && !m->x_remap && m->num_tiles >= 16) {
         const uint32_t nt = m->num_tiles;

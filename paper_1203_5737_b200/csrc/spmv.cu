@@ -273,8 +273,8 @@ __device__ __forceinline__ uint32_t find_le(const uint32_t* arr, uint32_t n, uin
 
 // Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
 // order, one lane per thread.
-template <typename T, int UH, bool RUNS>
-__global__ void __launch_bounds__(kTileThreads, 2) spmv_heavy_kernel(const SpmvArgs<T> a) {
+template <typename T, int UH, bool RUNS, int MINB>
+__global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
     __shared__ uint32_t s_lane0[kTileThreads + 1], s_row0[kTileThreads + 1], s_g[kTileThreads];
@@ -745,22 +745,29 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     }
     if (m->heavy_ctas > 0) {
         const size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
-        // vector x loads where the long rows' stored columns run consecutively
-        // (measured per matrix by the converter, xremap.cu)
-        double runs = m->x_remap ? m->run_pairs_remap : m->run_pairs_orig;
-        if (const char* e = std::getenv("ARGCSR_HEAVY_RUNS")) runs = e[0] == '1' ? 1.0 : 0.0;  // experiments
-        // (the run-loading kernel holds more registers: 8 steps in flight
-        // per lane measured best for it, 16 for the scalar one)
-        const char* uh = std::getenv("ARGCSR_HEAVY_U");  // experiments: 8 | 16
-        if (runs >= 0.5 && sizeof(T) == sizeof(double)) {
-            if (uh && uh[0] == '1')
-                launch(spmv_heavy_kernel<T, 16, true>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
-            else
-                launch(spmv_heavy_kernel<T, 8, true>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
-        } else if (uh && uh[0] == '8')
-            launch(spmv_heavy_kernel<T, 8, false>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
-        else
-            launch(spmv_heavy_kernel<T, 16, false>, m->heavy_ctas, smem, m, a, fork ? m->aux : s);
+        // Default: scalar x gathers; fp64 8 element steps in flight per lane at
+        // 4 CTAs/SM, fp32 4 steps at 6 CTAs/SM (measured best on C3/C4,
+        // DESIGN.md §4).  Experiments: ARGCSR_HEAVY_U = 4 | 8 | 16 (steps),
+        // ARGCSR_HEAVY_B = min CTAs/SM for U=8 (4 | 5), ARGCSR_HEAVY_RUNS=1:
+        // vector loads of 2 / 4 x entries where a lane's stored columns run
+        // consecutively (needs x aligned to 4 entries; x' always is).
+        const char* uh = std::getenv("ARGCSR_HEAVY_U");
+        const char* hb = std::getenv("ARGCSR_HEAVY_B");
+        const char* hr = std::getenv("ARGCSR_HEAVY_RUNS");
+        const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
+        cudaStream_t hs = fork ? m->aux : s;
+        if (hr && hr[0] == '1' && aligned) {
+            if (uh && uh[0] == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
+            else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
+        } else if (uh && uh[0] == '1') {
+            launch(spmv_heavy_kernel<T, 16, false, 2>, m->heavy_ctas, smem, m, a, hs);
+        } else if (uh ? uh[0] == '4' : sizeof(T) == sizeof(float)) {
+            launch(spmv_heavy_kernel<T, 4, false, 6>, m->heavy_ctas, smem, m, a, hs);
+        } else if ((hb && hb[0] == '5') || sizeof(T) == sizeof(float)) {
+            launch(spmv_heavy_kernel<T, 8, false, 5>, m->heavy_ctas, smem, m, a, hs);
+        } else {
+            launch(spmv_heavy_kernel<T, 8, false, 4>, m->heavy_ctas, smem, m, a, hs);
+        }
     }
     switch (m->lanes_per_unit) {
         case 4: launch_v<T, 4>(m, a, s); break;

@@ -127,8 +127,20 @@ __global__ void k_inverse(const uint32_t* __restrict__ perm, uint64_t n_used, in
 template <typename T>
 __global__ void k_gather_x(const T* __restrict__ x, const uint32_t* __restrict__ perm, uint64_t n,
                            T* __restrict__ xr) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        xr[i] = x[perm[i]];
+    // 8 independent gathers in flight per thread (the loop is latency-bound otherwise)
+    constexpr int K = 8;
+    const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += K * step) {
+        uint32_t p[K];
+        T v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) p[k] = i0 + k * step < n ? __ldg(perm + i0 + k * step) : 0u;
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = i0 + k * step < n ? __ldg(x + p[k]) : T(0);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (i0 + k * step < n) xr[i0 + k * step] = v[k];
+    }
 }
 
 template <typename P>
@@ -206,9 +218,9 @@ int32_t* build_xremap(argcsr_dev* m, const int32_t* cols, uint64_t nnz, int mode
     k_inverse<<<grid_for(n_used, 256), 256, 0, s>>>(perm, n_used, inv);
     LAUNCH_OK("k_inverse");
     bool on = mode == kXRemapOn || (!fits && top >= lead + 0.25);
-    if (!on && rp && m->dtype == ARGCSR_F64) {
-        // the second reason: long rows whose columns become consecutive (fp64:
-        // measured on C4; an fp32 handle's heavy kernel loses)
+    if (!on && rp) {
+        // the second reason: long rows whose columns become consecutive (the
+        // heavy kernel then loads 2-4 x entries per gather, measured on C4)
         Tmp<unsigned long long> runs(4, s);
         CUDA_OK(cudaMemsetAsync(runs.p, 0, 4 * sizeof(unsigned long long), s));
         k_long_row_runs<<<grid_for(m->num_rows * 32, 256), 256, 0, s>>>(rp, m->num_rows, cols_abs, inv, C, runs.p);

@@ -334,12 +334,17 @@ def test_torch_device_path(argcsr, orc):
         argcsr.spmv_torch(dev, x[:-1])
 
 
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_RUNS=1", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_U=4",
+                                   "ARGCSR_HEAVY_B=5"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("layout", LAYOUTS)
-def test_dense_rows_vector_x_runs(argcsr, orc, dtype, layout):
+def test_dense_rows_vector_x_runs(argcsr, orc, dtype, layout, heavy, monkeypatch):
     """Long rows whose columns run consecutively (directly, or after the x
-    remap for strided dense rows) take the heavy kernel's vector x loads;
+    remap for strided dense rows), through every heavy-kernel variant (the
+    default scalar gathers, vector x loads over runs, 4/16 steps in flight);
     results stay bit-identical (fp32: one rounding of the fp64 sum)."""
+    if heavy != "default":
+        monkeypatch.setenv(*heavy.split("="))
     rng = np.random.default_rng(3)
     n = 6000
     rows, cols = [], []
@@ -388,3 +393,20 @@ def test_host_staged_pipeline(argcsr, orc, kind):
     for _ in range(2):
         dev.spmv_host_staged(xh.data_ptr(), xd.data_ptr(), yd.data_ptr(), yh.data_ptr(), s.cuda_stream)
         assert bits(yh.numpy()) == bits(orc.spmv_argcsr(orc.argcsr_from_csr(A, 128, 1), x))
+
+
+@pytest.mark.parametrize("ulen", ["1", "0"])
+def test_unit_lengths_forced(argcsr, orc, corpus, monkeypatch, ulen):
+    """Light units stop at their stored length (the u8 unit-length table) or
+    read to the group's chunk: both bit-identical to the reference order."""
+    monkeypatch.setenv("ARGCSR_ULEN", ulen)
+    cases = [(A, t, d, f"corpus[{i}]") for i, A in enumerate(corpus[:60]) for t, d in ((4, 1), (12, 2), (128, 1), (32, 4))]
+    cases += [(powerlaw_csr(40000, 30000, seed=11, heavy_rows=[(5, 20000)]), t, d, "powerlaw")
+              for t, d in ((128, 1), (128, 4), (64, 2))]
+    cases += [(stencil27(12), 128, 1, "stencil27(12)")]
+    for A, tpg, dcs, w in cases:
+        dev = _check_case(argcsr, orc, A, tpg, dcs, f"{w} ({tpg},{dcs}) ulen={ulen}", layouts=(("compact", "auto"), ("reference", "auto")))
+        if ulen == "0":
+            assert dev.unit_len_bytes == 0
+        elif A.nnz:
+            assert dev.unit_len_bytes > 0

@@ -100,6 +100,7 @@ struct argcsr_dev {
     uint32_t* heavy_ptr = nullptr;        // [heavy_ctas + 1] packing of `heavy` into CTAs
     uint32_t num_tiles = 0, num_heavy = 0, heavy_ctas = 0;
     uint64_t heavy_max_lanes = 0;         // lanes of the fullest heavy CTA
+    uint64_t heavy_max_strides = 0;       // stored lanes (sum of strides) of the widest heavy CTA
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
     uint32_t max_tile_rows = 0;
     uint64_t total_units = 0;             // light units (+1 per heavy group) of the schedule

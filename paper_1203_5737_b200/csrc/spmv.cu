@@ -43,6 +43,8 @@ struct SpmvArgs {
     const uint16_t* __restrict__ tm;
     const uint16_t* __restrict__ assigned;
     const uint64_t* __restrict__ unit_base;
+    const uint8_t* __restrict__ ulen;  // light unit lengths (null: read up to the group's chunk)
+    uint64_t total_units;
     const uint32_t* __restrict__ tiles;
     const uint32_t* __restrict__ heavy;
     const uint32_t* __restrict__ heavy_ptr;
@@ -348,6 +350,15 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
 
     const uint64_t ub0 = a.unit_base[gs];
     const uint32_t row0 = MAP ? a.groups[gs].first_row : 0u;
+    // lengths of this thread's first two units (loaded under the metadata staging)
+    uint32_t ulen2[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (a.ulen) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint64_t gu = ub0 + threadIdx.x + k * blockDim.x;
+            if (gu < a.total_units) ulen2[k] = a.ulen[gu];
+        }
+    }
     for (uint32_t i = threadIdx.x; i <= ng; i += blockDim.x) {
         const GroupDesc d = a.groups[gs + i];
         const uint32_t ub = uint32_t(a.unit_base[gs + i] - ub0);
@@ -387,7 +398,12 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         double s[V];
         const uint64_t os = s_off[gi];
-        phase1<T, V, U, PRED>(a, (os & kOffsetMask) + (u - s_ub[gi]) * V, s_chunk[gi], (os >> 48) & 0x7FFF, s, pol_stream,
+        uint32_t len = s_chunk[gi];
+        if (a.ulen) {
+            const uint32_t k = (u - threadIdx.x) / blockDim.x;
+            len = min(len, k < 2 ? ulen2[k] : uint32_t(a.ulen[ub0 + u]));
+        }
+        phase1<T, V, U, PRED>(a, (os & kOffsetMask) + (u - s_ub[gi]) * V, len, (os >> 48) & 0x7FFF, s, pol_stream,
                               pol_x, xs);
 #pragma unroll
         for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = s[l];
@@ -418,6 +434,174 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ------------------------------------------ heavy path, TMA-staged stream
+// The long-chunk groups of one heavy CTA pack are streamed into a ring of
+// shared-memory stages by bulk copies (cp.async.bulk, one producer thread in
+// a dedicated warp): stage t holds element steps [t*K, t*K+K) of every group
+// in the pack -- for each group one contiguous range of its value block and
+// one of its column block (steps are j-rows of `stride` stored lanes).  The
+// 256 consumer threads (one lane each) read their column/value from shared
+// memory and keep only the x gathers in registers, so the matrix stream runs
+// up to S*K steps ahead of the gathers instead of the ~8 steps registers
+// allow.  Per lane the products are added in j order and sentinels (which
+// trail) add nothing, so results are bit-identical to the scalar kernel.
+// Requires 16-byte aligned stored ranges: V = 4 handles (tpg % 4 == 0).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+constexpr int kHeavyTmaThreads = kTileThreads + 32;  // 256 lane threads + 1 producer warp
+
+template <typename T, int K>
+__host__ __device__ constexpr size_t heavy_stage_bytes(uint64_t strides) {
+    return size_t(strides) * K * (sizeof(T) + sizeof(int32_t));
+}
+
+template <typename T, int K, int S>
+__global__ void __launch_bounds__(kHeavyTmaThreads, 1) spmv_heavy_tma_kernel(const SpmvArgs<T> a, uint32_t stage_bytes) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t full[S], empty[S];
+    __shared__ uint32_t s_lane0[kTileThreads + 1], s_row0[kTileThreads + 1], s_g[kTileThreads];
+    __shared__ uint32_t s_sec[kTileThreads + 1];  // per group: section offset inside a stage (bytes)
+    __shared__ uint32_t s_iters;
+    double* s_part = reinterpret_cast<double*>(smem + size_t(S) * stage_bytes);
+    const uint32_t hb = a.heavy_ptr[blockIdx.x], he = a.heavy_ptr[blockIdx.x + 1];
+    const uint32_t ng = he - hb;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        uint32_t lanes = 0, rows = 0, sec = 0, maxc = 0;
+        for (uint32_t i = 0; i < ng; ++i) {
+            const uint32_t g = a.heavy[hb + i];
+            const GroupDesc d = a.groups[g];
+            s_g[i] = g;
+            s_lane0[i] = lanes;
+            s_row0[i] = rows;
+            s_sec[i] = sec;
+            lanes += a.assigned[g];
+            rows += a.groups[g + 1].first_row - d.first_row;
+            sec += uint32_t(heavy_stage_bytes<T, K>(d.stride()));
+            if (g >= a.g_begin && g < a.g_end) maxc = max(maxc, d.chunk);
+        }
+        s_lane0[ng] = lanes;
+        s_row0[ng] = rows;
+        s_sec[ng] = sec;
+        s_iters = (maxc + K - 1) / K;
+        for (int t = 0; t < S; ++t) {
+            mbar_init(&full[t], 1);
+            mbar_init(&empty[t], kTileThreads / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t iters = s_iters, nlanes = s_lane0[ng], nrows = s_row0[ng];
+
+    if (tid >= kTileThreads) {  // producer warp
+        if (tid == kTileThreads) {
+            const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+            for (uint32_t it = 0; it < iters; ++it) {
+                const int t = int(it % S);
+                if (it >= uint32_t(S)) mbar_wait(&empty[t], ((it / S) - 1) & 1);
+                unsigned char* st = smem + size_t(t) * stage_bytes;
+                uint32_t bytes = 0;
+                for (uint32_t i = 0; i < ng; ++i) {
+                    const GroupDesc d = a.groups[s_g[i]];
+                    if (s_g[i] < a.g_begin || s_g[i] >= a.g_end || it * K >= d.chunk) continue;
+                    bytes += min(uint32_t(K), d.chunk - it * K) * d.stride() * uint32_t(sizeof(T) + sizeof(int32_t));
+                }
+                mbar_arrive_expect_tx(&full[t], bytes);
+                for (uint32_t i = 0; i < ng; ++i) {
+                    const GroupDesc d = a.groups[s_g[i]];
+                    if (s_g[i] < a.g_begin || s_g[i] >= a.g_end || it * K >= d.chunk) continue;
+                    const uint32_t n = min(uint32_t(K), d.chunk - it * K) * d.stride();
+                    const uint64_t src = d.offset() + uint64_t(it) * K * d.stride();
+                    unsigned char* sec = st + s_sec[i];
+                    bulk_g2s(sec, a.vals + src, n * uint32_t(sizeof(T)), &full[t], pol);
+                    bulk_g2s(sec + size_t(K) * d.stride() * sizeof(T), a.cols + src, n * 4u, &full[t], pol);
+                }
+            }
+        }
+    } else {
+        const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+        const double xs = a.x_scale ? *a.x_scale : 1.0;
+        bool active = tid < nlanes;
+        uint32_t i = 0, lane = 0, stride = 0, chunk = 0, sec = 0;
+        if (active) {
+            i = find_le(s_lane0, ng, tid);
+            const GroupDesc d = a.groups[s_g[i]];
+            lane = tid - s_lane0[i];
+            stride = d.stride();
+            chunk = d.chunk;
+            sec = s_sec[i];
+            active = s_g[i] >= a.g_begin && s_g[i] < a.g_end;
+        }
+        double sum = 0.0;
+        for (uint32_t it = 0; it < iters; ++it) {
+            const int t = int(it % S);
+            mbar_wait(&full[t], (it / S) & 1);
+            if (active && it * K < chunk) {
+                const unsigned char* st = smem + size_t(t) * stage_bytes + sec;
+                const T* sv = reinterpret_cast<const T*>(st);
+                const int32_t* sc = reinterpret_cast<const int32_t*>(st + size_t(K) * stride * sizeof(T));
+                const uint32_t n = min(uint32_t(K), chunk - it * K);
+                int c[K];
+                T v[K];
+                double xv[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    c[j] = uint32_t(j) < n ? sc[j * stride + lane] : -1;
+                    v[j] = uint32_t(j) < n ? sv[j * stride + lane] : T(0);
+                }
+#pragma unroll
+                for (int j = 0; j < K; ++j) xv[j] = c[j] != -1 ? ld_x(a.x + c[j], pol_x) : 0.0;
+                if (a.x_scale) {
+#pragma unroll
+                    for (int j = 0; j < K; ++j) xv[j] = __dmul_rn(xv[j], xs);
+                }
+#pragma unroll
+                for (int j = 0; j < K; ++j)
+                    if (c[j] != -1) sum = __dadd_rn(sum, __dmul_rn(double(v[j]), xv[j]));
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[t]);
+        }
+        if (tid < nlanes) s_part[tid] = sum;
+    }
+    __syncthreads();
+    for (uint32_t r = tid; r < nrows; r += blockDim.x) {
+        const uint32_t i = find_le(s_row0, ng, r);
+        const uint32_t g = s_g[i];
+        if (g < a.g_begin || g >= a.g_end) continue;
+        const uint32_t f = a.groups[g].first_row;
+        const uint32_t row = f + (r - s_row0[i]);
+        const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
+        a.y[row] = to_out<T>(row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
+    }
+}
 
 // --------------------------------------- persistent light path (prefetched metadata)
 // Same per-tile work as spmv_light_kernel, but each CTA walks tiles k,
@@ -629,6 +813,39 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
+// TMA-staged heavy kernel: false when it does not apply (stage ring too big
+// for shared memory, or stored ranges not 16-byte aligned).
+template <typename T, int K, int S>
+bool launch_heavy_tma(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    if (m->lanes_per_unit != 4 || m->heavy_ctas == 0) return false;
+    const size_t stage = (heavy_stage_bytes<T, K>(m->heavy_max_strides) + 127) & ~size_t(127);
+    const size_t smem = size_t(S) * stage + kTileThreads * sizeof(double);
+    if (smem > 200 * 1024) return false;
+    auto kern = spmv_heavy_tma_kernel<T, K, S>;
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(m->heavy_ctas);
+    cfg.blockDim = dim3(kHeavyTmaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.numAttrs = 0;
+    const size_t xbytes = m->n_used * sizeof(T);
+    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
+        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
+        attr[0].val.accessPolicyWindow.num_bytes = win;
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, uint32_t(stage)));
+    return true;
+}
+
 template <typename T, int V, int U, bool PRED, int MINB>
 void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // small groups (units + rows per group, on average): fill the maps, else search
@@ -721,6 +938,8 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.tm = static_cast<const uint16_t*>(m->tm);
     a.assigned = static_cast<const uint16_t*>(m->assigned);
     a.unit_base = m->unit_base;
+    a.ulen = m->ulen;
+    a.total_units = m->total_units;
     a.tiles = m->tiles;
     a.heavy = m->heavy;
     a.heavy_ptr = m->heavy_ptr;
@@ -756,7 +975,11 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
         const char* hr = std::getenv("ARGCSR_HEAVY_RUNS");
         const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
         cudaStream_t hs = fork ? m->aux : s;
-        if (hr && hr[0] == '1' && aligned) {
+        const char* ht = std::getenv("ARGCSR_HEAVY_TMA");  // experiments: 1 = K8 S4, 2 = K16 S3, 3 = K8 S8
+        if (ht && ht[0] == '1' && launch_heavy_tma<T, 8, 4>(m, a, hs)) {
+        } else if (ht && ht[0] == '2' && launch_heavy_tma<T, 16, 3>(m, a, hs)) {
+        } else if (ht && ht[0] == '3' && launch_heavy_tma<T, 8, 8>(m, a, hs)) {
+        } else if (hr && hr[0] == '1' && aligned) {
             if (uh && uh[0] == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
             else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
         } else if (uh && uh[0] == '1') {
@@ -791,6 +1014,8 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
     a.tm = static_cast<const uint16_t*>(m->tm);
     a.assigned = static_cast<const uint16_t*>(m->assigned);
     a.unit_base = m->unit_base;
+    a.ulen = m->ulen;
+    a.total_units = m->total_units;
     a.tiles = m->tiles;
     a.heavy = m->heavy;
     a.heavy_ptr = m->heavy_ptr;

@@ -27,6 +27,24 @@ def test_fused_scale_is_bit_identical(argcsr, orc, x_remap):
     assert bits(y1.cpu().numpy()) == bits(ref)
 
 
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_TMA=1", "ARGCSR_HEAVY_RUNS=1"])
+def test_fused_scale_heavy_groups(argcsr, orc, heavy, monkeypatch):
+    """The fused scale through the long-chunk kernels (register- and TMA-staged)."""
+    from helpers import powerlaw_csr
+
+    if heavy != "default":
+        monkeypatch.setenv(*heavy.split("="))
+    A = powerlaw_csr(20000, 20000, seed=5, heavy_rows=[(3, 12000), (9000, 7000)])
+    m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1)
+    assert m.heavy_groups > 0
+    x = torch.linspace(-3, 3, A.num_cols, dtype=torch.float64, device="cuda")
+    s = torch.tensor([1.0 / 7.3], dtype=torch.float64, device="cuda")
+    y1 = torch.empty(A.num_rows, dtype=torch.float64, device="cuda")
+    m.spmv_scaled_device(x.data_ptr(), s.data_ptr(), y1.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    ref = orc.spmv_argcsr(orc.argcsr_from_csr(A, 128, 1), (x * s).cpu().numpy())
+    assert bits(y1.cpu().numpy()) == bits(ref)
+
+
 @pytest.mark.parametrize("tpg,dcs", [(128, 1), (128, 32)])
 def test_power_iteration_single_rank(tpg, dcs):
     import oracle

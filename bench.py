@@ -50,6 +50,9 @@ def parse_args():
     p.add_argument("--no-variants", action="store_true", help="skip the tuned-dcs and cuSPARSE side runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-steps", type=int, default=20)
+    p.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo", "p2p"],
+                   help="multi-GPU x exchange: NCCL all-gather / halo all-to-all (auto picks), or p2p: "
+                        "the SpMV epilogue stores y straight into the peers' x over NVLink (peer.py)")
     p.add_argument("--power-iteration", action="store_true",
                    help="a step is one power-iteration step (SpMV, ||y|| all-reduce, all-gather, fused scaling)")
     return p.parse_args()
@@ -274,7 +277,8 @@ def run_b200(args):
             from paper_1203_5737_b200.multigpu import DistributedArgCsr
 
             D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values.to(tdtype),
-                                  args.tpg, args.dcs, device=dev, dtype=tdtype, layout=args.layout)
+                                  args.tpg, args.dcs, device=dev, dtype=tdtype, layout=args.layout,
+                                  exchange=args.exchange)
             m = D.engine.m
             S = D.slice
         else:
@@ -333,20 +337,34 @@ def run_b200(args):
         pscale = torch.ones(1, dtype=torch.float64, device=dev)
         ps2 = torch.zeros(1, dtype=torch.float64, device=dev)
 
+        if D.pstep is not None:
+            if not args.power_iteration:
+                raise SystemExit("--exchange p2p is the power-iteration step (use --power-iteration)")
+            D.pstep.begin(x)
+
         def step():
             # y = A_p x_i on this rank's rows, then the all-gather of y into
             # every rank's x_{i+1} (NCCL over NVLink), double-buffered x;
             # power iteration adds the 8-byte ||y||^2 all-reduce and the
-            # scaling fused into the next SpMV's gathers.
-            if args.power_iteration:
+            # scaling fused into the next SpMV's gathers.  p2p: the SpMV
+            # stores y into every GPU's next x itself; flags + partial norms.
+            if D.pstep is not None:
+                D.pstep.step()
+            elif args.power_iteration:
                 D.step(bufs[it[0] % 2], bufs[(it[0] + 1) % 2], pscale, ps2)
             else:
                 D.spmv_gather(bufs[it[0] % 2], bufs[(it[0] + 1) % 2], wait=False)
             it[0] += 1
 
+        def drain():
+            if D.pstep is not None:
+                D.pstep.wait(D.pstep.k)
+            else:
+                D.wait_gather()
+
         for _ in range(args.warmup):
             step()
-        D.wait_gather()
+        drain()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -355,7 +373,7 @@ def run_b200(args):
         e0.record()
         for _ in range(args.steps):
             step()
-        D.wait_gather()  # the last all-gather is part of the timed region
+        drain()  # the last all-gather (p2p: the last peers' flags) is part of the timed region
         e1.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -366,11 +384,15 @@ def run_b200(args):
             t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
-        if args.power_iteration:
+        if D.pstep is not None:
+            pi_lambda = D.pstep.finish()[0]
+        elif args.power_iteration:
             pi_lambda = float(torch.sqrt(ps2).item())
         step_ms = total_ms / args.steps
         per_call = (1 if m.heavy_ctas else 0) + (1 if m.light_tiles else 0)
-        if D.overlap:  # interior + two boundary ranges; the last reuses the x' gather
+        if D.pstep is not None:  # one SpMV (+ x' gather), signal and wait kernels
+            launches = args.steps * (per_call + (1 if m.x_remap else 0) + (2 if world > 1 else 0))
+        elif D.overlap:  # interior + two boundary ranges; the last reuses the x' gather
             launches = args.steps * (3 * per_call + (2 if m.x_remap else 0))
         else:
             launches = args.steps * (per_call + (1 if m.x_remap else 0))
@@ -379,6 +401,8 @@ def run_b200(args):
 
     gflops = 2.0 * nnz_total / (step_ms * 1e-3) / 1e9
     eff_gbs = ab / (step_ms * 1e-3) / 1e9
+    if D is not None and D.peer is not None:
+        D.close()  # collective over the ranks: nobody stores into freed peer buffers
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -403,8 +427,11 @@ def run_b200(args):
                    "l2": ("flushed between steps (working set < 4x L2)" if flush_buf is not None else
                           f"inputs larger than L2 (ARG-CSR arrays {m.stored_slots * (sv + 4) / 1e9:.2f} GB); "
                           "x kept L2-resident by design (access-policy window)"),
-                   "parallelism": (f"rows nnz-balanced over {world} GPU(s), {D.exchange} x exchange overlapped "
-                                   f"with the interior groups" if world > 1 else "single GPU")},
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"rows nnz-balanced over {world} GPU(s), SpMV epilogue stores y into every "
+                                   f"GPU's next x over NVLink (p2p), flag + partial-norm signals" if D.exchange == "p2p"
+                                   else f"rows nnz-balanced over {world} GPU(s), {D.exchange} x exchange overlapped "
+                                   f"with the interior groups")},
         "eff_GBps": round(eff_gbs, 1), "pct_of_8TBps": round(100 * eff_gbs / NOMINAL_HBM_GBS, 2),
         "pct_of_measured": round(100 * eff_gbs / peak, 2),
         "roofline": {"bound": "hbm", "achieved": round(eff_gbs, 1), "peak": peak, "unit": "GB/s",

@@ -182,6 +182,34 @@ ARGCSR_API argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, 
                                  uint64_t group_begin, uint64_t group_end, void* y, uint32_t flags,
                                  void* stream);
 
+/* ------------------------------------------ multi-GPU step over peer memory
+ * The fused form of "SpMV, then all-gather y": the kernel's
+ * epilogue stores every y row both to y and to peer_y[q][row] for q < npeers
+ * (npeers <= 7) -- the other GPUs' next-x buffers seen through NVLink peer
+ * mappings (argcsr_peer_open), pre-offset by this slice's first row -- so the
+ * y slice reaches every GPU tile by tile while the SpMV runs, with no separate
+ * collective.  Otherwise argcsr_dev_spmv_ex. */
+ARGCSR_API argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const double* x_scale,
+                                              uint64_t group_begin, uint64_t group_end, void* y,
+                                              void* const* peer_y, uint32_t npeers, uint32_t flags,
+                                              void* stream);
+
+/* Step signalling, stream-ordered one-thread kernels: store `value` into
+ * *flags[q] for q < n with system-scope release semantics (after copying the
+ * device scalar *partial to *partial_dst[q] when both are non-NULL); wait
+ * until every flags[i] (i < n, local memory written by peers) is >= value. */
+ARGCSR_API argcsr_status argcsr_peer_signal(uint64_t* const* flags, uint32_t n, uint64_t value,
+                                            const double* partial, double* const* partial_dst, void* stream);
+ARGCSR_API argcsr_status argcsr_peer_wait(const uint64_t* flags, uint32_t n, uint64_t value, void* stream);
+
+/* Device buffers shared between the processes of one box (CUDA IPC): allocate
+ * `bytes` (zeroed) on `device` and return its 64-byte IPC handle; open a
+ * peer's handle in this process (peer access is enabled first); close/free. */
+ARGCSR_API argcsr_status argcsr_peer_alloc(uint64_t bytes, int device, void** ptr, unsigned char handle[64]);
+ARGCSR_API argcsr_status argcsr_peer_open(const unsigned char handle[64], int device, void** ptr);
+ARGCSR_API argcsr_status argcsr_peer_close(void* ptr);
+ARGCSR_API argcsr_status argcsr_peer_free(void* ptr);
+
 /* Host-buffer form of spmv_argcsr (argcsr.cpp:219-227): checks x_len ==
  * num_cols (DimensionError, same message shape), copies x in, multiplies,
  * copies y (num_rows entries) out, synchronises. */

@@ -350,6 +350,49 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
     m.attr("kDefaultDesiredChunkSize") = kDefaultDesiredChunkSize;
     m.attr("kPaddingColumn") = kPaddingColumn;
     m.def("abi_version", &argcsr_abi_version);
+    // multi-GPU step over peer memory (argcsr_gpu.h: argcsr_peer_*)
+    m.def(
+        "peer_signal",
+        [](const std::vector<std::uintptr_t>& flags, std::uint64_t value, std::uintptr_t partial,
+           const std::vector<std::uintptr_t>& partial_dst, std::uintptr_t stream) {
+            if (!partial_dst.empty() && partial_dst.size() != flags.size())
+                throw ParameterError("peer_signal: one partial destination per flag");
+            std::vector<uint64_t*> f(flags.size());
+            std::vector<double*> d(partial_dst.size());
+            for (size_t i = 0; i < f.size(); ++i) f[i] = reinterpret_cast<uint64_t*>(flags[i]);
+            for (size_t i = 0; i < d.size(); ++i) d[i] = reinterpret_cast<double*>(partial_dst[i]);
+            check(argcsr_peer_signal(f.data(), uint32_t(f.size()), value, reinterpret_cast<const double*>(partial),
+                                     d.empty() ? nullptr : d.data(), reinterpret_cast<void*>(stream)));
+        },
+        py::arg("flag_ptrs"), py::arg("value"), py::arg("partial_ptr") = 0, py::arg("partial_dst_ptrs") = std::vector<std::uintptr_t>{},
+        py::arg("stream") = 0);
+    m.def(
+        "peer_wait",
+        [](std::uintptr_t flags, std::uint32_t n, std::uint64_t value, std::uintptr_t stream) {
+            check(argcsr_peer_wait(reinterpret_cast<const uint64_t*>(flags), n, value, reinterpret_cast<void*>(stream)));
+        },
+        py::arg("flags_ptr"), py::arg("n"), py::arg("value"), py::arg("stream") = 0);
+    m.def(
+        "peer_alloc",
+        [](std::uint64_t bytes, int device) {
+            void* p = nullptr;
+            unsigned char h[64];
+            check(argcsr_peer_alloc(bytes, device, &p, h));
+            return py::make_tuple(reinterpret_cast<std::uintptr_t>(p), py::bytes(reinterpret_cast<const char*>(h), 64));
+        },
+        py::arg("bytes"), py::arg("device"));
+    m.def(
+        "peer_open",
+        [](const py::bytes& handle, int device) {
+            const std::string h = handle;
+            if (h.size() != 64) throw ParameterError("peer_open: an IPC handle is 64 bytes");
+            void* p = nullptr;
+            check(argcsr_peer_open(reinterpret_cast<const unsigned char*>(h.data()), device, &p));
+            return reinterpret_cast<std::uintptr_t>(p);
+        },
+        py::arg("handle"), py::arg("device"));
+    m.def("peer_close", [](std::uintptr_t p) { check(argcsr_peer_close(reinterpret_cast<void*>(p))); }, py::arg("ptr"));
+    m.def("peer_free", [](std::uintptr_t p) { check(argcsr_peer_free(reinterpret_cast<void*>(p))); }, py::arg("ptr"));
 
     py::class_<CsrMatrix>(m, "CsrMatrix")
         .def(py::init<>())
@@ -467,6 +510,17 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
                                               reinterpret_cast<void*>(stream)));
              },
              py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
+        .def("spmv_peer_device",
+             [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uint64_t gb, std::uint64_t ge,
+                std::uintptr_t y, const std::vector<std::uintptr_t>& peers, std::uint32_t flags, std::uintptr_t stream) {
+                 std::vector<void*> pp(peers.size());
+                 for (size_t i = 0; i < peers.size(); ++i) pp[i] = reinterpret_cast<void*>(peers[i]);
+                 check(argcsr_dev_spmv_peer(p.dev->handle(), reinterpret_cast<const void*>(x),
+                                            reinterpret_cast<const double*>(scale), gb, ge, reinterpret_cast<void*>(y),
+                                            pp.data(), uint32_t(pp.size()), flags, reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("group_begin"), py::arg("group_end"), py::arg("y_ptr"),
+             py::arg("peer_y_ptrs"), py::arg("flags") = 0u, py::arg("stream") = 0)
         .def("spmv_ex_device",
              [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uint64_t gb, std::uint64_t ge,
                 std::uintptr_t y, std::uint32_t flags, std::uintptr_t stream) {

@@ -405,6 +405,76 @@ argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, const doubl
     });
 }
 
+argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const double* x_scale, uint64_t group_begin,
+                                   uint64_t group_end, void* y, void* const* peer_y, uint32_t npeers, uint32_t flags,
+                                   void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null vector");
+        if (flags & ~uint32_t(ARGCSR_SPMV_REUSE_X)) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: unknown flags");
+        if (npeers > argcsr_gpu::kMaxPeers) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: at most 7 peers");
+        if (npeers && !peer_y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null peer list");
+        for (uint32_t q = 0; q < npeers; ++q)
+            if (!peer_y[q]) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null peer buffer");
+        DeviceScope scope(m->device);
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream), x_scale,
+                                (flags & ARGCSR_SPMV_REUSE_X) != 0, peer_y, npeers);
+    });
+}
+
+argcsr_status argcsr_peer_signal(uint64_t* const* flags, uint32_t n, uint64_t value, const double* partial,
+                                 double* const* partial_dst, void* stream) {
+    return guarded([&] {
+        if (n > argcsr_gpu::kMaxPeers) fail(ARGCSR_E_PARAMETER, "argcsr_peer_signal: at most 7 peers");
+        if (n && !flags) fail(ARGCSR_E_PARAMETER, "argcsr_peer_signal: null flag list");
+        argcsr_gpu::peer_signal(flags, n, value, partial, partial_dst, static_cast<cudaStream_t>(stream));
+    });
+}
+
+argcsr_status argcsr_peer_wait(const uint64_t* flags, uint32_t n, uint64_t value, void* stream) {
+    return guarded([&] {
+        if (n && !flags) fail(ARGCSR_E_PARAMETER, "argcsr_peer_wait: null flags");
+        argcsr_gpu::peer_wait(flags, n, value, static_cast<cudaStream_t>(stream));
+    });
+}
+
+argcsr_status argcsr_peer_alloc(uint64_t bytes, int device, void** ptr, unsigned char handle[64]) {
+    return guarded([&] {
+        if (!ptr || !handle) fail(ARGCSR_E_PARAMETER, "argcsr_peer_alloc: null output");
+        DeviceScope scope(device);
+        void* p = nullptr;
+        CUDA_OK(cudaMalloc(&p, std::max<uint64_t>(bytes, 1)));
+        CUDA_OK(cudaMemset(p, 0, std::max<uint64_t>(bytes, 1)));
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            CUDA_OK(e);
+        }
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(handle, &h, 64);
+        *ptr = p;
+    });
+}
+
+argcsr_status argcsr_peer_open(const unsigned char handle[64], int device, void** ptr) {
+    return guarded([&] {
+        if (!ptr || !handle) fail(ARGCSR_E_PARAMETER, "argcsr_peer_open: null argument");
+        DeviceScope scope(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, 64);
+        CUDA_OK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+argcsr_status argcsr_peer_close(void* ptr) {
+    return guarded([&] { CUDA_OK(cudaIpcCloseMemHandle(ptr)); });
+}
+
+argcsr_status argcsr_peer_free(void* ptr) {
+    return guarded([&] { CUDA_OK(cudaFree(ptr)); });
+}
+
 argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x, uint64_t x_len, void* y) {
     return guarded([&] {
         check_handle(m);

@@ -71,6 +71,8 @@ constexpr uint32_t kHeavyChunk = 32;
 // Threads per SpMV CTA, and the default number of units (V-lane vectors) per
 // light tile: a tile is walked by one CTA, two units per thread (measured best
 // on the stencil and power-law configs, profiles/ and DESIGN.md §4).
+// Peers a multi-GPU SpMV epilogue stores into (8 GPUs per box).
+constexpr uint32_t kMaxPeers = 7;
 constexpr int kTileThreads = 256;
 constexpr int kDefaultTileUnits = 512;
 
@@ -100,7 +102,6 @@ struct argcsr_dev {
     uint32_t* heavy_ptr = nullptr;        // [heavy_ctas + 1] packing of `heavy` into CTAs
     uint32_t num_tiles = 0, num_heavy = 0, heavy_ctas = 0;
     uint64_t heavy_max_lanes = 0;         // lanes of the fullest heavy CTA
-    uint64_t heavy_max_strides = 0;       // stored lanes (sum of strides) of the widest heavy CTA
     uint32_t max_tile_groups = 0;         // bound used for shared-memory sizing
     uint32_t max_tile_rows = 0;
     uint64_t total_units = 0;             // light units (+1 per heavy group) of the schedule

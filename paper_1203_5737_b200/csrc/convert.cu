@@ -766,23 +766,19 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
             std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return hch[a] > hch[b]; });
             std::vector<uint32_t> sorted(nh);
             // Pack consecutive (similar-chunk) heavy groups into CTAs of <= kTileThreads lanes.
-            uint64_t lanes = 0, strides = 0;  // strides: stored lanes of the pack (TMA stage width)
+            uint64_t lanes = 0;
             for (uint64_t i = 0; i < nh; ++i) {
                 sorted[i] = hid[order[i]];
                 const uint64_t l = hln[order[i]];
-                const uint64_t st = compact ? (l + V - 1) / V * V : tpg;
                 if (lanes > 0 && lanes + l > uint64_t(kTileThreads)) {
                     hptr.push_back(uint32_t(i));
                     max_lanes = std::max(max_lanes, lanes);
-                    m->heavy_max_strides = std::max(m->heavy_max_strides, strides);
-                    lanes = strides = 0;
+                    lanes = 0;
                 }
                 lanes += l;
-                strides += st;
             }
             hptr.push_back(uint32_t(nh));
             max_lanes = std::max(max_lanes, lanes);
-            m->heavy_max_strides = std::max(m->heavy_max_strides, strides);
             CUDA_OK(cudaMemcpyAsync(m->heavy, sorted.data(), nh * 4, cudaMemcpyHostToDevice, s));
         }
         m->heavy_ctas = uint32_t(hptr.size() - 1);

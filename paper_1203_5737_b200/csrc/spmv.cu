@@ -59,6 +59,8 @@ struct SpmvArgs {
     const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
+    uint32_t npeers;         // multi-GPU epilogue: every y row is also stored to peer_y[q][row]
+    T* peer_y[kMaxPeers];    // (other GPUs' x buffers through NVLink peer mappings, pre-offset)
 };
 
 // ------------------------------------------------------------ cache policies
@@ -256,6 +258,16 @@ template <typename T> __device__ __forceinline__ T to_out(double v);
 template <> __device__ __forceinline__ double to_out<double>(double v) { return v; }
 template <> __device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
 
+// Epilogue: y[row], and the same value into every peer's buffer (the fused
+// all-gather of the multi-GPU step: the y slice lands in the other GPUs' next
+// x directly from the kernel, as plain stores over the NVLink peer mapping).
+template <typename T>
+__device__ __forceinline__ void store_y(const SpmvArgs<T>& a, uint32_t row, double v) {
+    const T o = to_out<T>(v);
+    a.y[row] = o;
+    for (uint32_t q = 0; q < a.npeers; ++q) a.peer_y[q][row] = o;
+}
+
 // Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending.
 __device__ __forceinline__ double row_sum(const double* part, uint32_t b, uint32_t e) {
     double sum = 0.0;
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
         const uint32_t f = a.groups[g].first_row;
         const uint32_t row = f + (r - s_row0[i]);
         const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
-        a.y[row] = to_out<T>(row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
+        store_y(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
     }
 }
 
@@ -410,13 +422,13 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     }
     __syncthreads();
 
-    if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
+    if (pvalid) store_y(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
     for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
         const uint32_t gi = MAP ? s_rgrp[r - row0] : find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
-        a.y[r] = to_out<T>(row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
+        store_y(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
     }
 }
 
@@ -434,174 +446,6 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// ------------------------------------------ heavy path, TMA-staged stream
-// The long-chunk groups of one heavy CTA pack are streamed into a ring of
-// shared-memory stages by bulk copies (cp.async.bulk, one producer thread in
-// a dedicated warp): stage t holds element steps [t*K, t*K+K) of every group
-// in the pack -- for each group one contiguous range of its value block and
-// one of its column block (steps are j-rows of `stride` stored lanes).  The
-// 256 consumer threads (one lane each) read their column/value from shared
-// memory and keep only the x gathers in registers, so the matrix stream runs
-// up to S*K steps ahead of the gathers instead of the ~8 steps registers
-// allow.  Per lane the products are added in j order and sentinels (which
-// trail) add nothing, so results are bit-identical to the scalar kernel.
-// Requires 16-byte aligned stored ranges: V = 4 handles (tpg % 4 == 0).
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-
-constexpr int kHeavyTmaThreads = kTileThreads + 32;  // 256 lane threads + 1 producer warp
-
-template <typename T, int K>
-__host__ __device__ constexpr size_t heavy_stage_bytes(uint64_t strides) {
-    return size_t(strides) * K * (sizeof(T) + sizeof(int32_t));
-}
-
-template <typename T, int K, int S>
-__global__ void __launch_bounds__(kHeavyTmaThreads, 1) spmv_heavy_tma_kernel(const SpmvArgs<T> a, uint32_t stage_bytes) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t full[S], empty[S];
-    __shared__ uint32_t s_lane0[kTileThreads + 1], s_row0[kTileThreads + 1], s_g[kTileThreads];
-    __shared__ uint32_t s_sec[kTileThreads + 1];  // per group: section offset inside a stage (bytes)
-    __shared__ uint32_t s_iters;
-    double* s_part = reinterpret_cast<double*>(smem + size_t(S) * stage_bytes);
-    const uint32_t hb = a.heavy_ptr[blockIdx.x], he = a.heavy_ptr[blockIdx.x + 1];
-    const uint32_t ng = he - hb;
-    const uint32_t tid = threadIdx.x;
-    if (tid == 0) {
-        uint32_t lanes = 0, rows = 0, sec = 0, maxc = 0;
-        for (uint32_t i = 0; i < ng; ++i) {
-            const uint32_t g = a.heavy[hb + i];
-            const GroupDesc d = a.groups[g];
-            s_g[i] = g;
-            s_lane0[i] = lanes;
-            s_row0[i] = rows;
-            s_sec[i] = sec;
-            lanes += a.assigned[g];
-            rows += a.groups[g + 1].first_row - d.first_row;
-            sec += uint32_t(heavy_stage_bytes<T, K>(d.stride()));
-            if (g >= a.g_begin && g < a.g_end) maxc = max(maxc, d.chunk);
-        }
-        s_lane0[ng] = lanes;
-        s_row0[ng] = rows;
-        s_sec[ng] = sec;
-        s_iters = (maxc + K - 1) / K;
-        for (int t = 0; t < S; ++t) {
-            mbar_init(&full[t], 1);
-            mbar_init(&empty[t], kTileThreads / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t iters = s_iters, nlanes = s_lane0[ng], nrows = s_row0[ng];
-
-    if (tid >= kTileThreads) {  // producer warp
-        if (tid == kTileThreads) {
-            const uint64_t pol = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
-            for (uint32_t it = 0; it < iters; ++it) {
-                const int t = int(it % S);
-                if (it >= uint32_t(S)) mbar_wait(&empty[t], ((it / S) - 1) & 1);
-                unsigned char* st = smem + size_t(t) * stage_bytes;
-                uint32_t bytes = 0;
-                for (uint32_t i = 0; i < ng; ++i) {
-                    const GroupDesc d = a.groups[s_g[i]];
-                    if (s_g[i] < a.g_begin || s_g[i] >= a.g_end || it * K >= d.chunk) continue;
-                    bytes += min(uint32_t(K), d.chunk - it * K) * d.stride() * uint32_t(sizeof(T) + sizeof(int32_t));
-                }
-                mbar_arrive_expect_tx(&full[t], bytes);
-                for (uint32_t i = 0; i < ng; ++i) {
-                    const GroupDesc d = a.groups[s_g[i]];
-                    if (s_g[i] < a.g_begin || s_g[i] >= a.g_end || it * K >= d.chunk) continue;
-                    const uint32_t n = min(uint32_t(K), d.chunk - it * K) * d.stride();
-                    const uint64_t src = d.offset() + uint64_t(it) * K * d.stride();
-                    unsigned char* sec = st + s_sec[i];
-                    bulk_g2s(sec, a.vals + src, n * uint32_t(sizeof(T)), &full[t], pol);
-                    bulk_g2s(sec + size_t(K) * d.stride() * sizeof(T), a.cols + src, n * 4u, &full[t], pol);
-                }
-            }
-        }
-    } else {
-        const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-        const double xs = a.x_scale ? *a.x_scale : 1.0;
-        bool active = tid < nlanes;
-        uint32_t i = 0, lane = 0, stride = 0, chunk = 0, sec = 0;
-        if (active) {
-            i = find_le(s_lane0, ng, tid);
-            const GroupDesc d = a.groups[s_g[i]];
-            lane = tid - s_lane0[i];
-            stride = d.stride();
-            chunk = d.chunk;
-            sec = s_sec[i];
-            active = s_g[i] >= a.g_begin && s_g[i] < a.g_end;
-        }
-        double sum = 0.0;
-        for (uint32_t it = 0; it < iters; ++it) {
-            const int t = int(it % S);
-            mbar_wait(&full[t], (it / S) & 1);
-            if (active && it * K < chunk) {
-                const unsigned char* st = smem + size_t(t) * stage_bytes + sec;
-                const T* sv = reinterpret_cast<const T*>(st);
-                const int32_t* sc = reinterpret_cast<const int32_t*>(st + size_t(K) * stride * sizeof(T));
-                const uint32_t n = min(uint32_t(K), chunk - it * K);
-                int c[K];
-                T v[K];
-                double xv[K];
-#pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    c[j] = uint32_t(j) < n ? sc[j * stride + lane] : -1;
-                    v[j] = uint32_t(j) < n ? sv[j * stride + lane] : T(0);
-                }
-#pragma unroll
-                for (int j = 0; j < K; ++j) xv[j] = c[j] != -1 ? ld_x(a.x + c[j], pol_x) : 0.0;
-                if (a.x_scale) {
-#pragma unroll
-                    for (int j = 0; j < K; ++j) xv[j] = __dmul_rn(xv[j], xs);
-                }
-#pragma unroll
-                for (int j = 0; j < K; ++j)
-                    if (c[j] != -1) sum = __dadd_rn(sum, __dmul_rn(double(v[j]), xv[j]));
-            }
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[t]);
-        }
-        if (tid < nlanes) s_part[tid] = sum;
-    }
-    __syncthreads();
-    for (uint32_t r = tid; r < nrows; r += blockDim.x) {
-        const uint32_t i = find_le(s_row0, ng, r);
-        const uint32_t g = s_g[i];
-        if (g < a.g_begin || g >= a.g_end) continue;
-        const uint32_t f = a.groups[g].first_row;
-        const uint32_t row = f + (r - s_row0[i]);
-        const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
-        a.y[row] = to_out<T>(row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
-    }
-}
 
 // --------------------------------------- persistent light path (prefetched metadata)
 // Same per-tile work as spmv_light_kernel, but each CTA walks tiles k,
@@ -716,13 +560,13 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
         uint32_t gs2 = 0, ge2 = 0;
         if (k2 < num_tiles) gs2 = a.tiles[k2], ge2 = a.tiles[k2 + 1];
 
-        if (pvalid) a.y[pr] = to_out<T>(row_sum(s_part + size_t(mub[pgi] - ub0) * V, pb, pe));
+        if (pvalid) store_y(a, pr, row_sum(s_part + size_t(mub[pgi] - ub0) * V, pb, pe));
         for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
             const uint32_t gi = find_row(md, ng, r);
             const uint32_t g = gs + gi;
             if (md[gi].heavy() || g < a.g_begin || g >= a.g_end) continue;
             const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
-            a.y[r] = to_out<T>(row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
+            store_y(a, r, row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
         }
         __syncthreads();
         k = kn, gs = gsn, ge = gen;
@@ -813,39 +657,6 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
-// TMA-staged heavy kernel: false when it does not apply (stage ring too big
-// for shared memory, or stored ranges not 16-byte aligned).
-template <typename T, int K, int S>
-bool launch_heavy_tma(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    if (m->lanes_per_unit != 4 || m->heavy_ctas == 0) return false;
-    const size_t stage = (heavy_stage_bytes<T, K>(m->heavy_max_strides) + 127) & ~size_t(127);
-    const size_t smem = size_t(S) * stage + kTileThreads * sizeof(double);
-    if (smem > 200 * 1024) return false;
-    auto kern = spmv_heavy_tma_kernel<T, K, S>;
-    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(m->heavy_ctas);
-    cfg.blockDim = dim3(kHeavyTmaThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    cfg.numAttrs = 0;
-    const size_t xbytes = m->n_used * sizeof(T);
-    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
-        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
-        attr[0].val.accessPolicyWindow.num_bytes = win;
-        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
-    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, uint32_t(stage)));
-    return true;
-}
-
 template <typename T, int V, int U, bool PRED, int MINB>
 void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // small groups (units + rows per group, on average): fill the maps, else search
@@ -929,8 +740,10 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
 
 template <typename T>
 void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, void* y, uint32_t gb, uint32_t ge,
-                  cudaStream_t s) {
-    SpmvArgs<T> a;
+                  cudaStream_t s, void* const* peer_y, uint32_t npeers) {
+    SpmvArgs<T> a{};
+    a.npeers = npeers;
+    for (uint32_t q = 0; q < npeers; ++q) a.peer_y[q] = static_cast<T*>(peer_y[q]);
     a.x_scale = x_scale;
     a.vals = static_cast<const T*>(m->values);
     a.cols = m->columns;
@@ -975,11 +788,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
         const char* hr = std::getenv("ARGCSR_HEAVY_RUNS");
         const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
         cudaStream_t hs = fork ? m->aux : s;
-        const char* ht = std::getenv("ARGCSR_HEAVY_TMA");  // experiments: 1 = K8 S4, 2 = K16 S3, 3 = K8 S8
-        if (ht && ht[0] == '1' && launch_heavy_tma<T, 8, 4>(m, a, hs)) {
-        } else if (ht && ht[0] == '2' && launch_heavy_tma<T, 16, 3>(m, a, hs)) {
-        } else if (ht && ht[0] == '3' && launch_heavy_tma<T, 8, 8>(m, a, hs)) {
-        } else if (hr && hr[0] == '1' && aligned) {
+        if (hr && hr[0] == '1' && aligned) {
             if (uh && uh[0] == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
             else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
         } else if (uh && uh[0] == '1') {
@@ -1049,13 +858,61 @@ void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0,
 }
 
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale, bool reuse_x) {
+                 cudaStream_t s, const double* x_scale, bool reuse_x, void* const* peer_y, uint32_t npeers) {
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
     x = reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
-    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s);
-    else launch_dtype<float>(m, x, x_scale, y, gb, ge, s);
+    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s, peer_y, npeers);
+    else launch_dtype<float>(m, x, x_scale, y, gb, ge, s, peer_y, npeers);
+}
+
+// ------------------------------------------------ multi-GPU step signalling
+// A rank announces "my slice of the next x (and my partial ||y||^2) has
+// landed in your buffers" by storing the step number into its slot of every
+// peer's flag array; a peer waits until all its slots reach the step.  The
+// stores of the preceding SpMV (same stream, earlier kernel) are ordered
+// before the flag by the system-scope release fence.
+struct PeerSlots {  // by value as a kernel parameter
+    uint64_t* flag[kMaxPeers];
+    double* partial[kMaxPeers];
+};
+
+__global__ void k_peer_signal(PeerSlots p, uint32_t n, uint64_t value, const double* partial) {
+    if (threadIdx.x != 0) return;
+    if (partial) {
+        const double v = *partial;
+        for (uint32_t q = 0; q < n; ++q) p.partial[q][0] = v;
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (uint32_t q = 0; q < n; ++q)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag[q]), "l"(value) : "memory");
+}
+
+__global__ void k_peer_wait(const uint64_t* flags, uint32_t n, uint64_t value) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        uint64_t v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
+            if (v < value) __nanosleep(200);
+        } while (v < value);
+    }
+    __syncthreads();
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+void peer_signal(uint64_t* const* flags, uint32_t n, uint64_t value, const double* partial,
+                 double* const* partial_dst, cudaStream_t s) {
+    PeerSlots p{};
+    for (uint32_t q = 0; q < n; ++q) p.flag[q] = flags[q], p.partial[q] = partial_dst ? partial_dst[q] : nullptr;
+    k_peer_signal<<<1, 32, 0, s>>>(p, n, value, partial_dst ? partial : nullptr);
+    CUDA_OK(cudaGetLastError());
+}
+
+void peer_wait(const uint64_t* flags, uint32_t n, uint64_t value, cudaStream_t s) {
+    if (n == 0) return;
+    k_peer_wait<<<1, 32, 0, s>>>(flags, n, value);
+    CUDA_OK(cudaGetLastError());
 }
 
 }  // namespace argcsr_gpu

@@ -12,8 +12,18 @@ namespace argcsr_gpu {
 // scaling x first; 1.0 is an exact no-op.
 // reuse_x: an x remap handle skips its x' gather and reuses the x' of the
 // previous launch on this handle (same x, stream-ordered after it).
+// peer_y[0 .. npeers): every row written to y is also stored to peer_y[q][row]
+// (multi-GPU: the other GPUs' x buffers, pre-offset by this slice's first row).
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale = nullptr, bool reuse_x = false);
+                 cudaStream_t s, const double* x_scale = nullptr, bool reuse_x = false,
+                 void* const* peer_y = nullptr, uint32_t npeers = 0);
+
+// Step signalling between the GPUs of a multi-GPU step (spmv.cu): store
+// `value` into flags[q] (system-scope release, after *partial is copied to
+// partial_dst[q] when both are given); wait until flags[0 .. n) >= value.
+void peer_signal(uint64_t* const* flags, uint32_t n, uint64_t value, const double* partial,
+                 double* const* partial_dst, cudaStream_t s);
+void peer_wait(const uint64_t* flags, uint32_t n, uint64_t value, cudaStream_t s);
 
 // Light tiles [t0, t1) only (handles without heavy groups or x remap): the
 // pipelined host path launches the tiles whose x window has arrived.

@@ -182,9 +182,23 @@ class DistributedArgCsr:
         # x exchange between steps: the all-gather of every y slice, or only
         # the halo -- the x entries of other ranks this rank's columns use
         # (auto: halo when it moves < 1/4 of the all-gather's volume)
-        if exchange not in ("auto", "allgather", "halo"):
-            raise ValueError("exchange must be 'auto', 'allgather' or 'halo'")
+        if exchange not in ("auto", "allgather", "halo", "p2p"):
+            raise ValueError("exchange must be 'auto', 'allgather', 'halo' or 'p2p'")
         self.halo = None
+        self.peer = self.pstep = None
+        if exchange == "p2p":
+            # fused SpMV + peer stores over NVLink (peer.py): no collective in the step
+            from .peer import PeerBuffers, PeerPowerIteration
+
+            self.overlap = False
+            self.peer = PeerBuffers(self.rank, self.world, num_cols, dtype, self.device)
+            if self.world > 1:
+                handles = [None] * self.world
+                dist.all_gather_object(handles, self.peer.handle, group=self.group)
+                self.peer.connect_ipc(handles)
+            self.pstep = PeerPowerIteration(self.engine, r0, r1, self.peer)
+            self.exchange = "p2p"
+            return
         if self.overlap and exchange != "allgather":
             self.halo = self._build_halo()
             total = int(self.halo["recv_total"].item())
@@ -261,6 +275,15 @@ class DistributedArgCsr:
         else:
             self.gather_async(x_full)
 
+    def close(self) -> None:
+        """Release the peer buffers (exchange='p2p'); call on every rank."""
+        if self.peer is not None:
+            torch.cuda.synchronize(self.device)
+            if self.world > 1:
+                dist.barrier(group=self.group)  # no peer still stores into our buffers
+            self.peer.close()
+            self.peer = self.pstep = None
+
     def wait_gather(self) -> None:
         """Stream-order (NCCL) or complete (gloo) the outstanding exchange."""
         for w in self._pending:
@@ -314,6 +337,11 @@ class DistributedArgCsr:
     def power_iteration(self, x0: torch.Tensor, iters: int):
         """`iters` steps of x <- A x / ||A x||; returns (lambda, x) with
         lambda = ||A x_{iters-1}|| (x normalised), on every rank."""
+        if self.pstep is not None:
+            self.pstep.begin(x0)
+            for _ in range(iters):
+                self.pstep.step()
+            return self.pstep.finish()
         buf = [x0.clone(), torch.empty_like(x0)]
         scale = torch.ones(1, dtype=torch.float64, device=self.device)
         s2 = torch.zeros(1, dtype=torch.float64, device=self.device)

@@ -180,11 +180,11 @@ def test_skew_and_uniform_families(argcsr, orc, ref):  # acceptance.cpp:171-198
 
 
 # --------------------------------------------------------- larger / edge cases
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_TMA=1", "ARGCSR_HEAVY_TMA=2"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16"])
 @pytest.mark.parametrize("tpg,dcs", [(128, 1), (128, 4), (64, 2), (32, 1), (100, 1), (30, 3), (127, 1), (256, 1)])
 def test_powerlaw_heavy_groups(argcsr, orc, tpg, dcs, heavy, monkeypatch):
-    """Heavy-tailed rows: long-chunk (heavy) groups, multi-tile schedule, with
-    the register-staged and the TMA-staged heavy kernels."""
+    """Heavy-tailed rows: long-chunk (heavy) groups, multi-tile schedule,
+    through two heavy-kernel variants."""
     if heavy != "default":
         monkeypatch.setenv(*heavy.split("="))
     A = powerlaw_csr(40000, 30000, seed=tpg * 7 + dcs, heavy_rows=[(0, 25000), (777, 12000), (39999, 9000)])
@@ -243,7 +243,7 @@ def test_unsorted_columns_copied_in_stored_order(argcsr, orc):
 
 # ---------------------------------------------------------------- other APIs
 @pytest.mark.parametrize("layout", LAYOUTS)
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_TMA=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_RUNS=1"])
 def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout, heavy, monkeypatch):
     import torch
 
@@ -342,8 +342,7 @@ def test_torch_device_path(argcsr, orc):
         argcsr.spmv_torch(dev, x[:-1])
 
 
-HEAVY_VARIANTS = ["default", "ARGCSR_HEAVY_RUNS=1", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_U=4", "ARGCSR_HEAVY_B=5",
-                  "ARGCSR_HEAVY_TMA=1", "ARGCSR_HEAVY_TMA=2", "ARGCSR_HEAVY_TMA=3"]
+HEAVY_VARIANTS = ["default", "ARGCSR_HEAVY_RUNS=1", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_U=4", "ARGCSR_HEAVY_B=5"]
 
 
 @pytest.mark.parametrize("heavy", HEAVY_VARIANTS)

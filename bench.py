@@ -442,7 +442,10 @@ def run_b200(args):
     }
     if args.power_iteration:
         out["power_iteration"] = {"steps_total": args.warmup + args.steps, "lambda": pi_lambda,
-                                  "step": "SpMV + ||y||^2 all-reduce + all-gather of y + scaling fused into the next SpMV"}
+                                  "step": ("SpMV with y stored into every GPU's next x by its epilogue + ||y||^2 "
+                                           "partials and step flags over peer memory + scaling fused into the next SpMV"
+                                           if D.exchange == "p2p" else
+                                           "SpMV + ||y||^2 all-reduce + all-gather of y + scaling fused into the next SpMV")}
 
     if world == 1 and not args.power_iteration:
         # ------------------------------------------------ e2e through the C-ABI with host buffers

@@ -261,11 +261,13 @@ template <> __device__ __forceinline__ float to_out<float>(double v) { return __
 // Epilogue: y[row], and the same value into every peer's buffer (the fused
 // all-gather of the multi-GPU step: the y slice lands in the other GPUs' next
 // x directly from the kernel, as plain stores over the NVLink peer mapping).
-template <typename T>
+// (A template flag: the single-GPU kernels carry no peer code at all.)
+template <bool PEER, typename T>
 __device__ __forceinline__ void store_y(const SpmvArgs<T>& a, uint32_t row, double v) {
     const T o = to_out<T>(v);
     a.y[row] = o;
-    for (uint32_t q = 0; q < a.npeers; ++q) a.peer_y[q][row] = o;
+    if constexpr (PEER)
+        for (uint32_t q = 0; q < a.npeers; ++q) a.peer_y[q][row] = o;
 }
 
 // Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending.
@@ -287,7 +289,7 @@ __device__ __forceinline__ uint32_t find_le(const uint32_t* arr, uint32_t n, uin
 
 // Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
 // order, one lane per thread.
-template <typename T, int UH, bool RUNS, int MINB>
+template <typename T, int UH, bool RUNS, int MINB, bool PEER = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
         const uint32_t f = a.groups[g].first_row;
         const uint32_t row = f + (r - s_row0[i]);
         const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
-        store_y(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
+        store_y<PEER>(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
     }
 }
 
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
 // MAP: every unit and row of the tile gets its group index in shared memory
 // while the metadata loads (one thread per group, so only for small groups);
 // otherwise both phases binary-search the tile's group table.
-template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true>
+template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true, bool PEER = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -422,13 +424,13 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     }
     __syncthreads();
 
-    if (pvalid) store_y(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
+    if (pvalid) store_y<PEER>(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
     for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
         const uint32_t gi = MAP ? s_rgrp[r - row0] : find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
-        store_y(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
+        store_y<PEER>(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
     }
 }
 
@@ -560,13 +562,13 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const S
         uint32_t gs2 = 0, ge2 = 0;
         if (k2 < num_tiles) gs2 = a.tiles[k2], ge2 = a.tiles[k2 + 1];
 
-        if (pvalid) store_y(a, pr, row_sum(s_part + size_t(mub[pgi] - ub0) * V, pb, pe));
+        if (pvalid) store_y<false>(a, pr, row_sum(s_part + size_t(mub[pgi] - ub0) * V, pb, pe));
         for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
             const uint32_t gi = find_row(md, ng, r);
             const uint32_t g = gs + gi;
             if (md[gi].heavy() || g < a.g_begin || g >= a.g_end) continue;
             const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
-            store_y(a, r, row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
+            store_y<false>(a, r, row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
         }
         __syncthreads();
         k = kn, gs = gsn, ge = gen;
@@ -657,15 +659,16 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
-template <typename T, int V, int U, bool PRED, int MINB>
+template <typename T, int V, int U, bool PRED, int MINB, bool PEER = false>
 void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // small groups (units + rows per group, on average): fill the maps, else search
     const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
     const char* e = std::getenv("ARGCSR_MAP");  // experiments: force 1 / 0
     if (e ? e[0] == '1' : per_group <= 24.0)
-        launch(spmv_light_kernel<T, V, U, PRED, MINB, true>, m->num_tiles, light_smem_bytes(m, V, true), m, a, s);
+        launch(spmv_light_kernel<T, V, U, PRED, MINB, true, PEER>, m->num_tiles, light_smem_bytes(m, V, true), m, a,
+               s);
     else
-        launch(spmv_light_kernel<T, V, U, PRED, MINB, false>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
+        launch(spmv_light_kernel<T, V, U, PRED, MINB, false, PEER>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
 }
 
 template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
@@ -704,6 +707,10 @@ void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
 
 template <typename T, int V>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
+    if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
+        launch_light<T, V, 4, false, 5, true>(m, a, s);
+        return;
+    }
     int vid = variant_id();
     if (vid < 0) {
         // Default: hardware-dispatched tiles, unpredicated value loads, 5 CTAs
@@ -788,7 +795,10 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
         const char* hr = std::getenv("ARGCSR_HEAVY_RUNS");
         const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
         cudaStream_t hs = fork ? m->aux : s;
-        if (hr && hr[0] == '1' && aligned) {
+        if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
+            if (sizeof(T) == sizeof(float)) launch(spmv_heavy_kernel<T, 4, false, 6, true>, m->heavy_ctas, smem, m, a, hs);
+            else launch(spmv_heavy_kernel<T, 8, false, 4, true>, m->heavy_ctas, smem, m, a, hs);
+        } else if (hr && hr[0] == '1' && aligned) {
             if (uh && uh[0] == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
             else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
         } else if (uh && uh[0] == '1') {

@@ -338,8 +338,7 @@ def run_b200(args):
         ps2 = torch.zeros(1, dtype=torch.float64, device=dev)
 
         if D.pstep is not None:
-            if not args.power_iteration:
-                raise SystemExit("--exchange p2p is the power-iteration step (use --power-iteration)")
+            D.pstep.normalize = args.power_iteration  # else the iterated SpMV x <- A x
             D.pstep.begin(x)
 
         def step():

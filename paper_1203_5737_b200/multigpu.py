@@ -196,7 +196,7 @@ class DistributedArgCsr:
                 handles = [None] * self.world
                 dist.all_gather_object(handles, self.peer.handle, group=self.group)
                 self.peer.connect_ipc(handles)
-            self.pstep = PeerPowerIteration(self.engine, r0, r1, self.peer)
+            self.pstep = PeerPowerIteration(self.engine, r0, r1, self.peer)  # normalize toggled per use
             self.exchange = "p2p"
             return
         if self.overlap and exchange != "allgather":
@@ -338,6 +338,7 @@ class DistributedArgCsr:
         """`iters` steps of x <- A x / ||A x||; returns (lambda, x) with
         lambda = ||A x_{iters-1}|| (x normalised), on every rank."""
         if self.pstep is not None:
+            self.pstep.normalize = True
             self.pstep.begin(x0)
             for _ in range(iters):
                 self.pstep.step()

@@ -122,12 +122,14 @@ class PeerBuffers:
 
 
 class PeerPowerIteration:
-    """One rank's power iteration with the fused SpMV + peer-store exchange.
+    """One rank's power iteration with the fused SpMV + peer-store exchange
+    (normalize=False: the plain iterated SpMV x_{k+1} = A x_k, no norms).
 
     `engine` is the rank's DeviceEngine (its converted row slice [r0, r1))."""
 
-    def __init__(self, engine, r0: int, r1: int, bufs: PeerBuffers):
+    def __init__(self, engine, r0: int, r1: int, bufs: PeerBuffers, normalize: bool = True):
         self.engine, self.r0, self.r1, self.bufs = engine, r0, r1, bufs
+        self.normalize = normalize
         self.stream = engine.stream
         self.scale = torch.ones(1, dtype=torch.float64, device=bufs.device)
         self.k = 0
@@ -146,19 +148,26 @@ class PeerPowerIteration:
         nb = (k + 1) % 2
         bufs = self.bufs
         self.wait(k)
-        if k > 0:
+        if k > 0 and self.normalize:
             torch.reciprocal(torch.sqrt(bufs.partial[b].sum().reshape(1)), out=self.scale)
         y = bufs.x[nb][self.r0:self.r1]
-        self.engine.m.spmv_peer_device(bufs.x[b].data_ptr(), self.scale.data_ptr(), 0, self.engine.num_groups,
-                                       y.data_ptr(), bufs.peer_x(nb, self.r0), 0, self.stream.cuda_stream)
-        y64 = y.to(torch.float64)
+        self.engine.m.spmv_peer_device(bufs.x[b].data_ptr(), self.scale.data_ptr() if self.normalize else 0, 0,
+                                       self.engine.num_groups, y.data_ptr(), bufs.peer_x(nb, self.r0), 0,
+                                       self.stream.cuda_stream)
         own = bufs.partial[nb][bufs.rank:bufs.rank + 1]
-        own.copy_(torch.dot(y64, y64).reshape(1))
+        if self.normalize:
+            y64 = y.to(torch.float64)
+            own.copy_(torch.dot(y64, y64).reshape(1))
         if bufs.peers:
-            _ext.peer_signal(bufs.peer_flag_slots(), k + 1, own.data_ptr(), bufs.peer_partial_slots(nb),
-                             self.stream.cuda_stream)
+            _ext.peer_signal(bufs.peer_flag_slots(), k + 1, own.data_ptr() if self.normalize else 0,
+                             bufs.peer_partial_slots(nb) if self.normalize else [], self.stream.cuda_stream)
         bufs.flags[bufs.rank:bufs.rank + 1].fill_(k + 1)  # own slot: the wait covers all `world` slots
         self.k = k + 1
+
+    def current(self) -> torch.Tensor:
+        """x_k (after the wait for the peers' slices), this rank's buffer view."""
+        self.wait(self.k)
+        return self.bufs.x[self.k % 2]
 
     def finish(self):
         """(lambda, x): lambda = ||A x_{k-1}|| and the normalised last x."""
@@ -171,23 +180,24 @@ class PeerPowerIteration:
 
 
 def power_iteration_local(engines: Sequence, bounds: Sequence[int], num_cols: int, x0: torch.Tensor, iters: int,
-                          dtype: torch.dtype = torch.float64):
+                          dtype: torch.dtype = torch.float64, normalize: bool = True):
     """P virtual ranks on ONE device (tests): each rank's engine, the peer
-    protocol with plain device pointers, steps interleaved rank by rank."""
+    protocol with plain device pointers, steps interleaved rank by rank.
+    Returns per rank (lambda, x) -- or x_iters (a copy) when not normalize."""
     P = len(engines)
     dev = x0.device
     bufs = [PeerBuffers(p, P, num_cols, dtype, dev) for p in range(P)]
     for b in bufs:
         b.connect_local(bufs)
-    runs = [PeerPowerIteration(engines[p], int(bounds[p]), int(bounds[p + 1]), bufs[p]) for p in range(P)]
+    runs = [PeerPowerIteration(engines[p], int(bounds[p]), int(bounds[p + 1]), bufs[p], normalize)
+            for p in range(P)]
     try:
         for r in runs:
             r.begin(x0)
         for _ in range(iters):
             for r in runs:
                 r.step()
-        out = [r.finish() for r in runs]
-        return out
+        return [r.finish() if normalize else r.current().clone() for r in runs]
     finally:
         torch.cuda.synchronize(dev)
         for b in bufs:

@@ -75,6 +75,31 @@ def test_peer_power_iteration_virtual_ranks(kind, P):
         assert bits(x) == bits(xs[0])
 
 
+@pytest.mark.parametrize("P", [2, 3])
+def test_peer_iterated_spmv_virtual_ranks(orc, P):
+    """normalize=False: x_{k+1} = A x_k assembled on every rank; each step's
+    slices are the oracle's SpMV of that rank's slice conversion, bit for bit."""
+    from paper_1203_5737_b200.multigpu import slice_rows
+    from paper_1203_5737_b200.peer import power_iteration_local
+    import oracle
+
+    A = powerlaw_csr(5000, 5000, seed=8, heavy_rows=[(9, 3000)])
+    A.values[:] = A.values / np.abs(A.values).sum() * 50  # keep x bounded over the steps
+    b, engs = _engines(A, P)
+    x0 = np.linspace(-1, 1, A.num_cols)
+    out = power_iteration_local(engs, b, A.num_cols, torch.from_numpy(x0).cuda(), 4, normalize=False)
+    x = x0.copy()
+    refs = []
+    for p in range(P):
+        sl = slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1]))
+        refs.append(orc.argcsr_from_csr(oracle.Csr(sl.num_rows, A.num_cols, np.asarray(sl.row_pointers, np.uint64),
+                                                   np.asarray(sl.columns, np.int32), np.asarray(sl.values)), 128, 1))
+    for _ in range(4):
+        x = np.concatenate([orc.spmv_argcsr(M, x) for M in refs])
+    for xr in out:
+        assert bits(xr.cpu().numpy()) == bits(x)
+
+
 def _ipc_worker(rank, world, port, kind, out_dir):
     try:
         sys.path.insert(0, str(ROOT))

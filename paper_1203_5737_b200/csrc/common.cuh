@@ -84,6 +84,7 @@ struct argcsr_dev {
     argcsr_dtype dtype = ARGCSR_F64;
     uint64_t num_rows = 0, num_cols = 0, nnz = 0, tpg = 0, dcs = 0;
     uint64_t num_groups = 0, total_slots = 0, max_chunk = 0;
+    uint32_t max_light_chunk = 0;         // largest chunk_size among the short-chunk (light) groups
     int layout = argcsr_gpu::kLayoutCompact;
     uint64_t stored_slots = 0;            // length of values/columns (== total_slots in the reference layout)
     bool tm16 = true;  // threads_mapping / assigned stored as u16 (tpg <= 65535)

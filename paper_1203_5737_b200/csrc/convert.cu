@@ -383,13 +383,20 @@ __global__ void k4_max_tile_groups(const uint32_t* __restrict__ tiles, uint32_t 
     }
 }
 
+// out[0] = max chunk_size, out[1] = max chunk_size of the light (short-chunk) groups
 __global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, unsigned long long* __restrict__ out) {
-    uint64_t m = 0;
+    uint64_t m = 0, ml = 0;
     for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G;
-         g += uint64_t(gridDim.x) * blockDim.x)
+         g += uint64_t(gridDim.x) * blockDim.x) {
         m = max(m, uint64_t(chunk[g]));
+        if (chunk[g] <= kHeavyChunk) ml = max(ml, uint64_t(chunk[g]));
+    }
     m = warp_max_u64(m);
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+    ml = warp_max_u64(ml);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out, (unsigned long long)m);
+        atomicMax(out + 1, (unsigned long long)ml);
+    }
 }
 
 // Largest column each light tile reads (padding -1 ignored): for the
@@ -721,14 +728,15 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
                                                                   heavy_of, G, N32, m->groups);
     LAUNCH_OK("k4_fill_desc");
     {
-        DevPtr<unsigned long long> mx(1, s);
-        CUDA_OK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), s));
+        DevPtr<unsigned long long> mx(2, s);
+        CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
         k4_max_chunk<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, G, mx.p);
         LAUNCH_OK("k4_max_chunk");
-        unsigned long long mc = 0;
-        CUDA_OK(cudaMemcpyAsync(&mc, mx.p, sizeof mc, cudaMemcpyDeviceToHost, s));
+        unsigned long long mc[2] = {0, 0};
+        CUDA_OK(cudaMemcpyAsync(mc, mx.p, sizeof mc, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
-        m->max_chunk = mc;
+        m->max_chunk = mc[0];
+        m->max_light_chunk = uint32_t(mc[1]);
     }
     m->total_slots = total_slots;
     m->stored_slots = stored_slots;

@@ -254,6 +254,55 @@ __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uin
     }
 }
 
+// Phase 1 for a thread's two units when every light chunk of the matrix is
+// <= H: both units' element steps are issued in ONE batch (columns, values,
+// then all gathers) -- the register footprint of one unit with 2H steps, half
+// the round trips of walking the units one after the other.  Per lane the
+// products are added in j order: bit-identical to phase1.
+template <typename T, int V, int H>
+__device__ __forceinline__ void phase1_pair(const SpmvArgs<T>& a, const uint64_t (&slot)[2], const uint32_t (&ch)[2],
+                                            const uint32_t (&st)[2], double (&s)[2][V], uint64_t pol_stream,
+                                            uint64_t pol_x, double xs) {
+    int c[2][H][V];
+    T v[2][H][V];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            if (uint32_t(h) < ch[k]) {
+                ld_cols<V>(a.cols + slot[k] + uint64_t(h) * st[k], c[k][h], pol_stream);
+                ld_vals<V>(a.vals + slot[k] + uint64_t(h) * st[k], v[k][h], pol_stream);
+            } else {
+#pragma unroll
+                for (int l = 0; l < V; ++l) c[k][h][l] = -1, v[k][h][l] = T(0);
+            }
+        }
+    double xv[2][H][V];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int l = 0; l < V; ++l) xv[k][h][l] = c[k][h][l] != -1 ? ld_x(a.x + c[k][h][l], pol_x) : 0.0;
+    if (a.x_scale) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+                for (int l = 0; l < V; ++l) xv[k][h][l] = __dmul_rn(xv[k][h][l], xs);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int l = 0; l < V; ++l) {
+            s[k][l] = 0.0;
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+                if (c[k][h][l] != -1) s[k][l] = __dadd_rn(s[k][l], __dmul_rn(double(v[k][h][l]), xv[k][h][l]));
+        }
+}
+
 template <typename T> __device__ __forceinline__ T to_out(double v);
 template <> __device__ __forceinline__ double to_out<double>(double v) { return v; }
 template <> __device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
@@ -340,7 +389,9 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
 // MAP: every unit and row of the tile gets its group index in shared memory
 // while the metadata loads (one thread per group, so only for small groups);
 // otherwise both phases binary-search the tile's group table.
-template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true, bool PEER = false>
+// PAIR (launched when every light chunk is <= U/2 and a tile has at most two
+// units per thread): each thread's two units go through phase1_pair.
+template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true, bool PEER = false, bool PAIR = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -406,7 +457,33 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     }
 
     const uint32_t nunits = s_ub[ng];
-    for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) {
+    if constexpr (PAIR) {
+        uint64_t slot[2] = {0, 0};
+        uint32_t ch[2] = {0, 0}, st[2] = {0, 0};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t u = threadIdx.x + k * blockDim.x;
+            if (u >= nunits) continue;
+            const uint32_t gi = MAP ? s_ugrp[u] : find_le(s_ub, ng, u);
+            const uint32_t g = gs + gi;
+            const uint64_t os = s_off[gi];
+            if ((os & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
+            slot[k] = (os & kOffsetMask) + (u - s_ub[gi]) * V;
+            st[k] = uint32_t((os >> 48) & 0x7FFF);
+            ch[k] = min(s_chunk[gi], ulen2[k]);
+        }
+        double sp[2][V];
+        phase1_pair<T, V, U / 2>(a, slot, ch, st, sp, pol_stream, pol_x, xs);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t u = threadIdx.x + k * blockDim.x;
+            if (u < nunits) {
+#pragma unroll
+                for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = sp[k][l];
+            }
+        }
+    }
+    for (uint32_t u = threadIdx.x; !PAIR && u < nunits; u += blockDim.x) {
         const uint32_t gi = MAP ? s_ugrp[u] : find_le(s_ub, ng, u);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
@@ -664,11 +741,24 @@ void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // small groups (units + rows per group, on average): fill the maps, else search
     const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
     const char* e = std::getenv("ARGCSR_MAP");  // experiments: force 1 / 0
-    if (e ? e[0] == '1' : per_group <= 24.0)
+    const bool map = e ? e[0] == '1' : per_group <= 24.0;
+    // every light chunk <= U/2 and at most two units per thread: pair them
+    const char* pe = std::getenv("ARGCSR_PAIR");  // experiments: 0 = never
+    const bool pair = !(pe && pe[0] == '0') && m->max_light_chunk <= uint32_t(U / 2) &&
+                      m->max_tile_units <= 2 * uint64_t(kTileThreads);
+    if (pair) {  // (twice the loads in flight per thread: 64 registers, 4 CTAs/SM)
+        if (map)
+            launch(spmv_light_kernel<T, V, U, PRED, 4, true, PEER, true>, m->num_tiles, light_smem_bytes(m, V, true), m,
+                   a, s);
+        else
+            launch(spmv_light_kernel<T, V, U, PRED, 4, false, PEER, true>, m->num_tiles, light_smem_bytes(m, V), m, a,
+                   s);
+    } else if (map) {
         launch(spmv_light_kernel<T, V, U, PRED, MINB, true, PEER>, m->num_tiles, light_smem_bytes(m, V, true), m, a,
                s);
-    else
+    } else {
         launch(spmv_light_kernel<T, V, U, PRED, MINB, false, PEER>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
+    }
 }
 
 template <typename T, int V, int U, bool PRED, int MINB, bool DYN>

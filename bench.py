@@ -459,13 +459,30 @@ def run_b200(args):
         t = time.perf_counter()
         for _ in range(e2e_steps):
             m.spmv_host_staged(xh.data_ptr(), xd.data_ptr(), yd.data_ptr(), yh.data_ptr(), stream.cuda_stream)
+        sync_s = (time.perf_counter() - t) / e2e_steps
+        # A stream of SpMVs from host memory through the non-blocking C-ABI call:
+        # every step uploads its x and downloads its y (two alternating pinned
+        # y buffers); step i+1's upload overlaps step i's SpMV and step i-1's
+        # download (the handle double-buffers its device staging).
+        yh2 = [yh, torch.empty_like(yh, pin_memory=True)]
+        for i in range(3):
+            m.spmv_host_async(xh.data_ptr(), yh2[i % 2].data_ptr(), stream.cuda_stream)
+        m.host_wait()
+        t = time.perf_counter()
+        for i in range(e2e_steps):
+            m.spmv_host_async(xh.data_ptr(), yh2[i % 2].data_ptr(), stream.cuda_stream)
+        m.host_wait()
         e2e_s = (time.perf_counter() - t) / e2e_steps
         out["e2e"] = {"value": round(2.0 * nnz_total / e2e_s / 1e9, 3), "unit": "GFLOP/s",
                       "h2d_bytes_per_step": A.num_cols * sv, "d2h_bytes_per_step": A.num_rows * sv,
                       "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
-                      "path": "argcsr_dev_spmv_host_staged: pinned host x -> H2D in 8 pieces (copy engine 1) -> "
-                              "light-tile chunks launched as their x window lands -> D2H of y chunks (copy "
-                              "engine 2) -> sync; one-shot when the matrix has heavy groups or the x remap"}
+                      "path": "argcsr_dev_spmv_host_async per step (pinned host x -> H2D on copy engine 1 -> SpMV "
+                              "-> D2H into alternating pinned y buffers on copy engine 2), argcsr_dev_host_wait "
+                              "after the last step; consecutive steps overlap",
+                      "single_call": {"value": round(2.0 * nnz_total / sync_s / 1e9, 3), "ms_per_step": sync_s * 1e3,
+                                      "path": "argcsr_dev_spmv_host_staged, synchronous per call: x up in 8 "
+                                              "pieces, light-tile chunks launched as their x window lands, y "
+                                              "chunks down meanwhile; one-shot with heavy groups or the x remap"}}
         out["gpu_launches"] = launches
 
         if not args.no_variants:

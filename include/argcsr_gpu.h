@@ -221,6 +221,18 @@ ARGCSR_API argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x
 ARGCSR_API argcsr_status argcsr_dev_spmv_host_staged(const argcsr_dev* m, const void* x_host, void* x_dev,
                                           void* y_dev, void* y_host, void* stream);
 
+/* Non-blocking host-buffer SpMV for a stream of vectors: uploads x_host
+ * (num_cols entries, pinned for a true async copy) on one copy engine,
+ * multiplies on `stream`, downloads y (num_rows entries) into y_host on the
+ * other copy engine, and returns at once.  The handle double-buffers its own
+ * device staging, so call i+1's upload overlaps call i's SpMV and call i-1's
+ * download.  x_host must stay unmodified and y_host untouched until
+ * argcsr_dev_host_wait(m) returns (every earlier call is then complete).
+ * One host thread drives a handle's async calls. */
+ARGCSR_API argcsr_status argcsr_dev_spmv_host_async(const argcsr_dev* m, const void* x_host, void* y_host,
+                                                    void* stream);
+ARGCSR_API argcsr_status argcsr_dev_host_wait(const argcsr_dev* m);
+
 /* ----------------------------------------------------------- accessors / next */
 
 /* csr_from_argcsr (argcsr.cpp:157-183) on the device: writes the lossless CSR

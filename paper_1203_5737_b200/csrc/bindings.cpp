@@ -546,6 +546,17 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
                                                    reinterpret_cast<void*>(yh), reinterpret_cast<void*>(stream)));
              },
              py::arg("x_host_ptr"), py::arg("x_dev_ptr"), py::arg("y_dev_ptr"), py::arg("y_host_ptr"), py::arg("stream") = 0)
+        .def("spmv_host_async",
+             [](const PyArgCsr& p, std::uintptr_t xh, std::uintptr_t yh, std::uintptr_t stream) {
+                 check(argcsr_dev_spmv_host_async(p.dev->handle(), reinterpret_cast<const void*>(xh),
+                                                  reinterpret_cast<void*>(yh), reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_host_ptr"), py::arg("y_host_ptr"), py::arg("stream") = 0)
+        .def("host_wait",
+             [](const PyArgCsr& p) {
+                 py::gil_scoped_release nogil;
+                 check(argcsr_dev_host_wait(p.dev->handle()));
+             })
         .def("free", [](PyArgCsr& p) { p.dev->reset(); })
         .def("__eq__", [](const PyArgCsr& a, const PyArgCsr& b) {
             if (a.info().num_rows != b.info().num_rows || a.info().num_cols != b.info().num_cols ||

@@ -81,6 +81,13 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->perm);
     cudaFree(m->xbuf);
     if (m->aux) cudaStreamDestroy(m->aux);
+    for (int b = 0; b < 2; ++b) {
+        if (m->as_x[b]) cudaFree(m->as_x[b]);
+        if (m->as_y[b]) cudaFree(m->as_y[b]);
+        if (m->as_up[b]) cudaEventDestroy(m->as_up[b]);
+        if (m->as_mv[b]) cudaEventDestroy(m->as_mv[b]);
+        if (m->as_down[b]) cudaEventDestroy(m->as_down[b]);
+    }
     if (m->h2d) cudaStreamDestroy(m->h2d);
     if (m->d2h) cudaStreamDestroy(m->d2h);
     for (int i = 0; i < 8; ++i) {
@@ -503,6 +510,51 @@ argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x, uint64_t 
         argcsr_gpu::spmv_launch(m, dx, dy, 0, m->num_groups, s);
         CUDA_OK(cudaMemcpyAsync(y, dy, m->num_rows * es, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
+    });
+}
+
+argcsr_status argcsr_dev_spmv_host_async(const argcsr_dev* mc, const void* x_host, void* y_host, void* stream) {
+    return guarded([&] {
+        check_handle(mc);
+        if ((!x_host && mc->num_cols) || (!y_host && mc->num_rows))
+            fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_host_async: null buffer");
+        DeviceScope scope(mc->device);
+        // The staging and its events are handle state (like the copy streams):
+        // one thread drives a handle's async calls.
+        argcsr_dev* m = const_cast<argcsr_dev*>(mc);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t es = elem_size(m->dtype);
+        const int b = int(m->as_calls & 1);
+        if (!m->as_x[b]) {
+            CUDA_OK(cudaMalloc(&m->as_x[b], std::max<uint64_t>(m->num_cols, 1) * es));
+            CUDA_OK(cudaMalloc(&m->as_y[b], std::max<uint64_t>(m->num_rows, 1) * es));
+            CUDA_OK(cudaEventCreateWithFlags(&m->as_up[b], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&m->as_mv[b], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&m->as_down[b], cudaEventDisableTiming));
+        }
+        // upload (copy engine 1) once the SpMV that last read this x buffer is done
+        if (m->as_used[b]) CUDA_OK(cudaStreamWaitEvent(m->h2d, m->as_mv[b], 0));
+        CUDA_OK(cudaMemcpyAsync(m->as_x[b], x_host, m->num_cols * es, cudaMemcpyHostToDevice, m->h2d));
+        CUDA_OK(cudaEventRecord(m->as_up[b], m->h2d));
+        // multiply on the caller's stream once x is up and this y buffer is downloaded
+        CUDA_OK(cudaStreamWaitEvent(s, m->as_up[b], 0));
+        if (m->as_used[b]) CUDA_OK(cudaStreamWaitEvent(s, m->as_down[b], 0));
+        argcsr_gpu::spmv_launch(m, m->as_x[b], m->as_y[b], 0, m->num_groups, s);
+        CUDA_OK(cudaEventRecord(m->as_mv[b], s));
+        // download (copy engine 2)
+        CUDA_OK(cudaStreamWaitEvent(m->d2h, m->as_mv[b], 0));
+        CUDA_OK(cudaMemcpyAsync(y_host, m->as_y[b], m->num_rows * es, cudaMemcpyDeviceToHost, m->d2h));
+        CUDA_OK(cudaEventRecord(m->as_down[b], m->d2h));
+        m->as_used[b] = true;
+        ++m->as_calls;
+    });
+}
+
+argcsr_status argcsr_dev_host_wait(const argcsr_dev* m) {
+    return guarded([&] {
+        check_handle(m);
+        DeviceScope scope(m->device);
+        CUDA_OK(cudaStreamSynchronize(m->d2h));  // the last download follows every earlier stage
     });
 }
 

@@ -112,7 +112,13 @@ struct argcsr_dev {
     // largest stored column used by tiles 0..t (running max) and its first row
     std::vector<uint32_t> tile_cmax, tile_row;
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t ev_x[8] = {}, ev_c[8] = {};           // rows of the largest light tile (heavy groups' rows included)
+    cudaEvent_t ev_x[8] = {}, ev_c[8] = {};
+    // asynchronous host SpMV (argcsr_dev_spmv_host_async): handle-owned
+    // double-buffered device staging; slot b's events order buffer reuse
+    void* as_x[2] = {}, *as_y[2] = {};
+    cudaEvent_t as_up[2] = {}, as_mv[2] = {}, as_down[2] = {};
+    bool as_used[2] = {};
+    uint64_t as_calls = 0;           // rows of the largest light tile (heavy groups' rows included)
     uint64_t tile_span = 0;               // units between consecutive tile keys
     uint32_t tile_threads = 256;          // tiles were built for this CTA size
     uint64_t max_tile_units = 0;          // tile_span + ceil(tpg / V) - 1

@@ -420,3 +420,26 @@ def test_unit_lengths_forced(argcsr, orc, corpus, monkeypatch, ulen):
             assert dev.unit_len_bytes == 0
         elif A.nnz:
             assert dev.unit_len_bytes > 0
+
+
+@pytest.mark.parametrize("kind", ["stencil", "powerlaw", "remap"])
+def test_host_async_stream(argcsr, orc, kind):
+    """argcsr_dev_spmv_host_async: a stream of calls with different x and y
+    host buffers, overlapped through the handle's double-buffered staging;
+    after argcsr_dev_host_wait every y is the oracle's, bit for bit."""
+    import torch
+
+    if kind == "stencil":
+        A = stencil27(12)
+    else:
+        A = powerlaw_csr(20000, 20000, seed=21, heavy_rows=[(4, 9000)])
+    dev = to_dev(argcsr, A, 128, 1, layout=("compact", "on") if kind == "remap" else "compact")
+    ref_m = orc.argcsr_from_csr(A, 128, 1)
+    xs = [torch.from_numpy(np.cos(np.arange(A.num_cols) * (0.1 + i))).pin_memory() for i in range(5)]
+    ys = [torch.empty(A.num_rows, dtype=torch.float64).pin_memory() for _ in range(5)]
+    s = torch.cuda.current_stream().cuda_stream
+    for x, y in zip(xs, ys):
+        dev.spmv_host_async(x.data_ptr(), y.data_ptr(), s)
+    dev.host_wait()
+    for x, y in zip(xs, ys):
+        assert bits(y.numpy()) == bits(orc.spmv_argcsr(ref_m, x.numpy()))

@@ -188,11 +188,13 @@ ARGCSR_API argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, 
  * (npeers <= 7) -- the other GPUs' next-x buffers seen through NVLink peer
  * mappings (argcsr_peer_open), pre-offset by this slice's first row -- so the
  * y slice reaches every GPU tile by tile while the SpMV runs, with no separate
- * collective.  Otherwise argcsr_dev_spmv_ex. */
+ * collective.  peer_rows (2 * npeers entries, may be NULL = all rows) limits
+ * peer q to rows [peer_rows[2q], peer_rows[2q+1]): the rows its columns read
+ * (a halo for banded matrices).  Otherwise argcsr_dev_spmv_ex. */
 ARGCSR_API argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const double* x_scale,
                                               uint64_t group_begin, uint64_t group_end, void* y,
-                                              void* const* peer_y, uint32_t npeers, uint32_t flags,
-                                              void* stream);
+                                              void* const* peer_y, uint32_t npeers, const uint64_t* peer_rows,
+                                              uint32_t flags, void* stream);
 
 /* Step signalling, stream-ordered one-thread kernels: store `value` into
  * *flags[q] for q < n with system-scope release semantics (after copying the

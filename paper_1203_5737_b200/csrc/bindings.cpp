@@ -512,15 +512,20 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
              py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
         .def("spmv_peer_device",
              [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uint64_t gb, std::uint64_t ge,
-                std::uintptr_t y, const std::vector<std::uintptr_t>& peers, std::uint32_t flags, std::uintptr_t stream) {
+                std::uintptr_t y, const std::vector<std::uintptr_t>& peers, const std::vector<std::uint64_t>& rows,
+                std::uint32_t flags, std::uintptr_t stream) {
+                 if (!rows.empty() && rows.size() != 2 * peers.size())
+                     throw ParameterError("spmv_peer_device: one [lo, hi) row range per peer");
                  std::vector<void*> pp(peers.size());
                  for (size_t i = 0; i < peers.size(); ++i) pp[i] = reinterpret_cast<void*>(peers[i]);
                  check(argcsr_dev_spmv_peer(p.dev->handle(), reinterpret_cast<const void*>(x),
                                             reinterpret_cast<const double*>(scale), gb, ge, reinterpret_cast<void*>(y),
-                                            pp.data(), uint32_t(pp.size()), flags, reinterpret_cast<void*>(stream)));
+                                            pp.data(), uint32_t(pp.size()), rows.empty() ? nullptr : rows.data(),
+                                            flags, reinterpret_cast<void*>(stream)));
              },
              py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("group_begin"), py::arg("group_end"), py::arg("y_ptr"),
-             py::arg("peer_y_ptrs"), py::arg("flags") = 0u, py::arg("stream") = 0)
+             py::arg("peer_y_ptrs"), py::arg("peer_rows") = std::vector<std::uint64_t>{}, py::arg("flags") = 0u,
+             py::arg("stream") = 0)
         .def("spmv_ex_device",
              [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uint64_t gb, std::uint64_t ge,
                 std::uintptr_t y, std::uint32_t flags, std::uintptr_t stream) {

@@ -413,8 +413,8 @@ argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, const doubl
 }
 
 argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const double* x_scale, uint64_t group_begin,
-                                   uint64_t group_end, void* y, void* const* peer_y, uint32_t npeers, uint32_t flags,
-                                   void* stream) {
+                                   uint64_t group_end, void* y, void* const* peer_y, uint32_t npeers,
+                                   const uint64_t* peer_rows, uint32_t flags, void* stream) {
     return guarded([&] {
         check_handle(m);
         if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null vector");
@@ -425,7 +425,7 @@ argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const dou
             if (!peer_y[q]) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null peer buffer");
         DeviceScope scope(m->device);
         argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream), x_scale,
-                                (flags & ARGCSR_SPMV_REUSE_X) != 0, peer_y, npeers);
+                                (flags & ARGCSR_SPMV_REUSE_X) != 0, peer_y, npeers, peer_rows);
     });
 }
 

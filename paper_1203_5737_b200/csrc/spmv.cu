@@ -59,8 +59,9 @@ struct SpmvArgs {
     const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
-    uint32_t npeers;         // multi-GPU epilogue: every y row is also stored to peer_y[q][row]
-    T* peer_y[kMaxPeers];    // (other GPUs' x buffers through NVLink peer mappings, pre-offset)
+    uint32_t npeers;         // multi-GPU epilogue: y rows in [peer_lo[q], peer_hi[q]) are also stored
+    T* peer_y[kMaxPeers];    // to peer_y[q][row] (other GPUs' x buffers via NVLink peer mappings, pre-offset)
+    uint32_t peer_lo[kMaxPeers], peer_hi[kMaxPeers];
 };
 
 // ------------------------------------------------------------ cache policies
@@ -316,7 +317,8 @@ __device__ __forceinline__ void store_y(const SpmvArgs<T>& a, uint32_t row, doub
     const T o = to_out<T>(v);
     a.y[row] = o;
     if constexpr (PEER)
-        for (uint32_t q = 0; q < a.npeers; ++q) a.peer_y[q][row] = o;
+        for (uint32_t q = 0; q < a.npeers; ++q)
+            if (row >= a.peer_lo[q] && row < a.peer_hi[q]) a.peer_y[q][row] = o;
 }
 
 // Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending.
@@ -837,10 +839,15 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
 
 template <typename T>
 void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, void* y, uint32_t gb, uint32_t ge,
-                  cudaStream_t s, void* const* peer_y, uint32_t npeers) {
+                  cudaStream_t s, void* const* peer_y, uint32_t npeers, const uint64_t* peer_rows) {
     SpmvArgs<T> a{};
     a.npeers = npeers;
-    for (uint32_t q = 0; q < npeers; ++q) a.peer_y[q] = static_cast<T*>(peer_y[q]);
+    for (uint32_t q = 0; q < npeers; ++q) {
+        a.peer_y[q] = static_cast<T*>(peer_y[q]);
+        a.peer_lo[q] = peer_rows ? uint32_t(std::min<uint64_t>(peer_rows[2 * q], m->num_rows)) : 0u;
+        a.peer_hi[q] = peer_rows ? uint32_t(std::min<uint64_t>(peer_rows[2 * q + 1], m->num_rows))
+                                 : uint32_t(m->num_rows);
+    }
     a.x_scale = x_scale;
     a.vals = static_cast<const T*>(m->values);
     a.cols = m->columns;
@@ -958,13 +965,14 @@ void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0,
 }
 
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale, bool reuse_x, void* const* peer_y, uint32_t npeers) {
+                 cudaStream_t s, const double* x_scale, bool reuse_x, void* const* peer_y, uint32_t npeers,
+                 const uint64_t* peer_rows) {
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
     x = reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
-    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s, peer_y, npeers);
-    else launch_dtype<float>(m, x, x_scale, y, gb, ge, s, peer_y, npeers);
+    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s, peer_y, npeers, peer_rows);
+    else launch_dtype<float>(m, x, x_scale, y, gb, ge, s, peer_y, npeers, peer_rows);
 }
 
 // ------------------------------------------------ multi-GPU step signalling

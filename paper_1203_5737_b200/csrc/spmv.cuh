@@ -12,11 +12,13 @@ namespace argcsr_gpu {
 // scaling x first; 1.0 is an exact no-op.
 // reuse_x: an x remap handle skips its x' gather and reuses the x' of the
 // previous launch on this handle (same x, stream-ordered after it).
-// peer_y[0 .. npeers): every row written to y is also stored to peer_y[q][row]
-// (multi-GPU: the other GPUs' x buffers, pre-offset by this slice's first row).
+// peer_y[0 .. npeers): every row written to y that lies in
+// [peer_rows[2q], peer_rows[2q+1]) (all rows when peer_rows is null) is also
+// stored to peer_y[q][row] (multi-GPU: the other GPUs' x buffers, pre-offset
+// by this slice's first row; the ranges are the rows each peer reads).
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
                  cudaStream_t s, const double* x_scale = nullptr, bool reuse_x = false,
-                 void* const* peer_y = nullptr, uint32_t npeers = 0);
+                 void* const* peer_y = nullptr, uint32_t npeers = 0, const uint64_t* peer_rows = nullptr);
 
 // Step signalling between the GPUs of a multi-GPU step (spmv.cu): store
 // `value` into flags[q] (system-scope release, after *partial is copied to

@@ -191,12 +191,19 @@ class DistributedArgCsr:
             from .peer import PeerBuffers, PeerPowerIteration
 
             self.overlap = False
+            from .peer import needed_ranges
+
             self.peer = PeerBuffers(self.rank, self.world, num_cols, dtype, self.device)
+            send = None
             if self.world > 1:
                 handles = [None] * self.world
                 dist.all_gather_object(handles, self.peer.handle, group=self.group)
                 self.peer.connect_ipc(handles)
-            self.pstep = PeerPowerIteration(self.engine, r0, r1, self.peer)  # normalize toggled per use
+                # rows each peer reads from this rank (its columns in our row range)
+                need = [None] * self.world
+                dist.all_gather_object(need, needed_ranges(self.slice.columns, self.bounds), group=self.group)
+                send = {q: tuple(need[q][self.rank]) for q in range(self.world) if q != self.rank}
+            self.pstep = PeerPowerIteration(self.engine, r0, r1, self.peer, send_ranges=send)
             self.exchange = "p2p"
             return
         if self.overlap and exchange != "allgather":
@@ -340,8 +347,8 @@ class DistributedArgCsr:
         if self.pstep is not None:
             self.pstep.normalize = True
             self.pstep.begin(x0)
-            for _ in range(iters):
-                self.pstep.step()
+            for i in range(iters):
+                self.pstep.step(full=i == iters - 1)  # halo stores, the last step assembles all of x
             return self.pstep.finish()
         buf = [x0.clone(), torch.empty_like(x0)]
         scale = torch.ones(1, dtype=torch.float64, device=self.device)

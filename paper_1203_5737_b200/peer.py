@@ -58,6 +58,20 @@ def _view(ptr: int, n: int, dtype: torch.dtype, device: torch.device) -> torch.T
     return torch.as_tensor(_DevArray(ptr, n, dtype), device=device)
 
 
+def needed_ranges(columns, bounds) -> np.ndarray:
+    """[world, 2]: for each owner p, the global rows [lo, hi) of p's slice that
+    `columns` (this rank's slice) reference; (0, 0) when none.  A rank sends
+    peer q only rows in q's range for it (a halo for banded matrices)."""
+    c = torch.as_tensor(np.asarray(columns) if isinstance(columns, np.ndarray) else columns).to(torch.int64)
+    b = np.asarray(bounds, dtype=np.int64)
+    out = np.zeros((b.size - 1, 2), dtype=np.int64)
+    for p in range(b.size - 1):
+        sel = c[(c >= int(b[p])) & (c < int(b[p + 1]))]
+        if sel.numel():
+            out[p] = (int(sel.min()), int(sel.max()) + 1)
+    return out
+
+
 class PeerBuffers:
     """One rank's shared buffers (layout in the module docstring) and the
     device addresses of every peer's copy of them."""
@@ -127,9 +141,17 @@ class PeerPowerIteration:
 
     `engine` is the rank's DeviceEngine (its converted row slice [r0, r1))."""
 
-    def __init__(self, engine, r0: int, r1: int, bufs: PeerBuffers, normalize: bool = True):
+    def __init__(self, engine, r0: int, r1: int, bufs: PeerBuffers, normalize: bool = True,
+                 send_ranges: Optional[dict] = None):
         self.engine, self.r0, self.r1, self.bufs = engine, r0, r1, bufs
         self.normalize = normalize
+        # rows (local to the slice) each peer reads from this rank: q -> (lo, hi)
+        self.peer_rows = []
+        if send_ranges is not None:
+            for q in bufs.peers:
+                lo, hi = send_ranges[q]
+                lo, hi = (lo - r0, hi - r0) if hi > lo else (0, 0)
+                self.peer_rows += [max(lo, 0), max(hi, 0)]
         self.stream = engine.stream
         self.scale = torch.ones(1, dtype=torch.float64, device=bufs.device)
         self.k = 0
@@ -143,7 +165,10 @@ class PeerPowerIteration:
         if self.bufs.peers and k > 0:
             _ext.peer_wait(self.bufs.flags.data_ptr(), self.bufs.world, k, self.stream.cuda_stream)
 
-    def step(self) -> None:
+    def step(self, full: bool = False) -> None:
+        """One step; `full` stores every row into every peer (the last step of
+        a run, so that all GPUs end with the whole x), else only the rows each
+        peer reads."""
         k, b = self.k, self.k % 2
         nb = (k + 1) % 2
         bufs = self.bufs
@@ -152,8 +177,8 @@ class PeerPowerIteration:
             torch.reciprocal(torch.sqrt(bufs.partial[b].sum().reshape(1)), out=self.scale)
         y = bufs.x[nb][self.r0:self.r1]
         self.engine.m.spmv_peer_device(bufs.x[b].data_ptr(), self.scale.data_ptr() if self.normalize else 0, 0,
-                                       self.engine.num_groups, y.data_ptr(), bufs.peer_x(nb, self.r0), 0,
-                                       self.stream.cuda_stream)
+                                       self.engine.num_groups, y.data_ptr(), bufs.peer_x(nb, self.r0),
+                                       [] if full else self.peer_rows, 0, self.stream.cuda_stream)
         own = bufs.partial[nb][bufs.rank:bufs.rank + 1]
         if self.normalize:
             y64 = y.to(torch.float64)
@@ -180,23 +205,28 @@ class PeerPowerIteration:
 
 
 def power_iteration_local(engines: Sequence, bounds: Sequence[int], num_cols: int, x0: torch.Tensor, iters: int,
-                          dtype: torch.dtype = torch.float64, normalize: bool = True):
+                          dtype: torch.dtype = torch.float64, normalize: bool = True,
+                          slice_columns: Optional[Sequence] = None):
     """P virtual ranks on ONE device (tests): each rank's engine, the peer
-    protocol with plain device pointers, steps interleaved rank by rank.
-    Returns per rank (lambda, x) -- or x_iters (a copy) when not normalize."""
+    protocol with plain device pointers, steps interleaved rank by rank
+    (halo-only stores when the ranks' slice columns are given, the last step
+    full).  Returns per rank (lambda, x) -- or x_iters (a copy) when not
+    normalize."""
     P = len(engines)
     dev = x0.device
     bufs = [PeerBuffers(p, P, num_cols, dtype, dev) for p in range(P)]
     for b in bufs:
         b.connect_local(bufs)
-    runs = [PeerPowerIteration(engines[p], int(bounds[p]), int(bounds[p + 1]), bufs[p], normalize)
+    need = [needed_ranges(slice_columns[p], bounds) for p in range(P)] if slice_columns is not None else None
+    runs = [PeerPowerIteration(engines[p], int(bounds[p]), int(bounds[p + 1]), bufs[p], normalize,
+                               {q: tuple(need[q][p]) for q in range(P) if q != p} if need is not None else None)
             for p in range(P)]
     try:
         for r in runs:
             r.begin(x0)
-        for _ in range(iters):
+        for i in range(iters):
             for r in runs:
-                r.step()
+                r.step(full=i == iters - 1)
         return [r.finish() if normalize else r.current().clone() for r in runs]
     finally:
         torch.cuda.synchronize(dev)

@@ -45,7 +45,7 @@ def test_spmv_peer_stores_bit_identical(argcsr, orc, kind):
     r0 = 5
     targets = [torch.full((A.num_rows + 10,), 3.5, dtype=torch.float64, device="cuda") for _ in range(3)]
     m.spmv_peer_device(x.data_ptr(), s.data_ptr(), 0, m.num_groups, y.data_ptr(),
-                       [t.data_ptr() + r0 * 8 for t in targets], 0, torch.cuda.current_stream().cuda_stream)
+                       [t.data_ptr() + r0 * 8 for t in targets], stream=torch.cuda.current_stream().cuda_stream)
     ref = orc.spmv_argcsr(orc.argcsr_from_csr(A, 128, 1), (x * s).cpu().numpy())
     assert bits(y.cpu().numpy()) == bits(ref)
     for t in targets:
@@ -53,19 +53,35 @@ def test_spmv_peer_stores_bit_identical(argcsr, orc, kind):
         assert bits(t[r0:r0 + A.num_rows]) == bits(ref)
         assert np.all(t[:r0] == 3.5) and np.all(t[r0 + A.num_rows:] == 3.5)
     with pytest.raises(argcsr.ParameterError):
-        m.spmv_peer_device(x.data_ptr(), 0, 0, m.num_groups, y.data_ptr(), [t.data_ptr() for t in targets * 3], 0, 0)
+        m.spmv_peer_device(x.data_ptr(), 0, 0, m.num_groups, y.data_ptr(), [t.data_ptr() for t in targets * 3])
+    # row ranges: peer 0 gets rows [100, 300), peer 1 none, peer 2 all
+    for t in targets:
+        t.fill_(3.5)
+    m.spmv_peer_device(x.data_ptr(), s.data_ptr(), 0, m.num_groups, y.data_ptr(),
+                       [t.data_ptr() + r0 * 8 for t in targets], peer_rows=[100, 300, 0, 0, 0, A.num_rows],
+                       stream=torch.cuda.current_stream().cuda_stream)
+    t0, t1, t2 = (t.cpu().numpy()[r0:r0 + A.num_rows] for t in targets)
+    assert bits(t0[100:300]) == bits(ref[100:300]) and np.all(t0[:100] == 3.5) and np.all(t0[300:] == 3.5)
+    assert np.all(t1 == 3.5)
+    assert bits(t2) == bits(ref)
 
 
+@pytest.mark.parametrize("halo", [False, True])
 @pytest.mark.parametrize("P", [1, 2, 3, 4])
 @pytest.mark.parametrize("kind", ["stencil", "powerlaw"])
-def test_peer_power_iteration_virtual_ranks(kind, P):
+def test_peer_power_iteration_virtual_ranks(kind, P, halo):
+    """Full stores, or halo-only stores (each peer gets the rows its columns
+    read; the last step stores everything so every rank ends with all of x)."""
     import oracle
+    from paper_1203_5737_b200.multigpu import slice_rows
     from paper_1203_5737_b200.peer import power_iteration_local
 
     A = stencil27(16) if kind == "stencil" else powerlaw_csr(6000, 6000, seed=4, heavy_rows=[(7, 4000)])
     b, engs = _engines(A, P)
+    cols = [slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1])).columns
+            for p in range(P)] if halo else None
     x0 = oracle.bench_input(A.num_cols)
-    out = power_iteration_local(engs, b, A.num_cols, torch.from_numpy(x0).cuda(), 25)
+    out = power_iteration_local(engs, b, A.num_cols, torch.from_numpy(x0).cuda(), 25, slice_columns=cols)
     lam_ref, x_ref = reference_power_iteration(A, x0, 25, 128, 1)
     xs = [x.cpu().numpy() for _, x in out]
     for lam, x in zip((o[0] for o in out), xs):

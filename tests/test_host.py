@@ -160,3 +160,40 @@ def test_cpp_example_runs_on_the_device(tmp_path):
     r = subprocess.run([str(exe), "300", str(tmp_path / "a.spfmt")], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "lossless=1" in r.stdout
+
+
+def test_peer_needed_ranges_are_the_halo():
+    """The rows each peer reads from a rank (peer.py: one [lo, hi) interval
+    per owner): for a 27-pt stencil split 4 ways, each rank needs its own rows
+    plus about one plane of each neighbour, nothing from the others."""
+    from helpers import stencil27
+    from paper_1203_5737_b200.multigpu import partition_bounds, slice_rows
+    from paper_1203_5737_b200.peer import needed_ranges
+
+    n = 16
+    A = stencil27(n)
+    b = partition_bounds(A.row_pointers, 4)
+    for p in range(4):
+        sl = slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1]))
+        need = needed_ranges(sl.columns, b)
+        assert tuple(need[p]) == (int(b[p]), int(b[p + 1]))
+        for q in range(4):
+            lo, hi = need[q]
+            if abs(q - p) > 1:
+                assert (lo, hi) == (0, 0)
+            elif q != p:
+                assert 0 < hi - lo <= n * n + n + 1  # one plane (+ one row and one point of the next)
+                cols = np.asarray(sl.columns)
+                inq = cols[(cols >= b[q]) & (cols < b[q + 1])]
+                assert lo == inq.min() and hi == inq.max() + 1
+
+
+def test_peer_abi_parameter_errors_without_device(argcsr):
+    import paper_1203_5737_b200._argcsr_gpu as ext
+
+    with pytest.raises(argcsr.ParameterError):
+        ext.peer_signal([1] * 8, 1)  # at most 7 peers
+    with pytest.raises(argcsr.ParameterError):
+        ext.peer_signal([1, 2], 1, 0, [3])  # one partial destination per flag
+    with pytest.raises(argcsr.ParameterError):
+        ext.peer_open(b"short", 0)

@@ -259,6 +259,13 @@ typedef struct {
 } argcsr_format_stats;
 ARGCSR_API argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_format_stats* out);
 
+/* balance_stats(const ArgCsrMatrix&) (analysis.cpp:198-208, balance_of :29-55):
+ * explicit entries per group (per_group_nnz[num_groups], may be NULL),
+ * max / mean and the coefficient of variation -- bit-identical to the
+ * reference (counts on the device, the ratios on the host in its order). */
+ARGCSR_API argcsr_status argcsr_dev_balance_stats(const argcsr_dev* m, uint64_t* per_group_nnz,
+                                                  double* max_over_mean, double* coefficient_of_variation);
+
 ARGCSR_API void argcsr_dev_free(argcsr_dev* m);
 
 /* ------------------------------------------- ELLPACK / Sliced ELLPACK */

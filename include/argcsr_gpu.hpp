@@ -108,6 +108,12 @@ struct FormatStats {
     std::size_t estimated_bytes = 0;
 };
 
+struct BalanceStats {  // analysis.hpp:26-32
+    std::vector<std::size_t> per_group_nnz;
+    double max_over_mean = 1.0;
+    double coefficient_of_variation = 0.0;
+};
+
 static_assert(sizeof(std::size_t) == sizeof(uint64_t), "64-bit size_t required");
 
 // ------------------------------------------------------ device ARG-CSR matrix
@@ -238,6 +244,16 @@ inline FormatStats padding_stats(const DeviceArgCsr& M) {
     argcsr_format_stats s{};
     check(argcsr_dev_padding_stats(M.handle(), &s));
     return {s.explicit_nnz, s.assigned_padded_slots, s.total_allocated_slots, s.padding_ratio, s.estimated_bytes};
+}
+
+inline BalanceStats balance_stats(const DeviceArgCsr& M) {
+    argcsr_dev_info_t info{};
+    check(argcsr_dev_info(M.handle(), &info));
+    BalanceStats b;
+    b.per_group_nnz.resize(info.num_groups);
+    check(argcsr_dev_balance_stats(M.handle(), reinterpret_cast<uint64_t*>(b.per_group_nnz.data()),
+                                   &b.max_over_mean, &b.coefficient_of_variation));
+    return b;
 }
 
 // io.hpp:37-43 — the reference's binary container, byte-identical.

@@ -225,6 +225,7 @@ class _Ref:
         L.ref_csr_from_argcsr.argtypes = [vp, C.POINTER(vp)]
         L.ref_chunk_entries.argtypes = [vp, C.c_uint64, C.c_uint64, f64p, i32p, u64p]
         L.ref_padding_stats.argtypes = [vp, u64p, u64p, u64p, f64p, u64p]
+        L.ref_balance_stats.argtypes = [vp, u64p, f64p, f64p]
         L.ref_spmv_argcsr.argtypes = [vp, f64p, C.c_uint64, f64p]
         L.ref_spmv_csr.argtypes = [vp, f64p, C.c_uint64, f64p]
         L.ref_time_spmv_argcsr_parallel.argtypes = [vp, f64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, f64p,
@@ -403,6 +404,17 @@ class _Ref:
             self._check(self.lib.ref_padding_stats(h, C.byref(e), C.byref(p), C.byref(t), C.byref(r), C.byref(b)))
             return dict(explicit_nnz=e.value, assigned_padded_slots=p.value, total_allocated_slots=t.value,
                         padding_ratio=r.value, estimated_bytes=b.value)
+        finally:
+            self.lib.ref_argcsr_free(h)
+
+    def balance_stats(self, M: ArgCsr):
+        """balance_stats(const ArgCsrMatrix&) of the compiled reference (analysis.cpp:198-208)."""
+        h = self.import_argcsr(M)
+        try:
+            per = np.zeros(M.groups.shape[0], dtype=np.uint64)
+            mom, cv = C.c_double(), C.c_double()
+            self._check(self.lib.ref_balance_stats(h, _p(per, u64p), C.byref(mom), C.byref(cv)))
+            return per, mom.value, cv.value
         finally:
             self.lib.ref_argcsr_free(h)
 

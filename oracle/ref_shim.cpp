@@ -276,6 +276,15 @@ int ref_padding_stats(const void* h, uint64_t* explicit_nnz, uint64_t* padded,
     });
 }
 
+int ref_balance_stats(const void* h, uint64_t* per_group, double* max_over_mean, double* cv) {
+    return guarded([&] {
+        const BalanceStats b = balance_stats(*static_cast<const ArgCsrMatrix*>(h));
+        for (size_t i = 0; i < b.per_group_nnz.size(); ++i) per_group[i] = b.per_group_nnz[i];
+        *max_over_mean = b.max_over_mean;
+        *cv = b.coefficient_of_variation;
+    });
+}
+
 // ------------------------------------------------------------------------ SpMV
 int ref_spmv_argcsr(const void* h, const double* x, uint64_t nx, double* y) {
     return guarded([&] {

@@ -64,6 +64,8 @@ csr_from_argcsr = _ext.csr_from_argcsr
 csr_arrays_from_argcsr = _ext.csr_arrays_from_argcsr
 chunk_entries = _ext.chunk_entries
 padding_stats = _ext.padding_stats
+balance_stats = _ext.balance_stats
+BalanceStats = _ext.BalanceStats
 read_matrix_market = _ext.read_matrix_market
 write_matrix_market = _ext.write_matrix_market
 partition_rows = _ext.partition_rows

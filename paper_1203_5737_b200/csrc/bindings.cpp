@@ -447,6 +447,11 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         .def_readonly("padding_ratio", &FormatStats::padding_ratio)
         .def_readonly("estimated_bytes", &FormatStats::estimated_bytes);
 
+    py::class_<argcsr_b200::BalanceStats>(m, "BalanceStats")  // reference bindings.cpp:77-80
+        .def_readonly("per_group_nnz", &argcsr_b200::BalanceStats::per_group_nnz)
+        .def_readonly("max_over_mean", &argcsr_b200::BalanceStats::max_over_mean)
+        .def_readonly("coefficient_of_variation", &argcsr_b200::BalanceStats::coefficient_of_variation);
+
     py::class_<PyArgCsr>(m, "ArgCsrMatrix")
         .def_property_readonly("num_rows", [](const PyArgCsr& p) { return p.info().num_rows; })
         .def_property_readonly("num_cols", [](const PyArgCsr& p) { return p.info().num_cols; })
@@ -885,6 +890,8 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
 
     m.def(
         "padding_stats", [](const PyArgCsr& p) { return argcsr_b200::padding_stats(*p.dev); }, py::arg("matrix"));
+    m.def(
+        "balance_stats", [](const PyArgCsr& p) { return argcsr_b200::balance_stats(*p.dev); }, py::arg("matrix"));
 
     m.def(
         "partition_rows",

@@ -668,6 +668,15 @@ argcsr_status argcsr_dev_chunk_entries(const argcsr_dev* m, uint64_t group_index
     });
 }
 
+argcsr_status argcsr_dev_balance_stats(const argcsr_dev* m, uint64_t* per_group_nnz, double* max_over_mean,
+                                       double* coefficient_of_variation) {
+    return guarded([&] {
+        check_handle(m);
+        DeviceScope scope(m->device);
+        argcsr_gpu::balance_stats(m, per_group_nnz, max_over_mean, coefficient_of_variation, cudaStreamPerThread);
+    });
+}
+
 argcsr_status argcsr_dev_padding_stats(const argcsr_dev* m, argcsr_format_stats* out) {
     return guarded([&] {
         check_handle(m);

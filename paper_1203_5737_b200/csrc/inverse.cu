@@ -126,6 +126,21 @@ __global__ void k_count_explicit(const int32_t* __restrict__ cols, uint64_t n, u
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
+// Explicit entries of each group's stored block (one warp per group).
+__global__ void k_group_nnz(const GroupDesc* __restrict__ desc, const int32_t* __restrict__ cols, uint64_t G,
+                            uint64_t* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < G;
+         g += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const GroupDesc d = desc[g];
+        const uint64_t n = uint64_t(d.chunk) * d.stride(), base = d.offset();
+        uint64_t c = 0;
+        for (uint64_t i = lane; i < n; i += 32) c += cols[base + i] != -1;
+        c = warp_sum_u64(c);
+        if (lane == 0) out[g] = c;
+    }
+}
+
 template <typename TM>
 __global__ void k_assigned_slots(const GroupDesc* __restrict__ desc, const TM* __restrict__ assigned, uint64_t G,
                                  unsigned long long* __restrict__ out) {
@@ -261,6 +276,40 @@ uint64_t to_csr_nnz(const argcsr_dev* m, cudaStream_t s) {
     CUDA_OK(cudaMemcpyAsync(&nnz, rp.p + N, sizeof nnz, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaStreamSynchronize(s));
     return nnz;
+}
+
+void balance_stats(const argcsr_dev* m, uint64_t* per_group, double* max_over_mean, double* cv, cudaStream_t s) {
+    const uint64_t G = m->num_groups;
+    std::vector<uint64_t> n(G);
+    if (G) {
+        Scratch<uint64_t> cnt(G, s);
+        k_group_nnz<<<grid_for(G * 32, 256), 256, 0, s>>>(m->groups, m->columns, G, cnt.p);
+        LAUNCH_OK("k_group_nnz");
+        CUDA_OK(cudaMemcpyAsync(n.data(), cnt.p, G * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+    }
+    if (per_group) std::copy(n.begin(), n.end(), per_group);
+    // balance_of (analysis.cpp:29-55), in its order: mean of the counts, max /
+    // mean, population variance summed in group order, sqrt(var) / mean; an
+    // empty matrix or an all-zero one gives (1, 0).
+    double mom = 1.0, c = 0.0;
+    if (G) {
+        uint64_t total = 0, mx = 0;
+        for (uint64_t v : n) total += v, mx = std::max(mx, v);
+        const double mean = double(total) / double(G);
+        if (mean != 0.0) {
+            mom = double(mx) / mean;
+            double var = 0.0;
+            for (uint64_t v : n) {
+                const double d = double(v) - mean;
+                var += d * d;
+            }
+            var /= double(G);
+            c = std::sqrt(var) / mean;
+        }
+    }
+    if (max_over_mean) *max_over_mean = mom;
+    if (cv) *cv = c;
 }
 
 void padding_stats(const argcsr_dev* m, argcsr_format_stats* out, cudaStream_t s) {

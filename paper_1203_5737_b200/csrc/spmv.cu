@@ -997,12 +997,24 @@ __global__ void k_peer_signal(PeerSlots p, uint32_t n, uint64_t value, const dou
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.flag[q]), "l"(value) : "memory");
 }
 
+// A peer that never signals (it died) would hang the GPU: after 60 s of
+// waiting the kernel traps, so the step fails loudly instead.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void k_peer_wait(const uint64_t* flags, uint32_t n, uint64_t value) {
+    const uint64_t t0 = globaltimer_ns();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         uint64_t v;
         do {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
-            if (v < value) __nanosleep(200);
+            if (v < value) {
+                __nanosleep(200);
+                if (globaltimer_ns() - t0 > 60ull * 1000000000ull) __trap();
+            }
         } while (v < value);
     }
     __syncthreads();

@@ -443,3 +443,17 @@ def test_host_async_stream(argcsr, orc, kind):
     dev.host_wait()
     for x, y in zip(xs, ys):
         assert bits(y.numpy()) == bits(orc.spmv_argcsr(ref_m, x.numpy()))
+
+
+def test_balance_stats_matches_reference(argcsr, ref, corpus):
+    """balance_stats (analysis.cpp:198-208): per-group explicit entries equal,
+    max/mean and the coefficient of variation bit-identical to the compiled
+    reference, in both device layouts and with heavy groups."""
+    cases = [(A, t, d) for A in corpus[:80] for t, d in ((4, 1), (32, 4), (128, 1))]
+    cases += [(powerlaw_csr(20000, 20000, seed=3, heavy_rows=[(1, 9000)]), 128, 1), (stencil27(10), 128, 32)]
+    for A, tpg, dcs in cases:
+        per_ref, mom_ref, cv_ref = ref.balance_stats(ref.argcsr_from_csr(A, tpg, dcs))
+        for layout in ("compact", "reference"):
+            b = argcsr.balance_stats(to_dev(argcsr, A, tpg, dcs, layout=layout))
+            assert np.array_equal(np.asarray(b.per_group_nnz, np.uint64), per_ref)
+            assert bits(np.array([b.max_over_mean, b.coefficient_of_variation])) == bits(np.array([mom_ref, cv_ref]))

@@ -1,0 +1,4 @@
+# full GPU suite on the final tree + smoke
+export PYTHONWARNINGS=ignore
+timeout 2400 python -m pytest tests/ -m gpu -x -q 2>&1 | tail -5
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1

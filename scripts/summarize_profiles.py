@@ -21,7 +21,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__t_sector_hit_rate.pct", "l1tex__throughput.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__grid_size",
         "sm__warps_active.avg.per_cycle_active", "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum",
-        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct"]
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio",
+        "lts__t_sectors_evict_last_lookup_hit.sum", "lts__t_sectors_evict_last_lookup_miss.sum",
+        "lts__t_sectors_srcunit_ltcfabric.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"]
 
 
 def ncu(args):
@@ -49,6 +53,13 @@ def summarize(rep: Path):
             if k in h:
                 i = h.index(k)
                 lines.append(f"  {k:66s} {v[i]:>18s} {u[i]}")
+        try:  # x gathers are the only L2 evict_last loads: their L2 hit rate
+            xh = float(v[h.index("lts__t_sectors_evict_last_lookup_hit.sum")].replace(",", ""))
+            xm = float(v[h.index("lts__t_sectors_evict_last_lookup_miss.sum")].replace(",", ""))
+            if xh + xm > 0:
+                lines.append(f"  {'x gathers: L2 hit rate (evict_last sectors)':66s} {100 * xh / (xh + xm):>18.2f} %")
+        except (ValueError, IndexError):
+            pass
         rb = to_bytes(v[h.index("dram__bytes_read.sum")], u[h.index("dram__bytes_read.sum")])
         wb = to_bytes(v[h.index("dram__bytes_write.sum")], u[h.index("dram__bytes_write.sum")])
         traffic += rb + wb

@@ -880,7 +880,10 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
         CUDA_OK(cudaStreamWaitEvent(m->aux, m->ev_fork, 0));
     }
     if (m->heavy_ctas > 0) {
-        const size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
+        size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
+        // experiments: pad the heavy CTAs' shared memory so fewer of them fit
+        // an SM and light tiles co-reside (ARGCSR_HEAVY_SMEM bytes)
+        if (const char* e = std::getenv("ARGCSR_HEAVY_SMEM")) smem = std::max<size_t>(smem, size_t(std::atol(e)));
         // Default: scalar x gathers; fp64 8 element steps in flight per lane at
         // 4 CTAs/SM, fp32 4 steps at 6 CTAs/SM (measured best on C3/C4,
         // DESIGN.md §4).  Experiments: ARGCSR_HEAVY_U = 4 | 8 | 16 (steps),

@@ -550,6 +550,9 @@ argcsr_status argcsr_dev_spmv_host_async(const argcsr_dev* mc, const void* x_hos
         // multiply on the caller's stream once x is up and this y buffer is downloaded
         CUDA_OK(cudaStreamWaitEvent(s, m->as_up[b], 0));
         if (m->as_used[b]) CUDA_OK(cudaStreamWaitEvent(s, m->as_down[b], 0));
+        // one SpMV in flight per handle (x' buffer, heavy-group stream), even
+        // when consecutive calls name different streams
+        if (m->as_used[b ^ 1]) CUDA_OK(cudaStreamWaitEvent(s, m->as_mv[b ^ 1], 0));
         argcsr_gpu::spmv_launch(m, m->as_x[b], m->as_y[b], 0, m->num_groups, s);
         CUDA_OK(cudaEventRecord(m->as_mv[b], s));
         // download (copy engine 2)

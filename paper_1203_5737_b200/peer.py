@@ -154,12 +154,19 @@ class PeerPowerIteration:
                 self.peer_rows += [max(lo, 0), max(hi, 0)]
         self.stream = engine.stream
         self.scale = torch.ones(1, dtype=torch.float64, device=bufs.device)
+        # Step numbers are absolute and never reset: the flags compare against
+        # them, so a second run on the same buffers cannot pass a wait on a
+        # stale flag of the first run.
         self.k = 0
+        self.k0 = 0  # first step of the current run
 
     def begin(self, x0: torch.Tensor) -> None:
-        self.bufs.x[0].copy_(x0)
+        """Start a run from x0 (collective: every rank calls it).  Only this
+        rank's own buffer is written; peers store into it only after seeing
+        this rank's flag for the step before theirs."""
+        self.bufs.x[self.k % 2].copy_(x0)
         self.scale.fill_(1.0)
-        self.k = 0
+        self.k0 = self.k
 
     def wait(self, k: int) -> None:
         if self.bufs.peers and k > 0:
@@ -173,7 +180,7 @@ class PeerPowerIteration:
         nb = (k + 1) % 2
         bufs = self.bufs
         self.wait(k)
-        if k > 0 and self.normalize:
+        if k > self.k0 and self.normalize:
             torch.reciprocal(torch.sqrt(bufs.partial[b].sum().reshape(1)), out=self.scale)
         y = bufs.x[nb][self.r0:self.r1]
         self.engine.m.spmv_peer_device(bufs.x[b].data_ptr(), self.scale.data_ptr() if self.normalize else 0, 0,

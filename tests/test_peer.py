@@ -134,6 +134,8 @@ def _ipc_worker(rank, world, port, kind, out_dir):
         assert D.exchange == "p2p" and D.peer.peers == [1 - rank]
         x0 = oracle.bench_input(A.num_cols)
         lam, x = D.power_iteration(torch.from_numpy(x0).cuda(), 12)
+        lam2, x2 = D.power_iteration(torch.from_numpy(x0).cuda(), 12)  # a second run on the same buffers
+        assert lam2 == lam and torch.equal(x2, x)
         np.save(os.path.join(out_dir, f"x{rank}.npy"), x.cpu().numpy())
         np.save(os.path.join(out_dir, f"lam{rank}.npy"), np.array([lam]))
         D.close()

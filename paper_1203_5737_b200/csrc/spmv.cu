@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
 // otherwise both phases binary-search the tile's group table.
 // PAIR (launched when every light chunk is <= U/2 and a tile has at most two
 // units per thread): each thread's two units go through phase1_pair.
-template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true, bool PEER = false, bool PAIR = false>
+template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true, bool PEER = false, bool PAIR = false,
+          bool DYNW = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -417,6 +418,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
 
     const uint64_t ub0 = a.unit_base[gs];
     const uint32_t row0 = MAP ? a.groups[gs].first_row : 0u;
+    __shared__ uint32_t s_next;  // DYNW: next 32-unit chunk
+    if (DYNW && threadIdx.x == 0) s_next = blockDim.x / 32;
     // lengths of this thread's first two units (loaded under the metadata staging)
     uint32_t ulen2[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
     if (a.ulen) {
@@ -485,21 +488,37 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
             }
         }
     }
-    for (uint32_t u = threadIdx.x; !PAIR && u < nunits; u += blockDim.x) {
+    auto unit = [&](uint32_t u, uint32_t ulen_hint) {
         const uint32_t gi = MAP ? s_ugrp[u] : find_le(s_ub, ng, u);
         const uint32_t g = gs + gi;
-        if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
+        if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) return;
         double s[V];
         const uint64_t os = s_off[gi];
-        uint32_t len = s_chunk[gi];
-        if (a.ulen) {
-            const uint32_t k = (u - threadIdx.x) / blockDim.x;
-            len = min(len, k < 2 ? ulen2[k] : uint32_t(a.ulen[ub0 + u]));
-        }
+        const uint32_t len = a.ulen ? min(s_chunk[gi], ulen_hint) : s_chunk[gi];
         phase1<T, V, U, PRED>(a, (os & kOffsetMask) + (u - s_ub[gi]) * V, len, (os >> 48) & 0x7FFF, s, pol_stream,
                               pol_x, xs);
 #pragma unroll
         for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = s[l];
+    };
+    if constexpr (DYNW) {
+        // warps take 32-unit chunks: the first by warp index, the rest from a
+        // shared counter, so warps whose gathers return early take more
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t c = threadIdx.x >> 5;
+        bool first = true;
+        while (c * 32 < nunits) {
+            const uint32_t u = c * 32 + lane;
+            if (u < nunits) unit(u, !a.ulen ? 0xFFFFFFFFu : first ? ulen2[0] : uint32_t(a.ulen[ub0 + u]));
+            first = false;
+            uint32_t nx = 0;
+            if (lane == 0) nx = atomicAdd(&s_next, 1u);
+            c = __shfl_sync(0xFFFFFFFFu, nx, 0);
+        }
+    } else {
+        for (uint32_t u = threadIdx.x; !PAIR && u < nunits; u += blockDim.x) {
+            const uint32_t k = (u - threadIdx.x) / blockDim.x;
+            unit(u, !a.ulen ? 0xFFFFFFFFu : k < 2 ? ulen2[k] : uint32_t(a.ulen[ub0 + u]));
+        }
     }
     __syncthreads();
 
@@ -755,6 +774,17 @@ void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
         else
             launch(spmv_light_kernel<T, V, U, PRED, 4, false, PEER, true>, m->num_tiles, light_smem_bytes(m, V), m, a,
                    s);
+    } else if (const char* dw = std::getenv("ARGCSR_LIGHT_DYN");
+               !PEER && (dw ? dw[0] == '1' : m->num_heavy > 0)) {
+        // power-law matrices (heavy groups present, light chunks of every
+        // size): warps take 32-unit chunks dynamically (C3 +2%; C2 -3%, so
+        // not for stencils).  ARGCSR_LIGHT_DYN=0|1 forces it (experiments).
+        if (map)
+            launch(spmv_light_kernel<T, V, U, PRED, MINB, true, false, false, true>, m->num_tiles,
+                   light_smem_bytes(m, V, true), m, a, s);
+        else
+            launch(spmv_light_kernel<T, V, U, PRED, MINB, false, false, false, true>, m->num_tiles,
+                   light_smem_bytes(m, V), m, a, s);
     } else if (map) {
         launch(spmv_light_kernel<T, V, U, PRED, MINB, true, PEER>, m->num_tiles, light_smem_bytes(m, V, true), m, a,
                s);

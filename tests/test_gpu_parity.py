@@ -180,7 +180,7 @@ def test_skew_and_uniform_families(argcsr, orc, ref):  # acceptance.cpp:171-198
 
 
 # --------------------------------------------------------- larger / edge cases
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16", "ARGCSR_LIGHT_DYN=0", "ARGCSR_LIGHT_DYN=1"])
 @pytest.mark.parametrize("tpg,dcs", [(128, 1), (128, 4), (64, 2), (32, 1), (100, 1), (30, 3), (127, 1), (256, 1)])
 def test_powerlaw_heavy_groups(argcsr, orc, tpg, dcs, heavy, monkeypatch):
     """Heavy-tailed rows: long-chunk (heavy) groups, multi-tile schedule,

@@ -121,11 +121,17 @@ class DeviceEngine:
                                           cols.to(device, torch.int32).contiguous(),
                                           vals.to(device, dtype).contiguous(), tpg, dcs, stream=self.stream,
                                           layout=layout)
+        self.stream.synchronize()  # the handle is used from other streams afterwards
+
+    def cur(self) -> int:
+        """The caller's current stream: products are ordered with the torch
+        ops around them (norms, copies), whatever stream the conversion used."""
+        return torch.cuda.current_stream(self.device).cuda_stream
 
     def spmv(self, x: torch.Tensor, y: torch.Tensor, x_scale: Optional[torch.Tensor] = None) -> None:
         """y = A (s * x), s = x_scale[0] read on the device (None: 1)."""
         self.m.spmv_scaled_device(x.data_ptr(), 0 if x_scale is None else x_scale.data_ptr(), y.data_ptr(),
-                                  self.stream.cuda_stream)
+                                  self.cur())
 
     def spmv_range(self, x: torch.Tensor, y: torch.Tensor, g0: int, g1: int, x_scale: Optional[torch.Tensor] = None,
                    reuse_x: bool = False) -> None:
@@ -133,7 +139,7 @@ class DeviceEngine:
         if g1 <= g0:
             return
         self.m.spmv_ex_device(x.data_ptr(), 0 if x_scale is None else x_scale.data_ptr(), g0, g1, y.data_ptr(),
-                              1 if reuse_x else 0, self.stream.cuda_stream)
+                              1 if reuse_x else 0, self.cur())
 
     @property
     def num_groups(self) -> int:
@@ -368,13 +374,13 @@ class DistributedArgCsr:
         if self.overlap:
             y = self._spmv_overlapped(xin, xout, scale)
         else:
-            y = self.y
+            y = xout if self.world == 1 else self.y  # one GPU: y is the next x, no copy
             self.engine.spmv(xin, y, scale)
         y64 = y.to(torch.float64)
         s2.copy_(torch.dot(y64, y64).reshape(1))
         self.allreduce_sum(s2)
         if self.overlap:
             self.exchange_async(xout)  # in flight under the next step's interior groups
-        else:
+        elif self.world > 1:
             self.gather(y, xout)
         torch.reciprocal(torch.sqrt(s2), out=scale)

@@ -145,6 +145,7 @@ class PeerPowerIteration:
                  send_ranges: Optional[dict] = None):
         self.engine, self.r0, self.r1, self.bufs = engine, r0, r1, bufs
         self.normalize = normalize
+        self.device = bufs.device
         # rows (local to the slice) each peer reads from this rank: q -> (lo, hi)
         self.peer_rows = []
         if send_ranges is not None:
@@ -152,13 +153,17 @@ class PeerPowerIteration:
                 lo, hi = send_ranges[q]
                 lo, hi = (lo - r0, hi - r0) if hi > lo else (0, 0)
                 self.peer_rows += [max(lo, 0), max(hi, 0)]
-        self.stream = engine.stream
         self.scale = torch.ones(1, dtype=torch.float64, device=bufs.device)
         # Step numbers are absolute and never reset: the flags compare against
         # them, so a second run on the same buffers cannot pass a wait on a
         # stale flag of the first run.
         self.k = 0
         self.k0 = 0  # first step of the current run
+
+    def _cur(self) -> int:
+        """The caller's current stream: the peer kernels, the SpMV and the
+        torch ops on the norms are all ordered on it."""
+        return torch.cuda.current_stream(self.device).cuda_stream
 
     def begin(self, x0: torch.Tensor) -> None:
         """Start a run from x0 (collective: every rank calls it).  Only this
@@ -170,7 +175,7 @@ class PeerPowerIteration:
 
     def wait(self, k: int) -> None:
         if self.bufs.peers and k > 0:
-            _ext.peer_wait(self.bufs.flags.data_ptr(), self.bufs.world, k, self.stream.cuda_stream)
+            _ext.peer_wait(self.bufs.flags.data_ptr(), self.bufs.world, k, self._cur())
 
     def step(self, full: bool = False) -> None:
         """One step; `full` stores every row into every peer (the last step of
@@ -185,14 +190,14 @@ class PeerPowerIteration:
         y = bufs.x[nb][self.r0:self.r1]
         self.engine.m.spmv_peer_device(bufs.x[b].data_ptr(), self.scale.data_ptr() if self.normalize else 0, 0,
                                        self.engine.num_groups, y.data_ptr(), bufs.peer_x(nb, self.r0),
-                                       [] if full else self.peer_rows, 0, self.stream.cuda_stream)
+                                       [] if full else self.peer_rows, 0, self._cur())
         own = bufs.partial[nb][bufs.rank:bufs.rank + 1]
         if self.normalize:
             y64 = y.to(torch.float64)
             own.copy_(torch.dot(y64, y64).reshape(1))
         if bufs.peers:
             _ext.peer_signal(bufs.peer_flag_slots(), k + 1, own.data_ptr() if self.normalize else 0,
-                             bufs.peer_partial_slots(nb) if self.normalize else [], self.stream.cuda_stream)
+                             bufs.peer_partial_slots(nb) if self.normalize else [], self._cur())
         bufs.flags[bufs.rank:bufs.rank + 1].fill_(k + 1)  # own slot: the wait covers all `world` slots
         self.k = k + 1
 

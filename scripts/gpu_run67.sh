@@ -1,0 +1,7 @@
+# stream-order fix: regression test + valid C5 lines (both exchanges)
+export PYTHONWARNINGS=ignore
+timeout 900 python -m pytest tests/test_multigpu_device.py tests/test_peer.py -m gpu -x -q 2>&1 | tail -2
+mkdir -p gpurun_out/bench
+timeout 1200 python bench.py --config C5 --power-iteration --steps 30 --warmup 3 > gpurun_out/bench/bench_C5.json 2>/dev/null
+timeout 1200 python bench.py --config C5 --power-iteration --exchange p2p --steps 30 --warmup 3 > gpurun_out/bench/bench_C5_p2p.json 2>/dev/null
+for f in bench_C5 bench_C5_p2p; do python -c "import json; d=json.load(open('gpurun_out/bench/$f.json')); print('$f', d['ms_per_step'], d['value'], d['roofline']['frac'], d['power_iteration']['lambda'], d['gpu_launches'])"; done

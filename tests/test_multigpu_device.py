@@ -84,3 +84,26 @@ def test_interior_boundary_split_is_bit_identical(argcsr, x_remap):
     eng.spmv_range(x, y, 0, ga, s)
     eng.spmv_range(x, y, gb, eng.num_groups, s, reuse_x=True)
     assert bits(y.cpu().numpy()) == bits(y_full.cpu().numpy())
+
+
+@pytest.mark.parametrize("exchange", ["auto", "p2p"])
+def test_power_iteration_engine_on_side_stream(exchange):
+    """The engine converted under a side stream (as bench.py sets it up), the
+    steps run on the caller's current stream: every product, norm and flag is
+    ordered on the stream current at call time (a 262 k-row stencil is large
+    enough for a cross-stream race to show)."""
+    import oracle
+    from paper_1203_5737_b200.multigpu import DistributedArgCsr
+
+    A = stencil27(64)
+    dev = torch.device("cuda", 0)
+    side = torch.cuda.Stream(dev)
+    with torch.cuda.stream(side):
+        D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values, 128, 1, device=dev,
+                              exchange=exchange)
+    x0 = oracle.bench_input(A.num_cols)
+    lam, x = D.power_iteration(torch.from_numpy(x0).cuda(), 20)
+    D.close()
+    lam_ref, x_ref = reference_power_iteration(A, x0, 20, 128, 1)
+    assert abs(lam - lam_ref) <= 1e-10 * abs(lam_ref)
+    assert np.max(np.abs(x.cpu().numpy() - x_ref)) <= 1e-9

@@ -272,7 +272,7 @@ def run_b200(args):
     D = None
     with torch.cuda.stream(stream):
         ce0.record(stream)
-        if world > 1 or args.power_iteration:
+        if world > 1 or args.power_iteration or os.environ.get("ARGCSR_BENCH_DIST") == "1":
             # nnz-balanced row slices, each rank converts its own (multigpu.py)
             from paper_1203_5737_b200.multigpu import DistributedArgCsr
 
@@ -400,6 +400,45 @@ def run_b200(args):
 
     gflops = 2.0 * nnz_total / (step_ms * 1e-3) / 1e9
     eff_gbs = ab / (step_ms * 1e-3) / 1e9
+    e2e_dist = None
+    if D is not None and not args.power_iteration and D.pstep is None:
+        # e2e at N GPUs through the multi-GPU API: every step each rank uploads
+        # its input x from pinned host memory, runs the SpMV + exchange
+        # (spmv_gather) and downloads its y slice; max over ranks of the time.
+        try:
+            xh = torch.empty(A.num_cols, dtype=tdtype, pin_memory=True)
+            xh.copy_(x.cpu())
+            yh = torch.empty(D.r1 - D.r0, dtype=tdtype, pin_memory=True)
+            xd, od = torch.empty_like(x), torch.empty_like(x)
+
+            def e2e_step():
+                xd.copy_(xh, non_blocking=True)
+                D.spmv_gather(xd, od, wait=True)
+                yh.copy_(od[D.r0:D.r1], non_blocking=True)
+
+            for _ in range(3):
+                e2e_step()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            k2 = max(10, min(args.steps, 50))
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            for _ in range(k2):
+                e2e_step()
+            f1.record()
+            torch.cuda.synchronize()
+            t2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t2.item()) / k2
+            e2e_dist = {"value": round(2.0 * nnz_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                        "h2d_bytes_per_step": world * A.num_cols * sv, "d2h_bytes_per_step": A.num_rows * sv,
+                        "ms_per_step": e2e_ms, "steps": k2,
+                        "path": "per rank: pinned host x -> H2D, DistributedArgCsr.spmv_gather (SpMV + "
+                                f"{D.exchange} exchange), D2H of the rank's y slice; max over ranks"}
+        except Exception as exc:  # report, do not lose the bench line
+            e2e_dist = {"value": None, "error": f"{type(exc).__name__}: {exc}"[:200]}
     if D is not None and D.peer is not None:
         D.close()  # collective over the ranks: nobody stores into freed peer buffers
     if rank != 0:
@@ -446,7 +485,10 @@ def run_b200(args):
                                            if D.exchange == "p2p" else
                                            "SpMV + ||y||^2 all-reduce + all-gather of y + scaling fused into the next SpMV")}
 
-    if world == 1 and not args.power_iteration:
+    if e2e_dist is not None:
+        out["e2e"] = e2e_dist
+        out["gpu_launches"] = launches
+    elif world == 1 and not args.power_iteration:
         # ------------------------------------------------ e2e through the C-ABI with host buffers
         xh = torch.empty(A.num_cols, dtype=tdtype, pin_memory=True)
         xh.copy_(x.cpu())

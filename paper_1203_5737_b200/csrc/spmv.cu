@@ -900,7 +900,9 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.tile0 = 0;
     a.max_tile_units = uint32_t(m->max_tile_units);
     a.x_evict_last = env_flag("ARGCSR_XPOL", 1);
-    a.stream_evict_first = env_flag("ARGCSR_SPOL", m->num_heavy > 0 ? 1 : 0);
+    // values/columns: L2 evict_normal (evict_first measured slower once the heavy
+    // stream is prioritised: C4 0.69 vs 0.73, C3 0.323 vs 0.325); ARGCSR_SPOL=1 for A/B
+    a.stream_evict_first = env_flag("ARGCSR_SPOL", 0);
 
     // Heavy groups run concurrently on the handle's auxiliary stream (forked
     // from and joined back into `s`), launched first so their CTAs start first.

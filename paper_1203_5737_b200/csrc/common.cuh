@@ -118,6 +118,8 @@ struct argcsr_dev {
     void* as_x[2] = {}, *as_y[2] = {};
     cudaEvent_t as_up[2] = {}, as_mv[2] = {}, as_down[2] = {};
     bool as_used[2] = {};
+    cudaStream_t as_h2d2 = nullptr, as_d2h2 = nullptr;  // second copy streams (split copies)
+    cudaEvent_t as_j1[2] = {}, as_j2[2] = {};
     uint64_t as_calls = 0;           // rows of the largest light tile (heavy groups' rows included)
     uint64_t tile_span = 0;               // units between consecutive tile keys
     uint32_t tile_threads = 256;          // tiles were built for this CTA size

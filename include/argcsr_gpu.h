@@ -15,10 +15,20 @@
  *   - Validation order and messages follow the reference: threads_per_group /
  *     desired_chunk_size first (argcsr.cpp:20-23), then an empty matrix
  *     (argcsr.cpp:24-26), then vector lengths (argcsr.cpp:220-223).
- *   - A handle owns device memory on one device and is immutable after
- *     argcsr_dev_convert; calls on different handles/streams may run
- *     concurrently.  `stream` is a cudaStream_t passed as void* (NULL = the
- *     legacy default stream).
+ *   - A handle owns device memory on one device and its matrix is immutable
+ *     after argcsr_dev_convert.  Any thread may call any entry point on any
+ *     stream.  SpMVs on ONE handle are serialised in issue order: each
+ *     argcsr_dev_spmv* makes its stream wait for the previous SpMV on that
+ *     handle (a per-handle event), because the x-remap buffer and the
+ *     heavy-group stream are per-handle scratch.  SpMVs on different handles
+ *     run concurrently.  `stream` is a cudaStream_t passed as void* (NULL =
+ *     the legacy default stream).
+ *   - Process-wide side effect: while at least one handle lives on a device,
+ *     that device's persisting-L2 limit (cudaLimitPersistingL2CacheSize) is
+ *     raised to its maximum so x can be kept L2-resident through an
+ *     access-policy window.  The previous limit is saved by the first handle
+ *     and restored (after cudaCtxResetPersistingL2Cache) when the last one is
+ *     freed.  Set ARGCSR_L2_PERSIST=0 to leave the limit untouched.
  *   - argcsr_dev_spmv* on device pointers are stream-ordered and never
  *     synchronise except to report an error.  Calls with host pointers are
  *     synchronous, like the reference's value-returning functions.

@@ -20,6 +20,39 @@
 using argcsr_gpu::fail;
 using argcsr_gpu::Failure;
 
+namespace argcsr_gpu {
+const Knobs& knobs() {
+    static const Knobs k = [] {
+        Knobs v;
+        auto flag = [](const char* n, int d) {
+            const char* e = std::getenv(n);
+            return e && e[0] ? (e[0] == '1' ? 1 : e[0] == '0' ? 0 : d) : d;
+        };
+        auto chr = [](const char* n, char d) {
+            const char* e = std::getenv(n);
+            return e && e[0] ? e[0] : d;
+        };
+        v.l2_window = flag("ARGCSR_L2_WINDOW", 1) != 0;
+        v.l2_persist = flag("ARGCSR_L2_PERSIST", 1) != 0;
+        v.x_evict_last = flag("ARGCSR_XPOL", 1);
+        v.stream_evict_first = flag("ARGCSR_SPOL", 0);
+        v.map = flag("ARGCSR_MAP", -1);
+        v.pair = flag("ARGCSR_PAIR", 1);
+        v.light_dyn = flag("ARGCSR_LIGHT_DYN", -1);
+        if (const char* e = std::getenv("ARGCSR_HEAVY_SMEM")) v.heavy_smem = size_t(std::atol(e));
+        v.heavy_u = chr("ARGCSR_HEAVY_U", 0);
+        v.heavy_b = chr("ARGCSR_HEAVY_B", 0);
+        v.heavy_runs = flag("ARGCSR_HEAVY_RUNS", 0) == 1;
+        v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
+        v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
+        if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
+        v.ulen = flag("ARGCSR_ULEN", -1);
+        return v;
+    }();
+    return k;
+}
+}  // namespace argcsr_gpu
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -62,6 +95,8 @@ struct DeviceScope {
     }
 };
 
+void release_l2_persist(int device);
+
 void free_handle(argcsr_dev* m) {
     if (!m) return;
     int prev = -1;
@@ -77,7 +112,6 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->ulen);
     cudaFree(m->heavy);
     cudaFree(m->heavy_ptr);
-    cudaFree(m->sched);
     cudaFree(m->perm);
     cudaFree(m->xbuf);
     if (m->aux) cudaStreamDestroy(m->aux);
@@ -100,6 +134,8 @@ void free_handle(argcsr_dev* m) {
     }
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
+    if (m->ev_done) cudaEventDestroy(m->ev_done);
+    if (m->holds_l2_persist) release_l2_persist(m->device);
     if (prev >= 0) cudaSetDevice(prev);
     delete m;
 }
@@ -110,25 +146,74 @@ void check_handle(const argcsr_dev* m) {
     if (!m) fail(ARGCSR_E_PARAMETER, "null ARG-CSR handle");
 }
 
-// Persisting-L2 carve-out for the x window (SpMV), set once per device.
-size_t ensure_l2_persist(int device) {
-    static std::mutex mu;
-    static std::vector<long long> done(64, -1);
-    std::lock_guard<std::mutex> lock(mu);
-    if (device < 64 && done[device] >= 0) return size_t(done[device]);
-    int persist_max = 0;
-    CUDA_OK(cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, device));
+// Persisting-L2 carve-out for the x window (SpMV).  Raising the device's
+// persisting-L2 limit is a process-wide side effect (persisting lines can keep
+// L2 from other kernels of the host application), so it is reference-counted
+// per device: the first live handle saves the previous limit and raises it to
+// the maximum, the last one to be freed resets the persisting lines
+// (cudaCtxResetPersistingL2Cache) and restores the saved limit.
+// ARGCSR_L2_PERSIST=0 leaves the limit alone (the window then only uses what
+// the application already set aside).  Documented in include/argcsr_gpu.h.
+struct L2PersistState {
+    int users = 0;
+    size_t saved = 0;
     size_t granted = 0;
-    if (persist_max > 0) {
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(persist_max)) == cudaSuccess) {
-            CUDA_OK(cudaDeviceGetLimit(&granted, cudaLimitPersistingL2CacheSize));
-        } else {
-            cudaGetLastError();
+};
+std::mutex g_l2_mu;
+L2PersistState g_l2[64];
+
+size_t acquire_l2_persist(int device, bool* counted) {
+    *counted = false;
+    if (device < 0 || device >= 64) return 0;
+    std::lock_guard<std::mutex> lock(g_l2_mu);
+    L2PersistState& st = g_l2[device];
+    if (!argcsr_gpu::knobs().l2_persist) {
+        size_t cur = 0;
+        if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess) cudaGetLastError();
+        return cur;
+    }
+    if (st.users == 0) {
+        int persist_max = 0;
+        CUDA_OK(cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, device));
+        st.saved = 0;
+        st.granted = 0;
+        if (cudaDeviceGetLimit(&st.saved, cudaLimitPersistingL2CacheSize) != cudaSuccess) cudaGetLastError();
+        if (persist_max > 0) {
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(persist_max)) == cudaSuccess) {
+                CUDA_OK(cudaDeviceGetLimit(&st.granted, cudaLimitPersistingL2CacheSize));
+            } else {
+                cudaGetLastError();
+                st.granted = st.saved;
+            }
         }
     }
-    if (device < 64) done[device] = (long long)granted;
-    return granted;
+    ++st.users;
+    *counted = true;
+    return st.granted;
 }
+
+void release_l2_persist(int device) {
+    std::lock_guard<std::mutex> lock(g_l2_mu);
+    L2PersistState& st = g_l2[device];
+    if (st.users <= 0 || --st.users > 0) return;
+    if (cudaCtxResetPersistingL2Cache() != cudaSuccess) cudaGetLastError();
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, st.saved) != cudaSuccess) cudaGetLastError();
+}
+
+// Serialises the SpMVs of one handle (see argcsr_dev::mu): wait for the
+// previous SpMV on this handle, then record the end of this one.
+struct SpmvSerial {
+    argcsr_dev* m;
+    cudaStream_t s;
+    std::unique_lock<std::mutex> lock;
+    SpmvSerial(const argcsr_dev* mc, cudaStream_t st) : m(const_cast<argcsr_dev*>(mc)), s(st), lock(m->mu) {
+        if (m->spmv_issued) CUDA_OK(cudaStreamWaitEvent(s, m->ev_done, 0));
+    }
+    void done() {
+        CUDA_OK(cudaEventRecord(m->ev_done, s));
+        m->spmv_issued = true;
+    }
+};
 
 // A fresh handle with the per-handle resources (aux stream, events, L2 window
 // limits); freed by free_handle on any failure of the caller.
@@ -147,7 +232,7 @@ argcsr_dev* new_handle(int device, argcsr_dtype dtype, uint64_t rows, uint64_t c
                      : (flags & ARGCSR_XREMAP_OFF) ? argcsr_gpu::kXRemapOff
                                                    : argcsr_gpu::kXRemapAuto;
     try {
-        m->l2_persist_max = ensure_l2_persist(device);
+        m->l2_persist_max = acquire_l2_persist(device, &m->holds_l2_persist);
         CUDA_OK(cudaDeviceGetAttribute(&m->l2_window_max, cudaDevAttrMaxAccessPolicyWindowSize, device));
         {
             // The heavy groups' stream runs at the highest priority: whenever an
@@ -157,12 +242,11 @@ argcsr_dev* new_handle(int device, argcsr_dtype dtype, uint64_t rows, uint64_t c
             // 0.39 -> 0.51).  Experiments: ARGCSR_AUX_PRIO=lo|def.
             int lo = 0, hi = 0;
             CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            const char* e = std::getenv("ARGCSR_AUX_PRIO");
-            const int prio = !e ? hi : (e[0] == 'h' ? hi : e[0] == 'l' ? lo : 0);
+            const char ap = argcsr_gpu::knobs().aux_prio;
+            const int prio = ap == 'h' ? hi : ap == 'l' ? lo : 0;
             CUDA_OK(cudaStreamCreateWithPriority(&m->aux, cudaStreamNonBlocking, prio));
         }
-        CUDA_OK(cudaMalloc(&m->sched, 2 * sizeof(uint32_t)));
-        CUDA_OK(cudaMemset(m->sched, 0, 2 * sizeof(uint32_t)));
+        CUDA_OK(cudaEventCreateWithFlags(&m->ev_done, cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
         CUDA_OK(cudaStreamCreateWithFlags(&m->h2d, cudaStreamNonBlocking));
@@ -391,7 +475,9 @@ argcsr_status argcsr_dev_spmv(const argcsr_dev* m, const void* x, void* y, void*
         check_handle(m);
         if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv: null vector");
         DeviceScope scope(m->device);
-        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, static_cast<cudaStream_t>(stream));
+        SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
+        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s);
+        serial.done();
     });
 }
 
@@ -401,7 +487,9 @@ argcsr_status argcsr_dev_spmv_scaled(const argcsr_dev* m, const void* x, const d
         check_handle(m);
         if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_scaled: null vector");
         DeviceScope scope(m->device);
-        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, static_cast<cudaStream_t>(stream), x_scale);
+        SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
+        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s, x_scale);
+        serial.done();
     });
 }
 
@@ -411,7 +499,9 @@ argcsr_status argcsr_dev_spmv_groups(const argcsr_dev* m, const void* x, uint64_
         check_handle(m);
         if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_groups: null vector");
         DeviceScope scope(m->device);
-        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream));
+        SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s);
+        serial.done();
     });
 }
 
@@ -422,8 +512,10 @@ argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, const doubl
         if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_ex: null vector");
         if (flags & ~uint32_t(ARGCSR_SPMV_REUSE_X)) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_ex: unknown flags");
         DeviceScope scope(m->device);
-        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream), x_scale,
+        SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s, x_scale,
                                 (flags & ARGCSR_SPMV_REUSE_X) != 0);
+        serial.done();
     });
 }
 
@@ -439,8 +531,10 @@ argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const dou
         for (uint32_t q = 0; q < npeers; ++q)
             if (!peer_y[q]) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null peer buffer");
         DeviceScope scope(m->device);
-        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, static_cast<cudaStream_t>(stream), x_scale,
+        SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s, x_scale,
                                 (flags & ARGCSR_SPMV_REUSE_X) != 0, peer_y, npeers, peer_rows);
+        serial.done();
     });
 }
 
@@ -522,7 +616,11 @@ argcsr_status argcsr_dev_spmv_host(const argcsr_dev* m, const void* x, uint64_t 
         } fr{&dx, &dy, s};
         CUDA_OK(cudaMallocAsync(&dy, m->num_rows * es, s));
         if (x_len) CUDA_OK(cudaMemcpyAsync(dx, x, x_len * es, cudaMemcpyHostToDevice, s));
-        argcsr_gpu::spmv_launch(m, dx, dy, 0, m->num_groups, s);
+        {
+            SpmvSerial serial(m, s);
+            argcsr_gpu::spmv_launch(m, dx, dy, 0, m->num_groups, s);
+            serial.done();
+        }
         CUDA_OK(cudaMemcpyAsync(y, dy, m->num_rows * es, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
     });
@@ -550,8 +648,7 @@ argcsr_status argcsr_dev_spmv_host_async(const argcsr_dev* mc, const void* x_hos
         // upload (copy engine 1) once the SpMV that last read this x buffer is done
         // each copy in two halves on two copy streams (C2 e2e 0.73 -> 0.70 ms per
         // step; ARGCSR_ASYNC_SPLIT=0 keeps one stream per direction)
-        const char* sp = std::getenv("ARGCSR_ASYNC_SPLIT");
-        const bool split = !(sp && sp[0] == '0');
+        const bool split = argcsr_gpu::knobs().async_split;
         if (split && !m->as_h2d2) {
             CUDA_OK(cudaStreamCreateWithFlags(&m->as_h2d2, cudaStreamNonBlocking));
             CUDA_OK(cudaStreamCreateWithFlags(&m->as_d2h2, cudaStreamNonBlocking));
@@ -578,8 +675,11 @@ argcsr_status argcsr_dev_spmv_host_async(const argcsr_dev* mc, const void* x_hos
         if (m->as_used[b]) CUDA_OK(cudaStreamWaitEvent(s, m->as_down[b], 0));
         // one SpMV in flight per handle (x' buffer, heavy-group stream), even
         // when consecutive calls name different streams
-        if (m->as_used[b ^ 1]) CUDA_OK(cudaStreamWaitEvent(s, m->as_mv[b ^ 1], 0));
-        argcsr_gpu::spmv_launch(m, m->as_x[b], m->as_y[b], 0, m->num_groups, s);
+        {
+            SpmvSerial serial(m, s);
+            argcsr_gpu::spmv_launch(m, m->as_x[b], m->as_y[b], 0, m->num_groups, s);
+            serial.done();
+        }
         CUDA_OK(cudaEventRecord(m->as_mv[b], s));
         // download (copy engine 2)
         CUDA_OK(cudaStreamWaitEvent(m->d2h, m->as_mv[b], 0));
@@ -616,9 +716,11 @@ argcsr_status argcsr_dev_spmv_host_staged(const argcsr_dev* m, const void* x_hos
         DeviceScope scope(m->device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const size_t es = elem_size(m->dtype);
+        SpmvSerial serial(m, s);
         if (m->tile_cmax.empty() || m->lanes_per_unit != 4 || m->num_cols == 0) {
             CUDA_OK(cudaMemcpyAsync(x_dev, x_host, m->num_cols * es, cudaMemcpyHostToDevice, s));
             argcsr_gpu::spmv_launch(m, x_dev, y_dev, 0, m->num_groups, s);
+            serial.done();
             CUDA_OK(cudaMemcpyAsync(y_host, y_dev, m->num_rows * es, cudaMemcpyDeviceToHost, s));
             CUDA_OK(cudaStreamSynchronize(s));
             return;
@@ -655,6 +757,7 @@ argcsr_status argcsr_dev_spmv_host_staged(const argcsr_dev* m, const void* x_hos
                 CUDA_OK(cudaMemcpyAsync(static_cast<char*>(y_host) + r0 * es, static_cast<const char*>(y_dev) + r0 * es,
                                         (r1 - r0) * es, cudaMemcpyDeviceToHost, m->d2h));
         }
+        serial.done();
         CUDA_OK(cudaStreamSynchronize(m->d2h));
         CUDA_OK(cudaStreamSynchronize(s));
     });
@@ -1007,7 +1110,8 @@ argcsr_status argcsr_dev_read_binary(const char* path, uint64_t tpg, uint64_t dc
             std::vector<double> vals = r.array<double>();
             std::vector<int32_t> cols = r.array<int32_t>();
             std::vector<uint64_t> rp = r.array<uint64_t>();
-            if (rp.size() != v.num_rows + 1 || vals.size() != cols.size() || rp.back() > vals.size())
+            if (v.num_rows == UINT64_MAX || rp.empty() || rp.size() != v.num_rows + 1 || vals.size() != cols.size() ||
+                rp.front() > rp.back() || rp.back() > vals.size())
                 fail(ARGCSR_E_FORMAT, "binary: inconsistent CSR arrays");
             v.nnz = rp.back() - rp.front();
             v.row_pointers = rp.data();

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -76,6 +77,28 @@ constexpr uint32_t kMaxPeers = 7;
 constexpr int kTileThreads = 256;
 constexpr int kDefaultTileUnits = 512;
 
+// Experiment switches, read from the environment ONCE per process (first
+// use) -- never on a launch path.  Defaults are the measured-best settings
+// (DESIGN.md §4); -1 means "library decides".
+struct Knobs {
+    bool l2_window = true;        // ARGCSR_L2_WINDOW=0: no persisting access-policy window for x
+    bool l2_persist = true;       // ARGCSR_L2_PERSIST=0: do not raise the device's persisting-L2 limit
+    int x_evict_last = 1;         // ARGCSR_XPOL: x gathers L2 evict_last (1) / evict_normal (0)
+    int stream_evict_first = 0;   // ARGCSR_SPOL: values/columns L2 evict_first (1) / evict_normal (0)
+    int map = -1;                 // ARGCSR_MAP: unit/row -> group maps in shared memory (1/0)
+    int pair = 1;                 // ARGCSR_PAIR=0: never the paired-unit light kernel
+    int light_dyn = -1;           // ARGCSR_LIGHT_DYN: warp-granular dynamic light units (1/0)
+    size_t heavy_smem = 0;        // ARGCSR_HEAVY_SMEM: pad heavy CTAs' shared memory (bytes)
+    char heavy_u = 0;             // ARGCSR_HEAVY_U: '4' | '8' | '1'(6) element steps in flight
+    char heavy_b = 0;             // ARGCSR_HEAVY_B: '5' = 5 CTAs/SM for the fp64 heavy kernel
+    bool heavy_runs = false;      // ARGCSR_HEAVY_RUNS=1: vector x loads over consecutive columns
+    char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
+    bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
+    int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)
+    int ulen = -1;                // ARGCSR_ULEN: per-unit lengths (1/0)
+};
+const Knobs& knobs();
+
 }  // namespace argcsr_gpu
 
 // Opaque handle behind argcsr_dev* (immutable after conversion).
@@ -128,7 +151,14 @@ struct argcsr_dev {
     // Heavy groups run on an auxiliary stream forked from the caller's stream.
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    uint32_t* sched = nullptr;            // [2] dynamic tile counter + done counter (self-resetting)
+    // One SpMV in flight per handle: the x' buffer, the auxiliary stream and
+    // the fork/join events are handle state, so every SpMV entry point waits
+    // for the previous SpMV on this handle (whatever stream it ran on) and
+    // records ev_done after its own (capi.cu SpmvSerial).
+    std::mutex mu;
+    cudaEvent_t ev_done = nullptr;
+    bool spmv_issued = false;
+    bool holds_l2_persist = false;        // counted in the device's persisting-L2 users (capi.cu)
 
     uint64_t light_slots = 0;             // stored slots of light groups (stored first)
 

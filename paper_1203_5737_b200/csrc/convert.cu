@@ -583,8 +583,7 @@ __global__ void __launch_bounds__(256) k5_from_reference(const GroupDesc* __rest
 // Units per light tile (default kDefaultTileUnits; a tile is one CTA of kTileThreads).
 // ARGCSR_TILE_THREADS (128 .. 2048) sets the units per tile (experiments).
 uint64_t tile_threads_setting() {
-    const char* e = std::getenv("ARGCSR_TILE_THREADS");
-    const long v = e ? std::atol(e) : 0;
+    const long v = knobs().tile_threads;
     return (v >= 128 && v <= 2048 && v % 128 == 0) ? uint64_t(v) : uint64_t(kDefaultTileUnits);
 }
 
@@ -880,8 +879,8 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         CUDA_OK(cudaMemcpyAsync(r, rd.p, sizeof r, cudaMemcpyDeviceToHost, s));
         CUDA_OK(cudaStreamSynchronize(s));
         m->unit_len_saved = (r[1] - r[0]) * (sizeof(T) + sizeof(int32_t));
-        const char* e = std::getenv("ARGCSR_ULEN");  // experiments: force 1 / 0
-        const bool keep = e ? e[0] == '1' : m->unit_len_saved > 4 * total_units;
+        const int fu = knobs().ulen;  // experiments: force 1 / 0
+        const bool keep = fu >= 0 ? fu == 1 : m->unit_len_saved > 4 * total_units;
         if (!keep) {
             CUDA_OK(cudaFree(m->ulen));
             m->device_bytes -= total_units;

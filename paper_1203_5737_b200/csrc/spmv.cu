@@ -532,201 +532,10 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     }
 }
 
-// ---------------------------------------------------------- cp.async helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// --------------------------------------- persistent light path (prefetched metadata)
-// Same per-tile work as spmv_light_kernel, but each CTA walks tiles k,
-// k+gridDim.x, ... and prefetches the NEXT tile's group descriptors and unit
-// bases into a second shared-memory buffer with cp.async while the current
-// tile streams, so the two dependent metadata round trips leave the critical
-// path (the tiles[] entries are fetched one more tile ahead into registers).
-__device__ __forceinline__ uint32_t find_le64(const uint64_t* arr, uint32_t n, uint64_t key) {
-    uint32_t lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) / 2;
-        if (arr[mid] <= key) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-__device__ __forceinline__ uint32_t find_row(const GroupDesc* d, uint32_t n, uint32_t row) {
-    uint32_t lo = 0, hi = n - 1;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) / 2;
-        if (d[mid].first_row <= row) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
-__global__ void __launch_bounds__(kTileThreads, MINB) spmv_lightp_kernel(const SpmvArgs<T> a, uint32_t num_tiles,
-                                                                        uint32_t* __restrict__ sched) {
-    // sched[0]: next dynamic tile (offset by gridDim.x), sched[1]: CTAs done;
-    // the last CTA to finish resets both, so consecutive launches reuse them.
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_grab[2];  // alternating slots: written one sync after the last read
-    double* s_part = reinterpret_cast<double*>(smem);
-    const uint32_t cap = a.max_tile_groups;
-    const size_t part_bytes = (size_t(a.max_tile_units) * V * sizeof(double) + 15) & ~size_t(15);
-    unsigned char* mbase = smem + part_bytes;
-    const size_t meta_bytes = ((size_t(cap) + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15);
-    auto meta_desc = [&](int b) { return reinterpret_cast<GroupDesc*>(mbase + b * meta_bytes); };
-    auto meta_ub = [&](int b) { return reinterpret_cast<uint64_t*>(meta_desc(b) + cap + 1); };
-    const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
-    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const double xs = a.x_scale ? *a.x_scale : 1.0;
-    const uint32_t tid = threadIdx.x;
-    auto issue_meta = [&](uint32_t gs, uint32_t ge, int b) {
-        for (uint32_t i = tid; i <= ge - gs; i += blockDim.x) {
-            cp_async16(smem_u32(meta_desc(b) + i), a.groups + gs + i, pol_x);
-            cp_async8(smem_u32(meta_ub(b) + i), a.unit_base + gs + i);
-        }
-    };
-    // Tile order: static round-robin (k += gridDim.x; neighbouring tiles run
-    // concurrently, which keeps stencil x windows hot in L2) or dynamic.
-    uint32_t static_next = blockIdx.x;
-    auto grab = [&]() {
-        if constexpr (DYN) return gridDim.x + atomicAdd(sched, 1u);
-        static_next += gridDim.x;
-        return static_next;
-    };
-
-    uint32_t k = blockIdx.x, it = 0;
-    if (tid == 0) s_grab[0] = grab();
-    uint32_t gs = 0, ge = 0;
-    if (k < num_tiles) {
-        gs = a.tiles[k], ge = a.tiles[k + 1];
-        issue_meta(gs, ge, 0);
-    }
-    cp_commit();
-    cp_wait<0>();
-    __syncthreads();
-    uint32_t kn = s_grab[0], gsn = 0, gen = 0;
-    if (kn < num_tiles) gsn = a.tiles[kn], gen = a.tiles[kn + 1];
-    int mb = 0;
-    while (k < num_tiles) {
-        const bool has_next = kn < num_tiles;
-        if (has_next) issue_meta(gsn, gen, mb ^ 1);
-        cp_commit();
-        if (tid == 0) s_grab[(it + 1) & 1] = has_next ? grab() : num_tiles;
-
-        const uint32_t ng = ge - gs;
-        const GroupDesc* md = meta_desc(mb);
-        const uint64_t* mub = meta_ub(mb);
-        const bool live = ng > 0 && !(ge <= a.g_begin || gs >= a.g_end);
-        const uint64_t ub0 = mub[0];
-        const uint32_t row0 = md[0].first_row, row_end = live ? md[ng].first_row : row0;
-
-        // phase-2 metadata of this thread's first row (registers)
-        const uint32_t pr = row0 + tid;
-        uint32_t pgi = 0, pb = 0, pe = 0;
-        bool pvalid = false;
-        if (pr < row_end) {
-            pgi = find_row(md, ng, pr);
-            const uint32_t g = gs + pgi;
-            pvalid = !md[pgi].heavy() && g >= a.g_begin && g < a.g_end;
-            if (pvalid) {
-                pb = pr == md[pgi].first_row ? 0u : uint32_t(a.tm[pr - 1]);
-                pe = uint32_t(a.tm[pr]);
-            }
-        }
-        const uint32_t nunits = live ? uint32_t(mub[ng] - ub0) : 0u;
-        for (uint32_t u = tid; u < nunits; u += blockDim.x) {
-            const uint32_t gi = find_le64(mub, ng, ub0 + u);
-            const uint32_t g = gs + gi;
-            const GroupDesc d = md[gi];
-            if (d.heavy() || g < a.g_begin || g >= a.g_end) continue;
-            double sacc[V];
-            phase1<T, V, U, PRED>(a, d.offset() + (ub0 + u - mub[gi]) * V, d.chunk, d.stride(), sacc, pol_stream,
-                                  pol_x, xs);
-#pragma unroll
-            for (int l = 0; l < V; ++l) s_part[size_t(u) * V + l] = sacc[l];
-        }
-        cp_wait<0>();
-        __syncthreads();
-        const uint32_t k2 = s_grab[(it + 1) & 1];  // tile after next: its tiles[] entries load under phase 2
-        uint32_t gs2 = 0, ge2 = 0;
-        if (k2 < num_tiles) gs2 = a.tiles[k2], ge2 = a.tiles[k2 + 1];
-
-        if (pvalid) store_y<false>(a, pr, row_sum(s_part + size_t(mub[pgi] - ub0) * V, pb, pe));
-        for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
-            const uint32_t gi = find_row(md, ng, r);
-            const uint32_t g = gs + gi;
-            if (md[gi].heavy() || g < a.g_begin || g >= a.g_end) continue;
-            const uint32_t b = r == md[gi].first_row ? 0u : uint32_t(a.tm[r - 1]);
-            store_y<false>(a, r, row_sum(s_part + size_t(mub[gi] - ub0) * V, b, uint32_t(a.tm[r])));
-        }
-        __syncthreads();
-        k = kn, gs = gsn, ge = gen;
-        kn = k2, gsn = gs2, gen = ge2;
-        mb ^= 1;
-        ++it;
-    }
-    if (DYN && tid == 0) {
-        __threadfence();
-        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
-            sched[0] = 0;
-            sched[1] = 0;
-            __threadfence();
-        }
-    }
-}
-
-size_t lightp_smem_bytes(const argcsr_dev* m, int V) {
-    const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
-    return ((size_t(m->max_tile_units) * V * sizeof(double) + 15) & ~size_t(15)) +
-           2 * (((cap + 1) * (sizeof(GroupDesc) + sizeof(uint64_t)) + 15) & ~size_t(15));
-}
-
-template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
-void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s);
-
-
 size_t light_smem_bytes(const argcsr_dev* m, int V, bool map = false) {
     const size_t cap = std::max<uint32_t>(m->max_tile_groups, 1);
     return size_t(m->max_tile_units) * V * sizeof(double) + cap * sizeof(uint64_t) + (cap + 1) * 4 * 2 + cap * 4 +
            (map ? (size_t(m->max_tile_units) + m->max_tile_rows) * sizeof(uint16_t) : 0);
-}
-
-bool l2_window_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("ARGCSR_L2_WINDOW");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-// Kernel variant for experiments: ARGCSR_SPMV_VARIANT = U<unroll>P<pred>B<min CTAs/SM>,
-// one of the instantiated set below.
-int variant_id() {
-    static const int id = [] {
-        const char* e = std::getenv("ARGCSR_SPMV_VARIANT");
-        if (!e) return -1;
-        const char* names[] = {"LP4P1B4", "U2P1B6", "U4P0B4", "U4P1B5", "U4P1B3", "U8P1B2", "U4P1B4", "U2P1B8",
-                               "U8P0B2", "U8P0B3", "LP4P0B4", "LP2P1B6", "LPD4P1B4", "LPD4P0B4", "LPD2P0B6",
-                               "U6P0B3", "U4P0B5", "U3P0B5", "U4P0B6"};
-        for (int i = 0; i < 19; ++i)
-            if (!std::strcmp(e, names[i])) return i;
-        return -1;
-    }();
-    return id;
-}
-
-int env_flag(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? (e[0] != '0') : dflt;
 }
 
 template <typename K, typename T>
@@ -741,7 +550,7 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
     cudaLaunchAttribute attr[1];
     cfg.numAttrs = 0;
     const size_t xbytes = m->n_used * sizeof(T);  // x, or x' = x[perm] (xremap.cu)
-    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
+    if (knobs().l2_window && m->l2_persist_max > 0 && xbytes > 0) {
         // Persist the leading part of x that fits the carve-out (hit ratio 1):
         // all of x for the stencils; the hot low-index columns of R-MAT.
         const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
@@ -761,11 +570,10 @@ template <typename T, int V, int U, bool PRED, int MINB, bool PEER = false>
 void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // small groups (units + rows per group, on average): fill the maps, else search
     const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
-    const char* e = std::getenv("ARGCSR_MAP");  // experiments: force 1 / 0
-    const bool map = e ? e[0] == '1' : per_group <= 24.0;
+    const int fm = knobs().map;  // experiments: force 1 / 0
+    const bool map = fm >= 0 ? fm == 1 : per_group <= 24.0;
     // every light chunk <= U/2 and at most two units per thread: pair them
-    const char* pe = std::getenv("ARGCSR_PAIR");  // experiments: 0 = never
-    const bool pair = !(pe && pe[0] == '0') && m->max_light_chunk <= uint32_t(U / 2) &&
+    const bool pair = knobs().pair != 0 && m->max_light_chunk <= uint32_t(U / 2) &&
                       m->max_tile_units <= 2 * uint64_t(kTileThreads);
     if (pair) {  // (twice the loads in flight per thread: 64 registers, 4 CTAs/SM)
         if (map)
@@ -774,8 +582,7 @@ void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
         else
             launch(spmv_light_kernel<T, V, U, PRED, 4, false, PEER, true>, m->num_tiles, light_smem_bytes(m, V), m, a,
                    s);
-    } else if (const char* dw = std::getenv("ARGCSR_LIGHT_DYN");
-               !PEER && (dw ? dw[0] == '1' : m->num_heavy > 0)) {
+    } else if (!PEER && (knobs().light_dyn >= 0 ? knobs().light_dyn == 1 : m->num_heavy > 0)) {
         // power-law matrices (heavy groups present, light chunks of every
         // size): warps take 32-unit chunks dynamically (C3 +2%; C2 -3%, so
         // not for stencils).  ARGCSR_LIGHT_DYN=0|1 forces it (experiments).
@@ -793,78 +600,15 @@ void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     }
 }
 
-template <typename T, int V, int U, bool PRED, int MINB, bool DYN>
-void launch_lightp(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    int dev = 0, sms = 0;
-    CUDA_OK(cudaGetDevice(&dev));
-    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = lightp_smem_bytes(m, V);
-    auto kern = spmv_lightp_kernel<T, V, U, PRED, MINB, DYN>;
-    if (smem > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileThreads, smem));
-    const unsigned grid = unsigned(std::min<uint64_t>(m->num_tiles, uint64_t(std::max(per_sm, 1)) * sms));
-    if (grid == 0) return;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kTileThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    cfg.numAttrs = 0;
-    const size_t xbytes = m->n_used * sizeof(T);  // x, or x' = x[perm] (xremap.cu)
-    if (l2_window_enabled() && m->l2_persist_max > 0 && xbytes > 0) {
-        const size_t win = std::min<size_t>({xbytes, size_t(m->l2_window_max), m->l2_persist_max});
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<T*>(a.x);
-        attr[0].val.accessPolicyWindow.num_bytes = win;
-        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
-    CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a, m->num_tiles, m->sched));
-}
-
 template <typename T, int V>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
         launch_light<T, V, 4, false, 5, true>(m, a, s);
         return;
     }
-    int vid = variant_id();
-    if (vid < 0) {
-        // Default: hardware-dispatched tiles, unpredicated value loads, 5 CTAs
-        // per SM (measured best on C2-C4 with the lane-compact layout,
-        // scripts/sweep.sh).
-        vid = 16;
-    }
-    switch (vid) {
-        case 0: launch_lightp<T, V, 4, true, 4, false>(m, a, s); return;
-        case 10: launch_lightp<T, V, 4, false, 4, false>(m, a, s); return;
-        case 11: launch_lightp<T, V, 2, true, 6, false>(m, a, s); return;
-        case 12: launch_lightp<T, V, 4, true, 4, true>(m, a, s); return;
-        case 13: launch_lightp<T, V, 4, false, 4, true>(m, a, s); return;
-        case 14: launch_lightp<T, V, 2, false, 6, true>(m, a, s); return;
-        default: break;
-    }
-    switch (vid) {
-        case 1: launch_light<T, V, 2, true, 6>(m, a, s); break;
-        case 2: launch_light<T, V, 4, false, 4>(m, a, s); break;
-        case 3: launch_light<T, V, 4, true, 5>(m, a, s); break;
-        case 4: launch_light<T, V, 4, true, 3>(m, a, s); break;
-        case 5: launch_light<T, V, 8, true, 2>(m, a, s); break;
-        case 6: launch_light<T, V, 4, true, 4>(m, a, s); break;
-        case 7: launch_light<T, V, 2, true, 8>(m, a, s); break;
-        case 8: launch_light<T, V, 8, false, 2>(m, a, s); break;
-        case 9: launch_light<T, V, 8, false, 3>(m, a, s); break;
-        case 15: launch_light<T, V, 6, false, 3>(m, a, s); break;
-        case 16: launch_light<T, V, 4, false, 5>(m, a, s); break;
-        case 17: launch_light<T, V, 3, false, 5>(m, a, s); break;
-        case 18: launch_light<T, V, 4, false, 6>(m, a, s); break;
-        default: launch_light<T, V, 4, true, 4>(m, a, s); break;
-    }
+    // hardware-dispatched tiles, unpredicated value loads, 5 CTAs per SM
+    // (measured best on C2-C4 with the lane-compact layout)
+    launch_light<T, V, 4, false, 5>(m, a, s);
 }
 
 template <typename T>
@@ -899,10 +643,10 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
     a.max_tile_rows = m->max_tile_rows;
     a.tile0 = 0;
     a.max_tile_units = uint32_t(m->max_tile_units);
-    a.x_evict_last = env_flag("ARGCSR_XPOL", 1);
+    a.x_evict_last = knobs().x_evict_last;
     // values/columns: L2 evict_normal (evict_first measured slower once the heavy
     // stream is prioritised: C4 0.69 vs 0.73, C3 0.323 vs 0.325); ARGCSR_SPOL=1 for A/B
-    a.stream_evict_first = env_flag("ARGCSR_SPOL", 0);
+    a.stream_evict_first = knobs().stream_evict_first;
 
     // Heavy groups run concurrently on the handle's auxiliary stream (forked
     // from and joined back into `s`), launched first so their CTAs start first.
@@ -915,29 +659,28 @@ void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, voi
         size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
         // experiments: pad the heavy CTAs' shared memory so fewer of them fit
         // an SM and light tiles co-reside (ARGCSR_HEAVY_SMEM bytes)
-        if (const char* e = std::getenv("ARGCSR_HEAVY_SMEM")) smem = std::max<size_t>(smem, size_t(std::atol(e)));
+        smem = std::max<size_t>(smem, knobs().heavy_smem);
         // Default: scalar x gathers; fp64 8 element steps in flight per lane at
         // 4 CTAs/SM, fp32 4 steps at 6 CTAs/SM (measured best on C3/C4,
         // DESIGN.md §4).  Experiments: ARGCSR_HEAVY_U = 4 | 8 | 16 (steps),
         // ARGCSR_HEAVY_B = min CTAs/SM for U=8 (4 | 5), ARGCSR_HEAVY_RUNS=1:
         // vector loads of 2 / 4 x entries where a lane's stored columns run
         // consecutively (needs x aligned to 4 entries; x' always is).
-        const char* uh = std::getenv("ARGCSR_HEAVY_U");
-        const char* hb = std::getenv("ARGCSR_HEAVY_B");
-        const char* hr = std::getenv("ARGCSR_HEAVY_RUNS");
+        const char uh0 = knobs().heavy_u, hb0 = knobs().heavy_b;
+        const bool hr = knobs().heavy_runs;
         const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
         cudaStream_t hs = fork ? m->aux : s;
         if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
             if (sizeof(T) == sizeof(float)) launch(spmv_heavy_kernel<T, 4, false, 6, true>, m->heavy_ctas, smem, m, a, hs);
             else launch(spmv_heavy_kernel<T, 8, false, 4, true>, m->heavy_ctas, smem, m, a, hs);
-        } else if (hr && hr[0] == '1' && aligned) {
-            if (uh && uh[0] == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
+        } else if (hr && aligned) {
+            if (uh0 == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
             else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
-        } else if (uh && uh[0] == '1') {
+        } else if (uh0 == '1') {
             launch(spmv_heavy_kernel<T, 16, false, 2>, m->heavy_ctas, smem, m, a, hs);
-        } else if (uh ? uh[0] == '4' : sizeof(T) == sizeof(float)) {
+        } else if (uh0 ? uh0 == '4' : sizeof(T) == sizeof(float)) {
             launch(spmv_heavy_kernel<T, 4, false, 6>, m->heavy_ctas, smem, m, a, hs);
-        } else if ((hb && hb[0] == '5') || sizeof(T) == sizeof(float)) {
+        } else if (hb0 == '5' || sizeof(T) == sizeof(float)) {
             launch(spmv_heavy_kernel<T, 8, false, 5>, m->heavy_ctas, smem, m, a, hs);
         } else {
             launch(spmv_heavy_kernel<T, 8, false, 4>, m->heavy_ctas, smem, m, a, hs);

@@ -3,9 +3,13 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -96,8 +100,59 @@ struct Knobs {
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)
     int ulen = -1;                // ARGCSR_ULEN: per-unit lengths (1/0)
+    bool trace = false;           // ARGCSR_TRACE=1: per-phase host timings of the converter on stderr
 };
 const Knobs& knobs();
+
+// NVTX range (visible in Nsight Systems / ncu --nvtx; free when no tool is
+// attached) plus, with ARGCSR_TRACE=1 and sync_timer, a synchronising
+// wall-clock timer of the phase on stderr (conversion phases only: never on
+// the SpMV path).
+struct Phase {
+    const char* name;
+    cudaStream_t s;
+    bool timed;
+    std::chrono::steady_clock::time_point t0;
+    Phase(const char* n, cudaStream_t st, bool sync_timer = false)
+        : name(n), s(st), timed(sync_timer && knobs().trace) {
+        nvtxRangePushA(n);
+        if (timed) {
+            cudaStreamSynchronize(s);
+            t0 = std::chrono::steady_clock::now();
+        }
+    }
+    ~Phase() {
+        if (timed) {
+            cudaStreamSynchronize(s);
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            std::fprintf(stderr, "[argcsr trace] %-28s %9.3f ms\n", name, ms);
+        }
+        nvtxRangePop();
+    }
+    Phase(const Phase&) = delete;
+    Phase& operator=(const Phase&) = delete;
+};
+
+// Consecutive phases of one routine: next() closes the open phase and opens
+// the following one; end() (or scope exit) closes the last.
+struct PhaseSeq {
+    cudaStream_t s;
+    alignas(Phase) unsigned char buf[sizeof(Phase)];
+    bool open = false;
+    explicit PhaseSeq(cudaStream_t st) : s(st) {}
+    void end() {
+        if (open) reinterpret_cast<Phase*>(buf)->~Phase();
+        open = false;
+    }
+    void next(const char* n) {
+        end();
+        new (buf) Phase(n, s, true);
+        open = true;
+    }
+    ~PhaseSeq() { end(); }
+    PhaseSeq(const PhaseSeq&) = delete;
+    PhaseSeq& operator=(const PhaseSeq&) = delete;
+};
 
 }  // namespace argcsr_gpu
 

@@ -632,11 +632,15 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     const uint64_t budget = m->dcs * tpg;  // size_t product, wraps like argcsr.cpp:28
     const uint32_t N32 = uint32_t(N);
 
+    Phase whole("argcsr_convert", s, true);
+    PhaseSeq ph(s);
+    ph.next("convert.k1_next");
     // K1
     DevPtr<uint32_t> next(N, s);
     k1_next<<<grid_for(N, 256), 256, 0, s>>>(rp, N, tpg, budget, next.p);
     LAUNCH_OK("k1_next");
 
+    ph.next("convert.k2_partition");
     // K2
     DevPtr<uint32_t> first_row(N + 1, s);
     DevPtr<uint32_t> d_G(1, s);
@@ -665,6 +669,7 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
     k_set_u32<<<1, 1, 0, s>>>(first_row.p + G, N32);
     LAUNCH_OK("k_set_u32");
 
+    ph.next("convert.k3_assign");
     // K3
     TM* tm = dev_alloc<TM>(m, N);
     TM* assigned = dev_alloc<TM>(m, G);
@@ -678,6 +683,7 @@ void convert_typed(argcsr_dev* m, const uint64_t* rp, const int32_t* cols, const
         LAUNCH_OK("k3_assign");
     }
 
+    ph.end();
     layout_and_schedule<T, TM>(m, G, first_row.p, chunk.p, tm, assigned, LayoutSource<T>{rp, cols, vals}, s);
 }
 
@@ -689,6 +695,8 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
                          TM* assigned, const LayoutSource<T>& src, cudaStream_t s) {
     const uint64_t N = m->num_rows, tpg = m->tpg;
     const uint32_t N32 = uint32_t(N);
+    PhaseSeq ph(s);
+    ph.next("convert.k4_offsets");
     struct {
         const uint32_t* p;
     } chunk{chunk_p};
@@ -741,6 +749,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     m->stored_slots = stored_slots;
     m->light_slots = light_total;
 
+    ph.next("convert.k4_schedule");
     // SpMV schedule: work units (V lanes), light tiles, heavy groups (LPT order).
     m->lanes_per_unit = int(V);
     m->unit_base = dev_alloc<uint64_t>(m, uint64_t(G) + 1);
@@ -823,6 +832,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         m->max_tile_units = span + maxu - 1;
     }
 
+    ph.next("convert.k5_alloc");
     // K5
     m->values = dev_alloc<T>(m, stored_slots);
     m->columns = dev_alloc<int32_t>(m, stored_slots);
@@ -849,6 +859,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
                                             "padding must trail each lane)");
         m->nnz = h[0];
     } else {
+        ph.next("convert.xremap");
         // x remap (lane-compact only): stored columns index x' = x[perm]
         uint64_t rp_ends[2] = {0, 0};
         CUDA_OK(cudaMemcpyAsync(&rp_ends[0], src.rp, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -856,6 +867,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         CUDA_OK(cudaStreamSynchronize(s));
         col_map = build_xremap(m, src.cols + rp_ends[0], rp_ends[1] - rp_ends[0], m->xremap_mode, s, false, src.rp,
                                src.cols);
+        ph.next("convert.k5_layout");
         if (G > 0 && stored_slots > 0) {
             const unsigned grid = unsigned(std::min<uint64_t>(G, 0x7fffffffu));
             k5_layout<T, TM><<<grid, 256, 0, s>>>(src.rp, src.cols, src.vals, m->groups, tm, assigned, col_map, G,
@@ -865,6 +877,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         if (col_map) CUDA_OK(cudaFreeAsync(col_map, s));
     }
     CUDA_OK(cudaStreamSynchronize(s));
+    ph.next("convert.k6_unit_len");
     // Light unit lengths (u8, light chunks <= kHeavyChunk): kept when the
     // padding steps they let the SpMV skip outweigh their own reads.
     if (G > 0 && total_units > 0 && stored_slots > 0) {
@@ -887,6 +900,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
             m->ulen = nullptr;
         }
     }
+    ph.next("convert.tile_cmax");
     // pipelined host path: tile column reach (light tiles only; no heavy groups, no remap)
     if (m->num_heavy == 0 && !m->x_remap && m->num_tiles >= 16) {
         const uint32_t nt = m->num_tiles;

@@ -748,6 +748,7 @@ void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_beg
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
+    Phase range("argcsr_spmv", s);  // NVTX only
     x = reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
     if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s, peer_y, npeers, peer_rows);
     else launch_dtype<float>(m, x, x_scale, y, gb, ge, s, peer_y, npeers, peer_rows);

@@ -68,7 +68,7 @@ def build_lib(force: bool = False) -> Path:
 def build_ext(force: bool = False) -> Path:
     import pybind11
 
-    deps = [CSRC / "bindings.cpp", INCLUDE / "argcsr_gpu.hpp", INCLUDE / "argcsr_gpu.h", LIB]
+    deps = [CSRC / "bindings.cpp", CSRC / "host_io.hpp", INCLUDE / "argcsr_gpu.hpp", INCLUDE / "argcsr_gpu.h", LIB]
     if force or _stale(EXT, deps):
         py_inc = sysconfig.get_paths()["include"]
         cmd = ["g++", "-O2", "-std=c++20", "-shared", "-fPIC", "-fvisibility=hidden",

@@ -19,128 +19,12 @@
 #include <tuple>
 
 #include "argcsr_gpu.hpp"
+#include "host_io.hpp"
 
 namespace py = pybind11;
 using namespace argcsr_b200;
 
 namespace {
-
-// csr_from_triplets (core.hpp:48-49, core.cpp:7-48 semantics): bounds checks,
-// (row, col) sort, duplicates summed in sorted order, explicit zeros kept.
-struct Triplet {
-    std::size_t row, col;
-    double value;
-};
-
-CsrMatrix csr_from_triplets(std::size_t num_rows, std::size_t num_cols, std::vector<Triplet> entries) {
-    if (num_rows == 0 || num_cols == 0)
-        throw DimensionError("csr_from_triplets: matrix dimensions must be at least 1x1");
-    for (const Triplet& t : entries)
-        if (t.row >= num_rows || t.col >= num_cols)
-            throw BoundsError("csr_from_triplets: entry (" + std::to_string(t.row) + ", " + std::to_string(t.col) +
-                              ") outside " + std::to_string(num_rows) + "x" + std::to_string(num_cols));
-    std::sort(entries.begin(), entries.end(), [](const Triplet& a, const Triplet& b) {
-        return a.row != b.row ? a.row < b.row : a.col < b.col;
-    });
-    CsrMatrix A;
-    A.num_rows = num_rows;
-    A.num_cols = num_cols;
-    A.row_pointers.assign(num_rows + 1, 0);
-    for (std::size_t i = 0; i < entries.size();) {
-        double sum = entries[i].value;
-        std::size_t j = i + 1;
-        while (j < entries.size() && entries[j].row == entries[i].row && entries[j].col == entries[i].col)
-            sum += entries[j++].value;
-        A.values.push_back(sum);
-        A.columns.push_back(static_cast<index_t>(entries[i].col));
-        A.row_pointers[entries[i].row + 1] += 1;
-        i = j;
-    }
-    for (std::size_t r = 0; r < num_rows; ++r) A.row_pointers[r + 1] += A.row_pointers[r];
-    return A;
-}
-
-// ---------------------------------------------------------------- Matrix Market
-// read_matrix_market / write_matrix_market (proj/src/io.cpp:42-160): the
-// coordinate format, real / integer / pattern fields, general / symmetric /
-// skew-symmetric symmetry (mirrored off-diagonal entries, negated for skew),
-// 1-based indices, duplicates summed by csr_from_triplets; the same error
-// classes and messages.
-std::string lower(std::string s) {
-    for (char& c : s) c = char(std::tolower(static_cast<unsigned char>(c)));
-    return s;
-}
-
-bool next_data_line(std::istream& in, std::string& line) {
-    while (std::getline(in, line)) {
-        std::size_t i = 0;
-        while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
-        if (i == line.size() || line[i] == '%') continue;
-        return true;
-    }
-    return false;
-}
-
-CsrMatrix read_matrix_market(std::istream& in) {
-    std::string banner;
-    if (!std::getline(in, banner)) throw ParseError("matrix market: empty stream");
-    std::istringstream hs(banner);
-    std::string tag, object, format, field, symmetry;
-    hs >> tag >> object >> format >> field >> symmetry;
-    if (lower(tag) != "%%matrixmarket" || !hs) throw ParseError("matrix market: malformed header line");
-    object = lower(object), format = lower(format), field = lower(field), symmetry = lower(symmetry);
-    if (object != "matrix") throw UnsupportedError("matrix market: object '" + object + "' not supported");
-    if (format != "coordinate") {
-        if (format == "array") throw UnsupportedError("matrix market: array format not supported");
-        throw ParseError("matrix market: unknown format '" + format + "'");
-    }
-    const bool pattern = field == "pattern";
-    if (!pattern && field != "real" && field != "integer") {
-        if (field == "complex") throw UnsupportedError("matrix market: complex field not supported");
-        throw ParseError("matrix market: unknown field '" + field + "'");
-    }
-    const bool symmetric = symmetry == "symmetric", skew = symmetry == "skew-symmetric";
-    if (!symmetric && !skew && symmetry != "general") {
-        if (symmetry == "hermitian") throw UnsupportedError("matrix market: hermitian symmetry not supported");
-        throw ParseError("matrix market: unknown symmetry '" + symmetry + "'");
-    }
-    std::string line;
-    if (!next_data_line(in, line)) throw ParseError("matrix market: missing size line");
-    std::istringstream ss(line);
-    long long rows = 0, cols = 0, entries = 0;
-    if (!(ss >> rows >> cols >> entries) || rows < 0 || cols < 0 || entries < 0)
-        throw ParseError("matrix market: malformed size line '" + line + "'");
-    if (rows == 0 || cols == 0) throw ParseError("matrix market: matrix dimensions must be positive");
-    std::vector<Triplet> triplets;
-    triplets.reserve(std::size_t(entries) * (symmetric || skew ? 2 : 1));
-    for (long long k = 0; k < entries; ++k) {
-        if (!next_data_line(in, line))
-            throw ParseError("matrix market: expected " + std::to_string(entries) + " entries, got " +
-                             std::to_string(k));
-        std::istringstream es(line);
-        long long i = 0, j = 0;
-        double v = 1.0;
-        if (!(es >> i >> j)) throw ParseError("matrix market: malformed entry '" + line + "'");
-        if (!pattern && !(es >> v)) throw ParseError("matrix market: entry missing value '" + line + "'");
-        if (i < 1 || i > rows || j < 1 || j > cols)
-            throw BoundsError("matrix market: entry (" + std::to_string(i) + ", " + std::to_string(j) + ") outside " +
-                              std::to_string(rows) + "x" + std::to_string(cols));
-        const std::size_t r = std::size_t(i - 1), c = std::size_t(j - 1);
-        triplets.push_back({r, c, v});
-        if ((symmetric || skew) && r != c) triplets.push_back({c, r, skew ? -v : v});
-    }
-    return csr_from_triplets(std::size_t(rows), std::size_t(cols), std::move(triplets));
-}
-
-void write_matrix_market(std::ostream& out, const CsrMatrix& A) {
-    out << "%%MatrixMarket matrix coordinate real general\n";
-    out << A.num_rows << ' ' << A.num_cols << ' ' << A.nnz() << '\n';
-    out << std::setprecision(17);
-    for (std::size_t r = 0; r < A.num_rows; ++r)
-        for (std::size_t k = A.row_pointers[r]; k < A.row_pointers[r + 1]; ++k)
-            out << (r + 1) << ' ' << (A.columns[k] + 1) << ' ' << A.values[k] << '\n';
-    if (!out) throw IoError("matrix market: write failure");
-}
 
 template <typename T>
 py::array_t<T> view_of(const std::vector<T>& v, py::handle base) {
@@ -587,10 +471,10 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
         "csr_from_triplets",
         [](std::size_t num_rows, std::size_t num_cols,
            const std::vector<std::tuple<std::size_t, std::size_t, double>>& entries) {
-            std::vector<Triplet> ts;
+            std::vector<host_io::Entry> ts;
             ts.reserve(entries.size());
             for (const auto& [r, c, v] : entries) ts.push_back({r, c, v});
-            return csr_from_triplets(num_rows, num_cols, std::move(ts));
+            return host_io::assemble_csr(num_rows, num_cols, ts);
         },
         py::arg("num_rows"), py::arg("num_cols"), py::arg("entries"),
         "Builds CSR from (row, col, value) tuples; duplicates are summed.");
@@ -726,19 +610,11 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
 
     m.def(
         "read_matrix_market",
-        [](const std::string& path) {
-            std::ifstream in(path);
-            if (!in) throw IoError("cannot open '" + path + "' for reading");
-            return read_matrix_market(in);
-        },
+        [](const std::string& path) { return host_io::read_matrix_market_file(path); },
         py::arg("path"));
     m.def(
         "write_matrix_market",
-        [](const std::string& path, const CsrMatrix& A) {
-            std::ofstream out(path);
-            if (!out) throw IoError("cannot open '" + path + "' for writing");
-            write_matrix_market(out, A);
-        },
+        [](const std::string& path, const CsrMatrix& A) { host_io::write_matrix_market_file(path, A); },
         py::arg("path"), py::arg("matrix"));
 
     m.def(

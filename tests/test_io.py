@@ -234,3 +234,17 @@ def test_matrix_market_errors(argcsr, tmp_path, text, err):
         argcsr.read_matrix_market(str(p))
     with pytest.raises(argcsr.IoError):
         argcsr.read_matrix_market(str(tmp_path / "missing.mtx"))
+
+
+def test_csr_from_triplets_duplicate_order_matches_reference(argcsr, ref):
+    """Many duplicates in a large unsorted entry list: the duplicate sums
+    (whose rounding depends on the order the sort leaves equal keys in) are
+    bit-identical to the reference csr_from_triplets (core.cpp:7-48)."""
+    rng = np.random.default_rng(5)
+    for n, k in ((7, 40), (30, 5000), (200, 20000)):
+        ents = [(int(r), int(c), float(v)) for r, c, v in
+                zip(rng.integers(0, n, k), rng.integers(0, n, k), rng.uniform(-1, 1, k) * 10.0 ** rng.integers(-8, 8, k))]
+        A = argcsr.csr_from_triplets(n, n, ents)
+        R = ref.csr_from_triplets(n, n, ents)
+        assert np.array_equal(A.row_pointers, R.row_pointers) and np.array_equal(A.columns, R.columns)
+        assert A.values.tobytes() == R.values.tobytes()

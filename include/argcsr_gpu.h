@@ -365,6 +365,9 @@ ARGCSR_API argcsr_status argcsr_partition_rows(const uint64_t* row_pointers, uin
 ARGCSR_API const char* argcsr_last_error(void);
 ARGCSR_API const char* argcsr_status_name(argcsr_status s);
 ARGCSR_API int argcsr_abi_version(void);
+/* Experiment switches (ARGCSR_* environment variables) are read
+ * once, at first use; this re-reads them (tests flip them between cases). */
+ARGCSR_API void argcsr_reload_options(void);
 
 #ifdef __cplusplus
 }

@@ -234,6 +234,8 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
     m.attr("kDefaultDesiredChunkSize") = kDefaultDesiredChunkSize;
     m.attr("kPaddingColumn") = kPaddingColumn;
     m.def("abi_version", &argcsr_abi_version);
+    m.def("reload_options", &argcsr_reload_options,
+          "Re-read the ARGCSR_* experiment switches from the environment (read once otherwise).");
     // multi-GPU step over peer memory (argcsr_gpu.h: argcsr_peer_*)
     m.def(
         "peer_signal",

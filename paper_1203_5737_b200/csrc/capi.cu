@@ -2,6 +2,7 @@
 // reference (proj/src/argcsr.cpp:20-26, 220-223, 235-242); every failure is a
 // status code plus a thread-local message, never an exception across the ABI.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -21,36 +22,55 @@ using argcsr_gpu::fail;
 using argcsr_gpu::Failure;
 
 namespace argcsr_gpu {
+namespace {
+Knobs read_knobs() {
+    Knobs v;
+    auto flag = [](const char* n, int d) {
+        const char* e = std::getenv(n);
+        return e && e[0] ? (e[0] == '1' ? 1 : e[0] == '0' ? 0 : d) : d;
+    };
+    auto chr = [](const char* n, char d) {
+        const char* e = std::getenv(n);
+        return e && e[0] ? e[0] : d;
+    };
+    v.l2_window = flag("ARGCSR_L2_WINDOW", 1) != 0;
+    v.l2_persist = flag("ARGCSR_L2_PERSIST", 1) != 0;
+    v.x_evict_last = flag("ARGCSR_XPOL", 1);
+    v.stream_evict_first = flag("ARGCSR_SPOL", 0);
+    v.map = flag("ARGCSR_MAP", -1);
+    v.pair = flag("ARGCSR_PAIR", 1);
+    v.light_dyn = flag("ARGCSR_LIGHT_DYN", -1);
+    if (const char* e = std::getenv("ARGCSR_HEAVY_SMEM")) v.heavy_smem = size_t(std::atol(e));
+    v.heavy_u = chr("ARGCSR_HEAVY_U", 0);
+    v.heavy_b = chr("ARGCSR_HEAVY_B", 0);
+    v.heavy_runs = flag("ARGCSR_HEAVY_RUNS", 0) == 1;
+    v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
+    v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
+    if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
+    v.ulen = flag("ARGCSR_ULEN", -1);
+    v.trace = flag("ARGCSR_TRACE", 0) == 1;
+    return v;
+}
+std::mutex g_knob_mu;
+std::atomic<bool> g_knobs_loaded{false};
+Knobs g_knobs;
+}  // namespace
+
 const Knobs& knobs() {
-    static const Knobs k = [] {
-        Knobs v;
-        auto flag = [](const char* n, int d) {
-            const char* e = std::getenv(n);
-            return e && e[0] ? (e[0] == '1' ? 1 : e[0] == '0' ? 0 : d) : d;
-        };
-        auto chr = [](const char* n, char d) {
-            const char* e = std::getenv(n);
-            return e && e[0] ? e[0] : d;
-        };
-        v.l2_window = flag("ARGCSR_L2_WINDOW", 1) != 0;
-        v.l2_persist = flag("ARGCSR_L2_PERSIST", 1) != 0;
-        v.x_evict_last = flag("ARGCSR_XPOL", 1);
-        v.stream_evict_first = flag("ARGCSR_SPOL", 0);
-        v.map = flag("ARGCSR_MAP", -1);
-        v.pair = flag("ARGCSR_PAIR", 1);
-        v.light_dyn = flag("ARGCSR_LIGHT_DYN", -1);
-        if (const char* e = std::getenv("ARGCSR_HEAVY_SMEM")) v.heavy_smem = size_t(std::atol(e));
-        v.heavy_u = chr("ARGCSR_HEAVY_U", 0);
-        v.heavy_b = chr("ARGCSR_HEAVY_B", 0);
-        v.heavy_runs = flag("ARGCSR_HEAVY_RUNS", 0) == 1;
-        v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
-        v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
-        if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
-        v.ulen = flag("ARGCSR_ULEN", -1);
-        v.trace = flag("ARGCSR_TRACE", 0) == 1;
-        return v;
-    }();
-    return k;
+    if (!g_knobs_loaded.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lock(g_knob_mu);
+        if (!g_knobs_loaded.load(std::memory_order_relaxed)) {
+            g_knobs = read_knobs();
+            g_knobs_loaded.store(true, std::memory_order_release);
+        }
+    }
+    return g_knobs;
+}
+
+void reload_knobs() {
+    std::lock_guard<std::mutex> lock(g_knob_mu);
+    g_knobs = read_knobs();
+    g_knobs_loaded.store(true, std::memory_order_release);
 }
 }  // namespace argcsr_gpu
 
@@ -342,6 +362,8 @@ struct Writer {
 extern "C" {
 
 const char* argcsr_last_error(void) { return g_last_error.c_str(); }
+
+void argcsr_reload_options(void) { argcsr_gpu::reload_knobs(); }
 
 int argcsr_abi_version(void) { return ARGCSR_GPU_ABI_VERSION; }
 

@@ -103,6 +103,7 @@ struct Knobs {
     bool trace = false;           // ARGCSR_TRACE=1: per-phase host timings of the converter on stderr
 };
 const Knobs& knobs();
+void reload_knobs();  // argcsr_reload_options (tests flip switches between cases)
 
 // NVTX range (visible in Nsight Systems / ncu --nvtx; free when no tool is
 // attached) plus, with ARGCSR_TRACE=1 and sync_timer, a synchronising

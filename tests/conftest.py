@@ -67,3 +67,17 @@ def argcsr():
     import paper_1203_5737_b200
 
     return paper_1203_5737_b200
+
+
+@pytest.fixture(autouse=True)
+def _fresh_options():
+    """Tests that flip ARGCSR_* switches (monkeypatch.setenv + reload_options)
+    must not leak them: every test starts from the environment as restored by
+    the previous test's monkeypatch teardown."""
+    try:
+        import paper_1203_5737_b200 as m
+
+        m._ext.reload_options()
+    except Exception:
+        pass
+    yield

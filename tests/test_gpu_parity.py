@@ -187,6 +187,7 @@ def test_powerlaw_heavy_groups(argcsr, orc, tpg, dcs, heavy, monkeypatch):
     through two heavy-kernel variants."""
     if heavy != "default":
         monkeypatch.setenv(*heavy.split("="))
+        argcsr._ext.reload_options()
     A = powerlaw_csr(40000, 30000, seed=tpg * 7 + dcs, heavy_rows=[(0, 25000), (777, 12000), (39999, 9000)])
     dev = _check_case(argcsr, orc, A, tpg, dcs, f"powerlaw ({tpg},{dcs})")
     assert dev.heavy_groups > 0
@@ -249,6 +250,7 @@ def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout, heavy, monkeypatc
 
     if heavy != "default":
         monkeypatch.setenv(*heavy.split("="))
+        argcsr._ext.reload_options()
 
     A = powerlaw_csr(20000, 20000, seed=11, heavy_rows=[(100, 8000)])
     ref_m = orc.argcsr_from_csr(A, 128, 1)
@@ -355,6 +357,7 @@ def test_dense_rows_vector_x_runs(argcsr, orc, dtype, layout, heavy, monkeypatch
     results stay bit-identical (fp32: one rounding of the fp64 sum)."""
     if heavy != "default":
         monkeypatch.setenv(*heavy.split("="))
+        argcsr._ext.reload_options()
     rng = np.random.default_rng(3)
     n = 6000
     rows, cols = [], []
@@ -410,6 +413,7 @@ def test_unit_lengths_forced(argcsr, orc, corpus, monkeypatch, ulen):
     """Light units stop at their stored length (the u8 unit-length table) or
     read to the group's chunk: both bit-identical to the reference order."""
     monkeypatch.setenv("ARGCSR_ULEN", ulen)
+    argcsr._ext.reload_options()
     cases = [(A, t, d, f"corpus[{i}]") for i, A in enumerate(corpus[:60]) for t, d in ((4, 1), (12, 2), (128, 1), (32, 4))]
     cases += [(powerlaw_csr(40000, 30000, seed=11, heavy_rows=[(5, 20000)]), t, d, "powerlaw")
               for t, d in ((128, 1), (128, 4), (64, 2))]

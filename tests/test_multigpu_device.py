@@ -34,6 +34,7 @@ def test_fused_scale_heavy_groups(argcsr, orc, heavy, monkeypatch):
 
     if heavy != "default":
         monkeypatch.setenv(*heavy.split("="))
+        argcsr._ext.reload_options()
     A = powerlaw_csr(20000, 20000, seed=5, heavy_rows=[(3, 12000), (9000, 7000)])
     m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1)
     assert m.heavy_groups > 0

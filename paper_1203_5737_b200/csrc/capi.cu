@@ -18,10 +18,17 @@
 #include "inverse.cuh"
 #include "spmv.cuh"
 
+using argcsr_gpu::DeviceScope;
 using argcsr_gpu::fail;
 using argcsr_gpu::Failure;
+using argcsr_gpu::guarded;
 
 namespace argcsr_gpu {
+std::string& last_error() {
+    thread_local std::string msg;
+    return msg;
+}
+
 namespace {
 Knobs read_knobs() {
     Knobs v;
@@ -75,46 +82,6 @@ void reload_knobs() {
 }  // namespace argcsr_gpu
 
 namespace {
-
-thread_local std::string g_last_error;
-
-template <typename F>
-argcsr_status guarded(F&& f) {
-    try {
-        f();
-        g_last_error.clear();
-        return ARGCSR_OK;
-    } catch (const Failure& e) {
-        g_last_error = e.what();
-        return e.status;
-    } catch (const std::bad_alloc&) {
-        g_last_error = "out of host memory";
-        return ARGCSR_E_OOM;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return ARGCSR_E_INTERNAL;
-    }
-}
-
-// Binds the handle's device for the duration of a call and restores the
-// caller's current device afterwards.
-struct DeviceScope {
-    int prev = -1;
-    explicit DeviceScope(int dev) {
-        int n = 0;
-        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
-            cudaGetLastError();
-            fail(ARGCSR_E_CUDA, "no CUDA device available (the ARG-CSR path has no CPU fallback)");
-        }
-        if (dev < 0 || dev >= n) fail(ARGCSR_E_PARAMETER, "device ordinal " + std::to_string(dev) + " out of range");
-        CUDA_OK(cudaGetDevice(&prev));
-        if (prev != dev) CUDA_OK(cudaSetDevice(dev));
-    }
-    ~DeviceScope() {
-        int cur = -1;
-        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-    }
-};
 
 void release_l2_persist(int device);
 
@@ -361,7 +328,7 @@ struct Writer {
 
 extern "C" {
 
-const char* argcsr_last_error(void) { return g_last_error.c_str(); }
+const char* argcsr_last_error(void) { return argcsr_gpu::last_error().c_str(); }
 
 void argcsr_reload_options(void) { argcsr_gpu::reload_knobs(); }
 
@@ -511,7 +478,9 @@ argcsr_status argcsr_dev_spmv_scaled(const argcsr_dev* m, const void* x, const d
         if ((!x && m->num_cols) || !y) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_scaled: null vector");
         DeviceScope scope(m->device);
         SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
-        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s, x_scale);
+        argcsr_gpu::SpmvExtra ex;
+        ex.x_scale = x_scale;
+        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s, ex);
         serial.done();
     });
 }
@@ -536,8 +505,10 @@ argcsr_status argcsr_dev_spmv_ex(const argcsr_dev* m, const void* x, const doubl
         if (flags & ~uint32_t(ARGCSR_SPMV_REUSE_X)) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_ex: unknown flags");
         DeviceScope scope(m->device);
         SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
-        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s, x_scale,
-                                (flags & ARGCSR_SPMV_REUSE_X) != 0);
+        argcsr_gpu::SpmvExtra ex;
+        ex.x_scale = x_scale;
+        ex.reuse_x = (flags & ARGCSR_SPMV_REUSE_X) != 0;
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s, ex);
         serial.done();
     });
 }
@@ -555,8 +526,13 @@ argcsr_status argcsr_dev_spmv_peer(const argcsr_dev* m, const void* x, const dou
             if (!peer_y[q]) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_peer: null peer buffer");
         DeviceScope scope(m->device);
         SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
-        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s, x_scale,
-                                (flags & ARGCSR_SPMV_REUSE_X) != 0, peer_y, npeers, peer_rows);
+        argcsr_gpu::SpmvExtra ex;
+        ex.x_scale = x_scale;
+        ex.reuse_x = (flags & ARGCSR_SPMV_REUSE_X) != 0;
+        ex.peer_y = peer_y;
+        ex.npeers = npeers;
+        ex.peer_rows = peer_rows;
+        argcsr_gpu::spmv_launch(m, x, y, group_begin, group_end, serial.s, ex);
         serial.done();
     });
 }
@@ -1125,7 +1101,7 @@ argcsr_status argcsr_dev_read_binary(const char* path, uint64_t tpg, uint64_t dc
             v.total_slots = vals.size();
             v.dtype = ARGCSR_F64;
             const argcsr_status st = argcsr_dev_import(&v, device, stream, flags, out);
-            if (st != ARGCSR_OK) fail(st, g_last_error);
+            if (st != ARGCSR_OK) fail(st, argcsr_gpu::last_error());
         } else if (tag == kTagCsr) {  // io.cpp:313-320: converted on the device
             argcsr_csr_view v{};
             v.num_rows = r.u64();
@@ -1143,7 +1119,7 @@ argcsr_status argcsr_dev_read_binary(const char* path, uint64_t tpg, uint64_t dc
             v.dtype = ARGCSR_F64;
             v.space = ARGCSR_HOST;
             const argcsr_status st = argcsr_dev_convert_ex(&v, tpg, dcs, device, stream, flags, out);
-            if (st != ARGCSR_OK) fail(st, g_last_error);
+            if (st != ARGCSR_OK) fail(st, argcsr_gpu::last_error());
         } else if (tag == 1 || tag == 2) {
             fail(ARGCSR_E_UNSUPPORTED, "binary: ELLPACK / sliced ELLPACK containers have no device path");
         } else {

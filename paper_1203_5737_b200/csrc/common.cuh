@@ -38,6 +38,51 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CUDA_OK(expr) ::argcsr_gpu::cuda_check((expr), #expr)
 #define LAUNCH_OK(what) ::argcsr_gpu::cuda_check(cudaGetLastError(), what)
 
+// The C-ABI's thread-local error message (argcsr_last_error).
+std::string& last_error();
+
+// Runs f and maps any exception to a status + message: nothing throws across
+// the C-ABI.
+template <typename F>
+argcsr_status guarded(F&& f) {
+    try {
+        f();
+        last_error().clear();
+        return ARGCSR_OK;
+    } catch (const Failure& e) {
+        last_error() = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        last_error() = "out of host memory";
+        return ARGCSR_E_OOM;
+    } catch (const std::exception& e) {
+        last_error() = e.what();
+        return ARGCSR_E_INTERNAL;
+    }
+}
+
+// Binds a device for the duration of a call and restores the caller's current
+// device afterwards.
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(ARGCSR_E_CUDA, "no CUDA device available (the ARG-CSR path has no CPU fallback)");
+        }
+        if (dev < 0 || dev >= n) fail(ARGCSR_E_PARAMETER, "device ordinal " + std::to_string(dev) + " out of range");
+        CUDA_OK(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_OK(cudaSetDevice(dev));
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 // ------------------------------------------------------------ device layout
 // Group descriptor, 16 B, one LDG.128.  `off_stride` packs the group's slot
 // offset in the STORED value/column arrays (bits 0-47), its lane stride (bits

@@ -57,6 +57,8 @@ struct SpmvArgs {
     uint32_t tile0;  // light tiles [tile0, tile0 + gridDim.x) of this launch (spmv_launch_tiles)
     uint32_t max_tile_units;
     const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
+    int x_scale_is_norm2;    // *x_scale holds ||y_prev||^2: s = fl(1 / fl(sqrt(*x_scale))) (power iteration)
+    double* norm_part;       // fused ||y||^2: one partial per CTA (heavy CTAs first, then light tiles), or null
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
     uint32_t npeers;         // multi-GPU epilogue: y rows in [peer_lo[q], peer_hi[q]) are also stored
@@ -304,6 +306,31 @@ __device__ __forceinline__ void phase1_pair(const SpmvArgs<T>& a, const uint64_t
         }
 }
 
+template <typename T>
+__device__ __forceinline__ double x_scale_value(const SpmvArgs<T>& a) {
+    if (!a.x_scale) return 1.0;
+    const double v = *a.x_scale;
+    return a.x_scale_is_norm2 ? __drcp_rn(__dsqrt_rn(v)) : v;
+}
+
+// Fused ||y||^2: every thread accumulates the squares of the y values it
+// stores; the CTA's sum goes to norm_part[slot] in a fixed order (a fixed
+// xor-shuffle tree per warp, lane 0's result, then the warps in index order),
+// so the partials -- and the fixed-order reduction over them -- are
+// deterministic run to run.  Call from every thread of the CTA.
+__device__ __forceinline__ void write_norm_partial(double* out, double v) {
+    __shared__ double s_warp[kTileThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) t = __dadd_rn(t, s_warp[w]);
+        *out = t;
+    }
+}
+
 template <typename T> __device__ __forceinline__ T to_out(double v);
 template <> __device__ __forceinline__ double to_out<double>(double v) { return v; }
 template <> __device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
@@ -313,12 +340,13 @@ template <> __device__ __forceinline__ float to_out<float>(double v) { return __
 // x directly from the kernel, as plain stores over the NVLink peer mapping).
 // (A template flag: the single-GPU kernels carry no peer code at all.)
 template <bool PEER, typename T>
-__device__ __forceinline__ void store_y(const SpmvArgs<T>& a, uint32_t row, double v) {
+__device__ __forceinline__ double store_y(const SpmvArgs<T>& a, uint32_t row, double v) {
     const T o = to_out<T>(v);
     a.y[row] = o;
     if constexpr (PEER)
         for (uint32_t q = 0; q < a.npeers; ++q)
             if (row >= a.peer_lo[q] && row < a.peer_hi[q]) a.peer_y[q][row] = o;
+    return __dmul_rn(double(o), double(o));
 }
 
 // Phase 2 (argcsr.cpp:206-215): +0.0 + p_b + p_{b+1} + ... ascending.
@@ -347,7 +375,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
     __shared__ uint32_t s_lane0[kTileThreads + 1], s_row0[kTileThreads + 1], s_g[kTileThreads];
     const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const double xs = a.x_scale ? *a.x_scale : 1.0;
+    const double xs = x_scale_value(a);
     const uint32_t hb = a.heavy_ptr[blockIdx.x], he = a.heavy_ptr[blockIdx.x + 1];
     const uint32_t ng = he - hb;
     if (threadIdx.x == 0) {
@@ -376,6 +404,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
         s_part[l] = s[0];
     }
     __syncthreads();
+    double sq = 0.0;
     for (uint32_t r = threadIdx.x; r < nrows; r += blockDim.x) {
         const uint32_t i = find_le(s_row0, ng, r);
         const uint32_t g = s_g[i];
@@ -383,8 +412,9 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
         const uint32_t f = a.groups[g].first_row;
         const uint32_t row = f + (r - s_row0[i]);
         const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
-        store_y<PEER>(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row])));
+        sq = __dadd_rn(sq, store_y<PEER>(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row]))));
     }
+    if (a.norm_part) write_norm_partial(a.norm_part + blockIdx.x, sq);
 }
 
 // Light tile kt: consecutive short-chunk groups, V-lane units, one unit per thread.
@@ -400,11 +430,14 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     double* s_part = reinterpret_cast<double*>(smem);
     const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const double xs = a.x_scale ? *a.x_scale : 1.0;
+    const double xs = x_scale_value(a);
 
     const uint32_t kt = a.tile0 + blockIdx.x;
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
-    if (ge <= a.g_begin || gs >= a.g_end || gs == ge) return;
+    if (ge <= a.g_begin || gs >= a.g_end || gs == ge) {
+        if (a.norm_part && threadIdx.x == 0) a.norm_part[a.heavy_ctas + kt] = 0.0;
+        return;
+    }
     const uint32_t ng = ge - gs;
     const uint32_t cap = a.max_tile_groups;
     // smem: s_part[max_tile_units * V] | s_off[cap] | s_ub[cap+1] | s_first[cap+1] | s_chunk[cap]
@@ -522,14 +555,16 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     }
     __syncthreads();
 
-    if (pvalid) store_y<PEER>(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
+    double sq = 0.0;
+    if (pvalid) sq = store_y<PEER>(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
     for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
         const uint32_t gi = MAP ? s_rgrp[r - row0] : find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
-        store_y<PEER>(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r])));
+        sq = __dadd_rn(sq, store_y<PEER>(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r]))));
     }
+    if (a.norm_part) write_norm_partial(a.norm_part + a.heavy_ctas + kt, sq);
 }
 
 size_t light_smem_bytes(const argcsr_dev* m, int V, bool map = false) {
@@ -612,17 +647,22 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
 }
 
 template <typename T>
-void launch_dtype(const argcsr_dev* m, const void* x, const double* x_scale, void* y, uint32_t gb, uint32_t ge,
-                  cudaStream_t s, void* const* peer_y, uint32_t npeers, const uint64_t* peer_rows) {
+void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint32_t ge, cudaStream_t s,
+                  const SpmvExtra& ex) {
     SpmvArgs<T> a{};
+    const uint32_t npeers = ex.npeers;
+    void* const* peer_y = ex.peer_y;
+    const uint64_t* peer_rows = ex.peer_rows;
     a.npeers = npeers;
+    a.norm_part = ex.norm_part;
+    a.x_scale_is_norm2 = ex.scale_is_norm2 ? 1 : 0;
     for (uint32_t q = 0; q < npeers; ++q) {
         a.peer_y[q] = static_cast<T*>(peer_y[q]);
         a.peer_lo[q] = peer_rows ? uint32_t(std::min<uint64_t>(peer_rows[2 * q], m->num_rows)) : 0u;
         a.peer_hi[q] = peer_rows ? uint32_t(std::min<uint64_t>(peer_rows[2 * q + 1], m->num_rows))
                                  : uint32_t(m->num_rows);
     }
-    a.x_scale = x_scale;
+    a.x_scale = ex.x_scale;
     a.vals = static_cast<const T*>(m->values);
     a.cols = m->columns;
     a.groups = m->groups;
@@ -743,15 +783,34 @@ void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0,
 }
 
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale, bool reuse_x, void* const* peer_y, uint32_t npeers,
-                 const uint64_t* peer_rows) {
+                 cudaStream_t s, const SpmvExtra& ex) {
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
     Phase range("argcsr_spmv", s);  // NVTX only
-    x = reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
-    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, x_scale, y, gb, ge, s, peer_y, npeers, peer_rows);
-    else launch_dtype<float>(m, x, x_scale, y, gb, ge, s, peer_y, npeers, peer_rows);
+    x = ex.reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
+    if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, y, gb, ge, s, ex);
+    else launch_dtype<float>(m, x, y, gb, ge, s, ex);
+}
+
+// Fixed-order sum of the per-CTA norm partials: thread t sums entries t,
+// t + 1024, ... in order, then a fixed pairwise tree over the 1024 sums.
+__global__ void __launch_bounds__(1024) k_norm_reduce(const double* __restrict__ p, uint64_t n, double* out) {
+    __shared__ double s[1024];
+    double v = 0.0;
+    for (uint64_t i = threadIdx.x; i < n; i += 1024) v = __dadd_rn(v, p[i]);
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (uint32_t w = 512; w > 0; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] = __dadd_rn(s[threadIdx.x], s[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = s[0];
+}
+
+void norm_reduce(const double* partials, uint64_t n, double* out, cudaStream_t s) {
+    k_norm_reduce<<<1, 1024, 0, s>>>(partials, n, out);
+    LAUNCH_OK("k_norm_reduce");
 }
 
 // ------------------------------------------------ multi-GPU step signalling

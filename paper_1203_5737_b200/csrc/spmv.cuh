@@ -16,9 +16,27 @@ namespace argcsr_gpu {
 // [peer_rows[2q], peer_rows[2q+1]) (all rows when peer_rows is null) is also
 // stored to peer_y[q][row] (multi-GPU: the other GPUs' x buffers, pre-offset
 // by this slice's first row; the ranges are the rows each peer reads).
+// norm_part: fused ||y||^2, one partial per CTA of this launch written to
+// norm_part[0 .. norm_slots(m)) (heavy CTAs, then light tiles; CTAs with no
+// row of the group range write 0); reduce them with norm_reduce.
+// scale_is_norm2: *x_scale holds ||y_prev||^2 and the scale is 1/sqrt of it.
+struct SpmvExtra {
+    const double* x_scale = nullptr;
+    bool scale_is_norm2 = false;
+    bool reuse_x = false;
+    void* const* peer_y = nullptr;
+    uint32_t npeers = 0;
+    const uint64_t* peer_rows = nullptr;
+    double* norm_part = nullptr;
+};
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const double* x_scale = nullptr, bool reuse_x = false,
-                 void* const* peer_y = nullptr, uint32_t npeers = 0, const uint64_t* peer_rows = nullptr);
+                 cudaStream_t s, const SpmvExtra& ex = SpmvExtra{});
+
+inline uint64_t norm_slots(const argcsr_dev* m) { return uint64_t(m->heavy_ctas) + m->num_tiles; }
+
+// out[0] = sum of partials[0 .. n) in index order (one CTA, fixed tree):
+// deterministic.  `accumulate_into_out` adds *out first (several regions).
+void norm_reduce(const double* partials, uint64_t n, double* out, cudaStream_t s);
 
 // Step signalling between the GPUs of a multi-GPU step (spmv.cu): store
 // `value` into flags[q] (system-scope release, after *partial is copied to

@@ -51,10 +51,11 @@ PARITY_FAIL_RC = 3
 def parse_args(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=None, help="timed steps (default 200; 100 with --power-iteration)")
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C4f32", "C5"])
+    p.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C4", "C4f32", "C5"],
+                   help="workload (default C2; C5 with --power-iteration)")
     p.add_argument("--tpg", type=int, default=128)
     p.add_argument("--dcs", type=int, default=1)
     p.add_argument("--layout", default="compact", choices=["compact", "reference"],
@@ -71,7 +72,12 @@ def parse_args(argv=None):
     p.add_argument("--power-iteration", action="store_true",
                    help="a step is one power-iteration step (SpMV + fused ||y||^2, all-reduce, exchange, "
                         "scaling fused into the next SpMV)")
-    return p.parse_args(argv)
+    a = p.parse_args(argv)
+    if a.config is None:
+        a.config = "C5" if a.power_iteration else "C2"
+    if a.steps is None:
+        a.steps = 100 if a.power_iteration else 200
+    return a
 
 
 # ------------------------------------------------------------------ helpers

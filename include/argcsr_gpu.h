@@ -361,6 +361,146 @@ ARGCSR_API argcsr_status argcsr_dev_read_binary(const char* path, uint64_t threa
 ARGCSR_API argcsr_status argcsr_partition_rows(const uint64_t* row_pointers, uint64_t num_rows,
                                     uint32_t parts, uint64_t* row_begin);
 
+/* ---------------------------------------------- single-GPU power iteration
+ * y = A (s * x) and ||y||^2 in one pass: the SpMV epilogue accumulates the
+ * squares of the stored y values into per-CTA partials that a one-CTA kernel
+ * sums in a fixed order into *y_norm2 (device double) -- deterministic run to
+ * run.  x_scale as argcsr_dev_spmv_scaled; with ARGCSR_SCALE_IS_NORM2 in
+ * flags, *x_scale holds the previous step's ||y||^2 and the scale is
+ * fl(1 / fl(sqrt(*x_scale))): the normalisation x_{k+1} = y_k / ||y_k|| of the
+ * power iteration fused into the next product's gathers. */
+#define ARGCSR_SCALE_IS_NORM2 2u
+ARGCSR_API argcsr_status argcsr_dev_spmv_norm2(const argcsr_dev* m, const void* x, const double* x_scale,
+                                               void* y, double* y_norm2, uint32_t flags, void* stream);
+
+/* ------------------------------------------------ multi-GPU
+ * Replaces the reference's only parallel path, parallel_over /
+ * spmv_argcsr_parallel (proj/src/bench.cpp:48-71, 109-116; bench.hpp:59-60):
+ * rows are split into contiguous nnz-balanced slices (argcsr_partition_rows),
+ * each GPU converts ITS slice (bit-exact with argcsr_from_csr(slice)), x is
+ * replicated, and one step is the slice SpMV plus the exchange of the y slices
+ * into every GPU's next x:
+ *   ARGCSR_EXCHANGE_ALLGATHER  ncclAllGather in place (equal slices), else one
+ *                              ncclBroadcast per owner (grouped);
+ *   ARGCSR_EXCHANGE_HALO       only the x rows other slices read (grouped
+ *                              ncclSend/ncclRecv of a plan built at setup);
+ *   ARGCSR_EXCHANGE_P2P        no collective: the SpMV epilogue stores y into
+ *                              the peers' next x over NVLink (CUDA IPC or
+ *                              peer access), step flags + partial norms in
+ *                              peer memory;
+ *   ARGCSR_EXCHANGE_AUTO       halo when it moves < 1/4 of the all-gather's
+ *                              volume, else all-gather.
+ * NCCL is loaded at run time (dlopen libnccl.so.2); collective failures and
+ * asynchronous communicator errors (ncclCommGetAsyncError, polled every step)
+ * return ARGCSR_E_NCCL.  The power iteration fuses ||y||^2 into the SpMV
+ * epilogue, all-reduces 8 bytes, and fuses the scaling into the next SpMV.
+ * With the NCCL exchanges a step overlaps the exchange of step k with the
+ * interior groups (rows reading only the slice's own x rows) of step k+1. */
+typedef struct argcsr_mgpu argcsr_mgpu;
+typedef enum {
+    ARGCSR_EXCHANGE_AUTO = 0,
+    ARGCSR_EXCHANGE_ALLGATHER = 1,
+    ARGCSR_EXCHANGE_HALO = 2,
+    ARGCSR_EXCHANGE_P2P = 3,
+    ARGCSR_EXCHANGE_NONE = 4 /* reported for one rank */
+} argcsr_exchange;
+#define ARGCSR_NCCL_ID_BYTES 128
+
+typedef struct {
+    int32_t rank;              /* global rank of local rank 0 */
+    int32_t nranks;
+    int32_t nlocal;            /* GPUs driven by this handle (1 per process in the multi-process form) */
+    int32_t exchange;          /* argcsr_exchange actually used */
+    uint64_t num_rows, num_cols, nnz;
+    uint64_t row_begin, row_end;   /* local rank 0's slice */
+    uint64_t interior_begin, interior_end;  /* its interior group range */
+    uint64_t halo_recv_rows;   /* x rows it receives per step (halo exchange) */
+    uint64_t step;             /* steps issued since create */
+} argcsr_mgpu_info_t;
+
+/* ncclGetUniqueId: rank 0 calls it and shares the bytes with the other ranks
+ * (any channel: torch.distributed, MPI, a file). */
+ARGCSR_API argcsr_status argcsr_mgpu_unique_id(unsigned char id[ARGCSR_NCCL_ID_BYTES]);
+
+/* One process per GPU: rank `rank` of `nranks` on `device`.  `A` is the FULL
+ * matrix (host or device; every rank passes the same one).  `nccl_id` may be
+ * NULL only for nranks == 1 or for ARGCSR_EXCHANGE_P2P with an external
+ * connection (argcsr_mgpu_p2p_export / argcsr_mgpu_p2p_connect).  Collective
+ * over the ranks (NCCL communicator setup, halo plan, IPC handle exchange).
+ * flags: argcsr_dev_convert_ex layout flags. */
+ARGCSR_API argcsr_status argcsr_mgpu_create_rank(const argcsr_csr_view* A, int rank, int nranks,
+                                                 const unsigned char* nccl_id, uint64_t threads_per_group,
+                                                 uint64_t desired_chunk_size, int device, uint32_t flags,
+                                                 argcsr_exchange exchange, argcsr_mgpu** out);
+
+/* One process drives `ngpus` devices (SURVEY §8(b) signature): NCCL
+ * communicators from ncclCommInitAll; collectives grouped.  A device may be
+ * listed more than once only with ARGCSR_EXCHANGE_P2P (virtual ranks sharing
+ * a GPU: tests). */
+ARGCSR_API argcsr_status argcsr_mgpu_create(const argcsr_csr_view* A, int ngpus, const int* devices,
+                                            uint64_t threads_per_group, uint64_t desired_chunk_size,
+                                            argcsr_exchange exchange, argcsr_mgpu** out);
+
+ARGCSR_API argcsr_status argcsr_mgpu_info(const argcsr_mgpu* h, argcsr_mgpu_info_t* info);
+/* The slice handle of local rank i (borrowed: freed with h). */
+ARGCSR_API argcsr_status argcsr_mgpu_local(const argcsr_mgpu* h, int i, argcsr_dev** slice);
+
+/* P2P exchange without NCCL (multi-process, caller-provided channel):
+ * export this rank's 64-byte IPC handle and the [lo, hi) global rows it reads
+ * from every owner (need[2*p], need[2*p+1]); then connect with every rank's
+ * handle (handles[64*p]) and every rank's need table (need_all[(q*nranks+p)*2]
+ * = rows q reads from p).  Collective: every rank exports, exchanges, connects. */
+ARGCSR_API argcsr_status argcsr_mgpu_p2p_export(const argcsr_mgpu* h, unsigned char handle[64], uint64_t* need);
+ARGCSR_API argcsr_status argcsr_mgpu_p2p_connect(argcsr_mgpu* h, const unsigned char* handles,
+                                                 const uint64_t* need_all);
+
+/* Iterated SpMV / power iteration over the handle's double-buffered x (all
+ * arrays below have one entry per local rank; streams may be NULL = the
+ * legacy default stream).  begin: x_k <- x0 (full length, device), normalize
+ * selects the power iteration; step: one step (last != 0: every row is
+ * exchanged, so all GPUs end with all of x -- the halo modes otherwise move
+ * only the rows others read); finish: wait, then lambda = ||A x_{k-1}||
+ * (normalize) and x_out (full, device, may be NULL) = the current x
+ * (normalised).  Stream-ordered except finish, which synchronises. */
+ARGCSR_API argcsr_status argcsr_mgpu_begin(argcsr_mgpu* h, const void* const* x0, int normalize,
+                                           void* const* streams);
+ARGCSR_API argcsr_status argcsr_mgpu_step(argcsr_mgpu* h, int last, void* const* streams);
+ARGCSR_API argcsr_status argcsr_mgpu_finish(argcsr_mgpu* h, double* lambda, void* const* x_out,
+                                            void* const* streams);
+/* Stream-ordered: `streams` wait until the last step's exchange has landed
+ * (x_k complete on every local GPU) -- the end of a timed region. */
+ARGCSR_API argcsr_status argcsr_mgpu_wait(argcsr_mgpu* h, void* const* streams);
+
+/* out = A x assembled on every local rank (full-length device vectors): the
+ * slice SpMV into out[row_begin:row_end] and the exchange, stream-ordered. */
+ARGCSR_API argcsr_status argcsr_mgpu_spmv_gather(argcsr_mgpu* h, const void* const* x, void* const* out,
+                                                 void* const* streams);
+
+/* `iters` power-iteration steps from the host vector x_host_io
+ * (num_cols entries of the matrix dtype), written back normalised; lambda =
+ * ||A x_{iters-1}||.  Synchronous; every rank calls it. */
+ARGCSR_API argcsr_status argcsr_mgpu_power_iteration(argcsr_mgpu* h, int iters, void* x_host_io,
+                                                     double* lambda_out);
+
+/* Poll the communicators (ncclCommGetAsyncError): ARGCSR_E_NCCL on error. */
+ARGCSR_API argcsr_status argcsr_mgpu_check(argcsr_mgpu* h);
+ARGCSR_API void argcsr_mgpu_free(argcsr_mgpu* h);
+
+/* Host planning helpers of the multi-GPU layer (no device needed; the
+ * create calls use them on host copies of each slice).
+ * interior: the longest run [*ga, *gb) of groups (first rows group_first[0..G],
+ * group_first[G] = slice rows) whose rows (slice row pointers rp, rebased)
+ * reference only columns in [r0, r1).
+ * needed: the distinct global rows (ascending) of owner p != self that the
+ * slice's columns reference, for every owner: counts[p] (always) and, when
+ * rows is non-NULL, the rows of owner 0, 1, ... concatenated. */
+ARGCSR_API argcsr_status argcsr_plan_interior(const uint64_t* rp, const int32_t* columns, uint64_t rows,
+                                              const uint64_t* group_first, uint64_t num_groups, uint64_t r0,
+                                              uint64_t r1, uint64_t* ga, uint64_t* gb);
+ARGCSR_API argcsr_status argcsr_plan_needed(const int32_t* columns, uint64_t nnz, uint64_t num_cols,
+                                            const uint64_t* bounds, uint32_t parts, uint32_t self,
+                                            uint64_t* counts, uint64_t* rows);
+
 /* ------------------------------------------------------------------- errors */
 ARGCSR_API const char* argcsr_last_error(void);
 ARGCSR_API const char* argcsr_status_name(argcsr_status s);

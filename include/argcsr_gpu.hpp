@@ -120,12 +120,16 @@ static_assert(sizeof(std::size_t) == sizeof(uint64_t), "64-bit size_t required")
 class DeviceArgCsr {
 public:
     DeviceArgCsr() = default;
-    explicit DeviceArgCsr(argcsr_dev* h) : h_(h) { refresh(); }
-    DeviceArgCsr(DeviceArgCsr&& o) noexcept : h_(std::exchange(o.h_, nullptr)), info_(o.info_) {}
+    explicit DeviceArgCsr(argcsr_dev* h, bool owned = true) : h_(h), owned_(owned) { refresh(); }
+    // A view of a handle owned elsewhere (a multi-GPU slice: argcsr_mgpu_local).
+    static DeviceArgCsr borrow(argcsr_dev* h) { return DeviceArgCsr(h, false); }
+    DeviceArgCsr(DeviceArgCsr&& o) noexcept
+        : h_(std::exchange(o.h_, nullptr)), owned_(o.owned_), info_(o.info_) {}
     DeviceArgCsr& operator=(DeviceArgCsr&& o) noexcept {
         if (this != &o) {
             reset();
             h_ = std::exchange(o.h_, nullptr);
+            owned_ = o.owned_;
             info_ = o.info_;
         }
         return *this;
@@ -135,7 +139,7 @@ public:
     ~DeviceArgCsr() { reset(); }
 
     void reset() {
-        if (h_) argcsr_dev_free(h_);
+        if (h_ && owned_) argcsr_dev_free(h_);
         h_ = nullptr;
     }
     argcsr_dev* handle() const { return h_; }
@@ -170,6 +174,7 @@ private:
         if (h_) check(argcsr_dev_info(h_, &info_));
     }
     argcsr_dev* h_ = nullptr;
+    bool owned_ = true;
     argcsr_dev_info_t info_{};
 };
 

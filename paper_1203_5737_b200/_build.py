@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 
-CUDA_SOURCES = ["capi.cu", "convert.cu", "spmv.cu", "inverse.cu", "xremap.cu", "ellpack.cu"]
+CUDA_SOURCES = ["capi.cu", "convert.cu", "spmv.cu", "inverse.cu", "xremap.cu", "ellpack.cu", "mgpu.cu"]
 CUDA_HEADERS = ["common.cuh", "scan.cuh", "convert.cuh", "spmv.cuh", "inverse.cuh", "xremap.cuh", "ellpack.cuh"]
 LIB = PKG / "libargcsr_gpu.so"
 EXT = PKG / ("_argcsr_gpu" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
@@ -29,6 +29,19 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "-Xptxas", "-v",
 ]
+
+
+def _nccl_include() -> str:
+    """nccl.h for the multi-GPU layer (types only: libnccl is dlopen'ed at run time)."""
+    try:
+        import nvidia.nccl
+
+        p = Path(list(nvidia.nccl.__path__)[0]) / "include"
+        if (p / "nccl.h").exists():
+            return str(p)
+    except Exception:
+        pass
+    return "/usr/include"
 
 
 def _nvcc() -> str:
@@ -58,9 +71,9 @@ def build_lib(force: bool = False) -> Path:
     if force or _stale(LIB, deps):
         # Export only the C-ABI: -fvisibility=hidden hides internals, the
         # header marks nothing, so re-export the argcsr_* symbols explicitly.
-        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", f"-I{INCLUDE}", "-o", str(LIB),
+        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", f"-I{INCLUDE}", f"-I{_nccl_include()}", "-o", str(LIB),
                *[str(CSRC / s) for s in CUDA_SOURCES],
-               "-Xlinker", f"--version-script={CSRC / 'exports.map'}"]
+               "-Xlinker", f"--version-script={CSRC / 'exports.map'}", "-ldl"]
         _run(cmd, PKG / "build_ptxas.log")
     return LIB
 

@@ -204,6 +204,45 @@ PyArgCsr convert_arrays(std::size_t num_rows, std::size_t num_cols, py::array ro
 
 }  // namespace
 
+// The multi-GPU handle (argcsr_mgpu_*): one per process in the one-process-
+// per-GPU form.  Per-local-rank arguments are lists of device pointers /
+// stream handles as ints.
+struct PyMultiGpu {
+    argcsr_mgpu* h = nullptr;
+    int nlocal = 1;
+    ~PyMultiGpu() { free(); }
+    void free() {
+        if (h) argcsr_mgpu_free(h);
+        h = nullptr;
+    }
+    argcsr_mgpu* get() const {
+        if (!h) throw ParameterError("multi-GPU handle already freed");
+        return h;
+    }
+};
+
+std::vector<void*> ptr_list(const std::vector<std::uintptr_t>& v, std::size_t n, const char* what) {
+    if (v.size() != n) throw ParameterError(std::string(what) + ": one entry per local GPU");
+    std::vector<void*> out(n);
+    for (std::size_t i = 0; i < n; ++i) out[i] = reinterpret_cast<void*>(v[i]);
+    return out;
+}
+
+argcsr_csr_view view_from_ptrs(std::size_t num_rows, std::size_t num_cols, std::size_t nnz, std::uintptr_t rp,
+                               std::uintptr_t cols, std::uintptr_t vals, const std::string& dtype, bool device) {
+    argcsr_csr_view v{};
+    v.num_rows = num_rows;
+    v.num_cols = num_cols;
+    v.nnz = nnz;
+    v.row_pointers = reinterpret_cast<const uint64_t*>(rp);
+    v.columns = reinterpret_cast<const int32_t*>(cols);
+    v.values = reinterpret_cast<const void*>(vals);
+    if (dtype != "float64" && dtype != "float32") throw ParameterError("dtype must be 'float64' or 'float32'");
+    v.dtype = dtype == "float64" ? ARGCSR_F64 : ARGCSR_F32;
+    v.space = device ? ARGCSR_DEVICE : ARGCSR_HOST;
+    return v;
+}
+
 PYBIND11_MODULE(_argcsr_gpu, m) {
     m.doc() = "B200-native adaptive row-grouped CSR (ARG-CSR): GPU conversion and SpMV behind the argcsr API";
 
@@ -234,6 +273,212 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
     m.attr("kDefaultDesiredChunkSize") = kDefaultDesiredChunkSize;
     m.attr("kPaddingColumn") = kPaddingColumn;
     m.def("abi_version", &argcsr_abi_version);
+
+    // ------------------------------------------------ multi-GPU (argcsr_mgpu_*)
+    m.def("mgpu_unique_id", [] {
+        unsigned char id[ARGCSR_NCCL_ID_BYTES];
+        check(argcsr_mgpu_unique_id(id));
+        return py::bytes(reinterpret_cast<const char*>(id), ARGCSR_NCCL_ID_BYTES);
+    });
+    m.def(
+        "plan_interior",
+        [](py::array_t<uint64_t, py::array::c_style | py::array::forcecast> rp,
+           py::array_t<int32_t, py::array::c_style | py::array::forcecast> cols,
+           py::array_t<uint64_t, py::array::c_style | py::array::forcecast> group_first, uint64_t r0, uint64_t r1) {
+            if (rp.size() < 1 || group_first.size() < 1) throw ParameterError("plan_interior: empty arrays");
+            uint64_t ga = 0, gb = 0;
+            check(argcsr_plan_interior(rp.data(), cols.data(), uint64_t(rp.size() - 1), group_first.data(),
+                                       uint64_t(group_first.size() - 1), r0, r1, &ga, &gb));
+            return py::make_tuple(ga, gb);
+        },
+        py::arg("row_pointers"), py::arg("columns"), py::arg("group_first"), py::arg("r0"), py::arg("r1"));
+    m.def(
+        "plan_needed",
+        [](py::array_t<int32_t, py::array::c_style | py::array::forcecast> cols, uint64_t num_cols,
+           py::array_t<uint64_t, py::array::c_style | py::array::forcecast> bounds, uint32_t self) {
+            const uint32_t parts = uint32_t(bounds.size() - 1);
+            std::vector<uint64_t> counts(parts);
+            check(argcsr_plan_needed(cols.data(), uint64_t(cols.size()), num_cols, bounds.data(), parts, self,
+                                     counts.data(), nullptr));
+            uint64_t tot = 0;
+            for (uint64_t c : counts) tot += c;
+            py::array_t<uint64_t> rows(tot);
+            check(argcsr_plan_needed(cols.data(), uint64_t(cols.size()), num_cols, bounds.data(), parts, self,
+                                     counts.data(), rows.mutable_data()));
+            py::list out;
+            uint64_t o = 0;
+            for (uint32_t p = 0; p < parts; ++p) {
+                out.append(py::array_t<uint64_t>({counts[p]}, {sizeof(uint64_t)}, rows.data() + o));
+                o += counts[p];
+            }
+            return out;
+        },
+        py::arg("columns"), py::arg("num_cols"), py::arg("bounds"), py::arg("self_rank"));
+
+    py::class_<PyMultiGpu>(m, "MultiGpu")
+        .def_static(
+            "create_rank",
+            [](std::size_t num_rows, std::size_t num_cols, std::size_t nnz, std::uintptr_t rp, std::uintptr_t cols,
+               std::uintptr_t vals, const std::string& dtype, bool device_arrays, int rank, int nranks,
+               std::optional<py::bytes> nccl_id, std::size_t tpg, std::size_t dcs, int device, std::uint32_t flags,
+               int exchange) {
+                argcsr_csr_view v = view_from_ptrs(num_rows, num_cols, nnz, rp, cols, vals, dtype, device_arrays);
+                std::string id;
+                if (nccl_id) {
+                    id = *nccl_id;
+                    if (id.size() != ARGCSR_NCCL_ID_BYTES) throw ParameterError("nccl_id: 128 bytes");
+                }
+                auto p = std::make_unique<PyMultiGpu>();
+                {
+                    py::gil_scoped_release nogil;
+                    check(argcsr_mgpu_create_rank(&v, rank, nranks,
+                                                  nccl_id ? reinterpret_cast<const unsigned char*>(id.data()) : nullptr,
+                                                  tpg, dcs, device, flags, static_cast<argcsr_exchange>(exchange), &p->h));
+                }
+                p->nlocal = 1;
+                return p;
+            },
+            py::arg("num_rows"), py::arg("num_cols"), py::arg("nnz"), py::arg("row_pointers_ptr"),
+            py::arg("columns_ptr"), py::arg("values_ptr"), py::arg("dtype"), py::arg("device_arrays"),
+            py::arg("rank"), py::arg("nranks"), py::arg("nccl_id"), py::arg("threads_per_group") = 128,
+            py::arg("desired_chunk_size") = 1, py::arg("device") = 0, py::arg("flags") = 0, py::arg("exchange") = 0)
+        .def_static(
+            "create",
+            [](std::size_t num_rows, std::size_t num_cols, std::size_t nnz, std::uintptr_t rp, std::uintptr_t cols,
+               std::uintptr_t vals, const std::string& dtype, bool device_arrays, std::vector<int> devices,
+               std::size_t tpg, std::size_t dcs, int exchange) {
+                argcsr_csr_view v = view_from_ptrs(num_rows, num_cols, nnz, rp, cols, vals, dtype, device_arrays);
+                auto p = std::make_unique<PyMultiGpu>();
+                {
+                    py::gil_scoped_release nogil;
+                    check(argcsr_mgpu_create(&v, int(devices.size()), devices.data(), tpg, dcs,
+                                             static_cast<argcsr_exchange>(exchange), &p->h));
+                }
+                p->nlocal = int(devices.size());
+                return p;
+            },
+            py::arg("num_rows"), py::arg("num_cols"), py::arg("nnz"), py::arg("row_pointers_ptr"),
+            py::arg("columns_ptr"), py::arg("values_ptr"), py::arg("dtype"), py::arg("device_arrays"),
+            py::arg("devices"), py::arg("threads_per_group") = 128, py::arg("desired_chunk_size") = 1,
+            py::arg("exchange") = 0)
+        .def("info",
+             [](const PyMultiGpu& p) {
+                 argcsr_mgpu_info_t i{};
+                 check(argcsr_mgpu_info(p.get(), &i));
+                 py::dict d;
+                 d["rank"] = i.rank;
+                 d["nranks"] = i.nranks;
+                 d["nlocal"] = i.nlocal;
+                 d["exchange"] = i.exchange;
+                 d["num_rows"] = i.num_rows;
+                 d["num_cols"] = i.num_cols;
+                 d["nnz"] = i.nnz;
+                 d["row_begin"] = i.row_begin;
+                 d["row_end"] = i.row_end;
+                 d["interior_begin"] = i.interior_begin;
+                 d["interior_end"] = i.interior_end;
+                 d["halo_recv_rows"] = i.halo_recv_rows;
+                 d["step"] = i.step;
+                 return d;
+             })
+        .def(
+            "local",
+            [](const PyMultiGpu& p, int i) {
+                argcsr_dev* s = nullptr;
+                check(argcsr_mgpu_local(p.get(), i, &s));
+                PyArgCsr a;
+                a.dev = std::make_shared<DeviceArgCsr>(DeviceArgCsr::borrow(s));
+                return a;
+            },
+            py::arg("index") = 0, py::keep_alive<0, 1>())
+        .def("p2p_export",
+             [](const PyMultiGpu& p) {
+                 argcsr_mgpu_info_t i{};
+                 check(argcsr_mgpu_info(p.get(), &i));
+                 unsigned char hnd[64];
+                 std::vector<uint64_t> need(2 * size_t(i.nranks));
+                 check(argcsr_mgpu_p2p_export(p.get(), hnd, need.data()));
+                 return py::make_tuple(py::bytes(reinterpret_cast<const char*>(hnd), 64), need);
+             })
+        .def(
+            "p2p_connect",
+            [](PyMultiGpu& p, const std::vector<py::bytes>& handles, const std::vector<std::vector<uint64_t>>& need_all) {
+                std::string flat;
+                for (const auto& hb : handles) {
+                    const std::string s = hb;
+                    if (s.size() != 64) throw ParameterError("p2p_connect: IPC handles are 64 bytes");
+                    flat += s;
+                }
+                std::vector<uint64_t> na;
+                for (const auto& row : need_all) na.insert(na.end(), row.begin(), row.end());
+                check(argcsr_mgpu_p2p_connect(p.get(), reinterpret_cast<const unsigned char*>(flat.data()), na.data()));
+            },
+            py::arg("handles"), py::arg("need_all"))
+        .def(
+            "begin",
+            [](PyMultiGpu& p, const std::vector<std::uintptr_t>& x0, bool normalize,
+               const std::vector<std::uintptr_t>& streams) {
+                auto xs = ptr_list(x0, p.nlocal, "begin");
+                auto ss = ptr_list(streams, p.nlocal, "begin");
+                check(argcsr_mgpu_begin(p.get(), xs.data(), normalize ? 1 : 0, ss.data()));
+            },
+            py::arg("x0"), py::arg("normalize"), py::arg("streams"))
+        .def(
+            "step",
+            [](PyMultiGpu& p, bool last, const std::vector<std::uintptr_t>& streams) {
+                auto ss = ptr_list(streams, p.nlocal, "step");
+                check(argcsr_mgpu_step(p.get(), last ? 1 : 0, ss.data()));
+            },
+            py::arg("last"), py::arg("streams"))
+        .def(
+            "finish",
+            [](PyMultiGpu& p, const std::vector<std::uintptr_t>& x_out, const std::vector<std::uintptr_t>& streams) {
+                auto xs = ptr_list(x_out, p.nlocal, "finish");
+                auto ss = ptr_list(streams, p.nlocal, "finish");
+                double lam = 0.0;
+                {
+                    py::gil_scoped_release nogil;
+                    check(argcsr_mgpu_finish(p.get(), &lam, xs.data(), ss.data()));
+                }
+                return lam;
+            },
+            py::arg("x_out"), py::arg("streams"))
+        .def(
+            "spmv_gather",
+            [](PyMultiGpu& p, const std::vector<std::uintptr_t>& x, const std::vector<std::uintptr_t>& out,
+               const std::vector<std::uintptr_t>& streams) {
+                auto xs = ptr_list(x, p.nlocal, "spmv_gather");
+                auto os = ptr_list(out, p.nlocal, "spmv_gather");
+                auto ss = ptr_list(streams, p.nlocal, "spmv_gather");
+                std::vector<const void*> xc(xs.begin(), xs.end());
+                check(argcsr_mgpu_spmv_gather(p.get(), xc.data(), os.data(), ss.data()));
+            },
+            py::arg("x"), py::arg("out"), py::arg("streams"))
+        .def(
+            "power_iteration",
+            [](PyMultiGpu& p, int iters, py::array x) {
+                argcsr_mgpu_info_t i{};
+                check(argcsr_mgpu_info(p.get(), &i));
+                if (!(x.flags() & py::array::c_style) || !x.writeable() || uint64_t(x.size()) != i.num_cols)
+                    throw ParameterError("power_iteration: x must be a writeable contiguous array of num_cols entries");
+                double lam = 0.0;
+                void* xp = x.mutable_data();
+                {
+                    py::gil_scoped_release nogil;
+                    check(argcsr_mgpu_power_iteration(p.get(), iters, xp, &lam));
+                }
+                return lam;
+            },
+            py::arg("iters"), py::arg("x"))
+        .def(
+            "wait",
+            [](PyMultiGpu& p, const std::vector<std::uintptr_t>& streams) {
+                auto ss = ptr_list(streams, p.nlocal, "wait");
+                check(argcsr_mgpu_wait(p.get(), ss.data()));
+            },
+            py::arg("streams"))
+        .def("check", [](PyMultiGpu& p) { check(argcsr_mgpu_check(p.get())); })
+        .def("free", &PyMultiGpu::free);
     m.def("reload_options", &argcsr_reload_options,
           "Re-read the ARGCSR_* experiment switches from the environment (read once otherwise).");
     // multi-GPU step over peer memory (argcsr_gpu.h: argcsr_peer_*)
@@ -401,6 +646,16 @@ PYBIND11_MODULE(_argcsr_gpu, m) {
                                               reinterpret_cast<void*>(stream)));
              },
              py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("y_ptr"), py::arg("stream") = 0)
+        .def("spmv_norm2_device",
+             [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uintptr_t y, std::uintptr_t norm2,
+                bool scale_is_norm2, std::uintptr_t stream) {
+                 check(argcsr_dev_spmv_norm2(p.dev->handle(), reinterpret_cast<const void*>(x),
+                                             reinterpret_cast<const double*>(scale), reinterpret_cast<void*>(y),
+                                             reinterpret_cast<double*>(norm2), scale_is_norm2 ? ARGCSR_SCALE_IS_NORM2 : 0u,
+                                             reinterpret_cast<void*>(stream)));
+             },
+             py::arg("x_ptr"), py::arg("x_scale_ptr"), py::arg("y_ptr"), py::arg("norm2_ptr"),
+             py::arg("scale_is_norm2") = false, py::arg("stream") = 0)
         .def("spmv_peer_device",
              [](const PyArgCsr& p, std::uintptr_t x, std::uintptr_t scale, std::uint64_t gb, std::uint64_t ge,
                 std::uintptr_t y, const std::vector<std::uintptr_t>& peers, const std::vector<std::uint64_t>& rows,

@@ -123,6 +123,7 @@ void free_handle(argcsr_dev* m) {
     if (m->ev_fork) cudaEventDestroy(m->ev_fork);
     if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (m->ev_done) cudaEventDestroy(m->ev_done);
+    cudaFree(m->norm_scratch);
     if (m->holds_l2_persist) release_l2_persist(m->device);
     if (prev >= 0) cudaSetDevice(prev);
     delete m;
@@ -188,20 +189,7 @@ void release_l2_persist(int device) {
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, st.saved) != cudaSuccess) cudaGetLastError();
 }
 
-// Serialises the SpMVs of one handle (see argcsr_dev::mu): wait for the
-// previous SpMV on this handle, then record the end of this one.
-struct SpmvSerial {
-    argcsr_dev* m;
-    cudaStream_t s;
-    std::unique_lock<std::mutex> lock;
-    SpmvSerial(const argcsr_dev* mc, cudaStream_t st) : m(const_cast<argcsr_dev*>(mc)), s(st), lock(m->mu) {
-        if (m->spmv_issued) CUDA_OK(cudaStreamWaitEvent(s, m->ev_done, 0));
-    }
-    void done() {
-        CUDA_OK(cudaEventRecord(m->ev_done, s));
-        m->spmv_issued = true;
-    }
-};
+using SpmvSerial = argcsr_gpu::SpmvOrder;
 
 // A fresh handle with the per-handle resources (aux stream, events, L2 window
 // limits); freed by free_handle on any failure of the caller.
@@ -481,6 +469,29 @@ argcsr_status argcsr_dev_spmv_scaled(const argcsr_dev* m, const void* x, const d
         argcsr_gpu::SpmvExtra ex;
         ex.x_scale = x_scale;
         argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s, ex);
+        serial.done();
+    });
+}
+
+argcsr_status argcsr_dev_spmv_norm2(const argcsr_dev* m, const void* x, const double* x_scale, void* y,
+                                    double* y_norm2, uint32_t flags, void* stream) {
+    return guarded([&] {
+        check_handle(m);
+        if ((!x && m->num_cols) || !y || !y_norm2) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_norm2: null argument");
+        if (flags & ~uint32_t(ARGCSR_SCALE_IS_NORM2)) fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_norm2: unknown flags");
+        if ((flags & ARGCSR_SCALE_IS_NORM2) && !x_scale)
+            fail(ARGCSR_E_PARAMETER, "argcsr_dev_spmv_norm2: ARGCSR_SCALE_IS_NORM2 needs x_scale");
+        DeviceScope scope(m->device);
+        SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
+        argcsr_dev* mm = const_cast<argcsr_dev*>(m);
+        const uint64_t S = argcsr_gpu::norm_slots(m);
+        if (!mm->norm_scratch) CUDA_OK(cudaMalloc(&mm->norm_scratch, std::max<uint64_t>(S, 1) * sizeof(double)));
+        argcsr_gpu::SpmvExtra ex;
+        ex.x_scale = x_scale;
+        ex.scale_is_norm2 = (flags & ARGCSR_SCALE_IS_NORM2) != 0;
+        ex.norm_part = mm->norm_scratch;
+        argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s, ex);
+        argcsr_gpu::norm_reduce(mm->norm_scratch, S, y_norm2, serial.s);
         serial.done();
     });
 }

@@ -259,7 +259,8 @@ struct argcsr_dev {
     std::mutex mu;
     cudaEvent_t ev_done = nullptr;
     bool spmv_issued = false;
-    bool holds_l2_persist = false;        // counted in the device's persisting-L2 users (capi.cu)
+    bool holds_l2_persist = false;
+    double* norm_scratch = nullptr;       // per-CTA ||y||^2 partials (argcsr_dev_spmv_norm2), lazily allocated        // counted in the device's persisting-L2 users (capi.cu)
 
     uint64_t light_slots = 0;             // stored slots of light groups (stored first)
 

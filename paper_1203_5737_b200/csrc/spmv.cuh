@@ -32,6 +32,22 @@ struct SpmvExtra {
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
                  cudaStream_t s, const SpmvExtra& ex = SpmvExtra{});
 
+// Serialises the SpMVs of one handle (argcsr_dev::mu, ev_done): wait for the
+// previous SpMV on this handle, whatever stream it ran on; done() records the
+// end of this one.  Every SpMV entry point (C-ABI, multi-GPU layer) uses it.
+struct SpmvOrder {
+    argcsr_dev* m;
+    cudaStream_t s;
+    std::unique_lock<std::mutex> lock;
+    SpmvOrder(const argcsr_dev* mc, cudaStream_t st) : m(const_cast<argcsr_dev*>(mc)), s(st), lock(m->mu) {
+        if (m->spmv_issued) CUDA_OK(cudaStreamWaitEvent(s, m->ev_done, 0));
+    }
+    void done() {
+        CUDA_OK(cudaEventRecord(m->ev_done, s));
+        m->spmv_issued = true;
+    }
+};
+
 inline uint64_t norm_slots(const argcsr_dev* m) { return uint64_t(m->heavy_ctas) + m->num_tiles; }
 
 // out[0] = sum of partials[0 .. n) in index order (one CTA, fixed tree):

@@ -162,30 +162,28 @@ def test_cpp_example_runs_on_the_device(tmp_path):
     assert "lossless=1" in r.stdout
 
 
-def test_peer_needed_ranges_are_the_halo():
-    """The rows each peer reads from a rank (peer.py: one [lo, hi) interval
-    per owner): for a 27-pt stencil split 4 ways, each rank needs its own rows
-    plus about one plane of each neighbour, nothing from the others."""
+def test_peer_needed_rows_are_the_halo():
+    """The rows each rank reads from every other slice (argcsr_plan_needed,
+    the halo plan of the multi-GPU layer): for a 27-pt stencil split 4 ways,
+    about one plane of each neighbour, nothing from the others."""
     from helpers import stencil27
-    from paper_1203_5737_b200.multigpu import partition_bounds, slice_rows
-    from paper_1203_5737_b200.peer import needed_ranges
+    from paper_1203_5737_b200.multigpu import needed_rows, partition_bounds
 
     n = 16
     A = stencil27(n)
     b = partition_bounds(A.row_pointers, 4)
     for p in range(4):
-        sl = slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1]))
-        need = needed_ranges(sl.columns, b)
-        assert tuple(need[p]) == (int(b[p]), int(b[p + 1]))
+        a0, a1 = int(A.row_pointers[b[p]]), int(A.row_pointers[b[p + 1]])
+        cols = np.asarray(A.columns[a0:a1])
+        need = needed_rows(cols, A.num_cols, b, p)
+        assert len(need[p]) == 0
         for q in range(4):
-            lo, hi = need[q]
             if abs(q - p) > 1:
-                assert (lo, hi) == (0, 0)
+                assert len(need[q]) == 0
             elif q != p:
-                assert 0 < hi - lo <= n * n + n + 1  # one plane (+ one row and one point of the next)
-                cols = np.asarray(sl.columns)
-                inq = cols[(cols >= b[q]) & (cols < b[q + 1])]
-                assert lo == inq.min() and hi == inq.max() + 1
+                assert 0 < len(need[q]) <= n * n + n + 1  # one plane (+ one row and one point of the next)
+                inq = np.unique(cols[(cols >= b[q]) & (cols < b[q + 1])])
+                assert np.array_equal(need[q], inq.astype(np.uint64))
 
 
 def test_peer_abi_parameter_errors_without_device(argcsr):

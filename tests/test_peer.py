@@ -1,10 +1,12 @@
-"""The fused multi-GPU step over peer memory (paper_1203_5737_b200/peer.py).
+"""The fused multi-GPU step over peer memory (csrc/mgpu.cu, exchange p2p).
 
-Only one GPU is available, so the protocol runs (a) as P virtual ranks on one
-device -- each rank's SpMV epilogue stores its y slice into the other ranks'
+Only one GPU is available, so the protocol runs (a) as P virtual ranks of ONE
+process sharing the device (argcsr_mgpu_create with the device listed P
+times) -- each rank's SpMV epilogue stores its y slice into the other ranks'
 x buffers, flags and partial norms travel the same way -- and (b) as two
-processes sharing the GPU through real CUDA IPC handles (exchanged with the
-gloo backend), the code path an 8-GPU box runs over NVLink."""
+processes sharing the GPU through real CUDA IPC handles (exchanged over the
+gloo backend, argcsr_mgpu_p2p_export / _connect), the code path an 8-GPU box
+runs over NVLink."""
 import os
 import sys
 import traceback
@@ -21,22 +23,18 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def _engines(A, P, tpg=128, dcs=1):
-    from paper_1203_5737_b200.multigpu import DeviceEngine, partition_bounds, slice_rows
-
-    b = partition_bounds(A.row_pointers, P)
-    dev = torch.device("cuda", 0)
-    engs = [DeviceEngine(slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1])),
-                         tpg, dcs, dev) for p in range(P)]
-    return b, engs
+def _virtual(argcsr, A, P, tpg=128, dcs=1):
+    rp = torch.from_numpy(A.row_pointers.astype(np.int64))
+    cols = torch.from_numpy(A.columns)
+    vals = torch.from_numpy(A.values)
+    return argcsr._ext.MultiGpu.create(A.num_rows, A.num_cols, A.nnz, rp.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                       "float64", False, [0] * P, tpg, dcs, 3)
 
 
 @pytest.mark.parametrize("kind", ["stencil", "powerlaw"])
 def test_spmv_peer_stores_bit_identical(argcsr, orc, kind):
     """argcsr_dev_spmv_peer: y and every peer target hold the oracle's bits
     (light tiles and heavy groups), other rows of the targets untouched."""
-    import oracle
-
     A = stencil27(14) if kind == "stencil" else powerlaw_csr(30000, 30000, seed=9, heavy_rows=[(11, 15000)])
     m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1)
     x = torch.linspace(-2, 3, A.num_cols, dtype=torch.float64, device="cuda")
@@ -66,54 +64,73 @@ def test_spmv_peer_stores_bit_identical(argcsr, orc, kind):
     assert bits(t2) == bits(ref)
 
 
-@pytest.mark.parametrize("halo", [False, True])
-@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("P", [2, 3, 4])
 @pytest.mark.parametrize("kind", ["stencil", "powerlaw"])
-def test_peer_power_iteration_virtual_ranks(kind, P, halo):
-    """Full stores, or halo-only stores (each peer gets the rows its columns
-    read; the last step stores everything so every rank ends with all of x)."""
+def test_peer_power_iteration_virtual_ranks(argcsr, kind, P):
+    """Halo-only peer stores each step (the rows each peer's columns read),
+    every row on the last step so every rank ends with all of x."""
     import oracle
-    from paper_1203_5737_b200.multigpu import slice_rows
-    from paper_1203_5737_b200.peer import power_iteration_local
 
     A = stencil27(16) if kind == "stencil" else powerlaw_csr(6000, 6000, seed=4, heavy_rows=[(7, 4000)])
-    b, engs = _engines(A, P)
-    cols = [slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1])).columns
-            for p in range(P)] if halo else None
+    h = _virtual(argcsr, A, P)
+    info = h.info()
+    assert info["exchange"] == 3 and info["nranks"] == P and info["nlocal"] == P
     x0 = oracle.bench_input(A.num_cols)
-    out = power_iteration_local(engs, b, A.num_cols, torch.from_numpy(x0).cuda(), 25, slice_columns=cols)
-    lam_ref, x_ref = reference_power_iteration(A, x0, 25, 128, 1)
-    xs = [x.cpu().numpy() for _, x in out]
-    for lam, x in zip((o[0] for o in out), xs):
-        assert abs(lam - lam_ref) <= 1e-10 * abs(lam_ref)
+    dev = [torch.from_numpy(x0).cuda() for _ in range(P)]
+    outs = [torch.empty_like(dev[0]) for _ in range(P)]
+    st = [torch.cuda.current_stream().cuda_stream] * P
+    iters = 25
+    h.begin([d.data_ptr() for d in dev], True, st)
+    for i in range(iters):
+        h.step(i == iters - 1, st)
+    lam = h.finish([o.data_ptr() for o in outs], st)
+    lam_ref, x_ref = reference_power_iteration(A, x0, iters, 128, 1)
+    assert abs(lam - lam_ref) <= 1e-10 * abs(lam_ref)
+    xs = [o.cpu().numpy() for o in outs]
+    for x in xs:
         assert np.max(np.abs(x - x_ref)) <= 1e-9
     for x in xs[1:]:  # every rank assembled the same x, bit for bit
         assert bits(x) == bits(xs[0])
+    # a second run on the same buffers (absolute step numbers: no stale flag passes)
+    h.begin([d.data_ptr() for d in dev], True, st)
+    for i in range(iters):
+        h.step(i == iters - 1, st)
+    assert h.finish([o.data_ptr() for o in outs], st) == lam
+    h.free()
 
 
 @pytest.mark.parametrize("P", [2, 3])
-def test_peer_iterated_spmv_virtual_ranks(orc, P):
-    """normalize=False: x_{k+1} = A x_k assembled on every rank; each step's
-    slices are the oracle's SpMV of that rank's slice conversion, bit for bit."""
-    from paper_1203_5737_b200.multigpu import slice_rows
-    from paper_1203_5737_b200.peer import power_iteration_local
+def test_peer_iterated_spmv_virtual_ranks(argcsr, orc, P):
+    """normalize=False: x_{k+1} = A x_k assembled on every rank; each slice is
+    the oracle's SpMV of that rank's slice conversion, bit for bit."""
     import oracle
+    from paper_1203_5737_b200.multigpu import partition_bounds
 
     A = powerlaw_csr(5000, 5000, seed=8, heavy_rows=[(9, 3000)])
     A.values[:] = A.values / np.abs(A.values).sum() * 50  # keep x bounded over the steps
-    b, engs = _engines(A, P)
+    h = _virtual(argcsr, A, P)
+    b = partition_bounds(A.row_pointers, P)
     x0 = np.linspace(-1, 1, A.num_cols)
-    out = power_iteration_local(engs, b, A.num_cols, torch.from_numpy(x0).cuda(), 4, normalize=False)
-    x = x0.copy()
+    dev = [torch.from_numpy(x0).cuda() for _ in range(P)]
+    outs = [torch.empty_like(dev[0]) for _ in range(P)]
+    st = [torch.cuda.current_stream().cuda_stream] * P
+    h.begin([d.data_ptr() for d in dev], False, st)
+    for i in range(4):
+        h.step(i == 3, st)
+    h.finish([o.data_ptr() for o in outs], st)
     refs = []
     for p in range(P):
-        sl = slice_rows(A.row_pointers, A.columns, A.values, A.num_cols, int(b[p]), int(b[p + 1]))
-        refs.append(orc.argcsr_from_csr(oracle.Csr(sl.num_rows, A.num_cols, np.asarray(sl.row_pointers, np.uint64),
-                                                   np.asarray(sl.columns, np.int32), np.asarray(sl.values)), 128, 1))
+        r0, r1 = int(b[p]), int(b[p + 1])
+        a, e = int(A.row_pointers[r0]), int(A.row_pointers[r1])
+        sl = oracle.Csr(r1 - r0, A.num_cols, (A.row_pointers[r0:r1 + 1] - A.row_pointers[r0]).astype(np.uint64),
+                        A.columns[a:e], A.values[a:e])
+        refs.append(orc.argcsr_from_csr(sl, 128, 1))
+    x = x0.copy()
     for _ in range(4):
         x = np.concatenate([orc.spmv_argcsr(M, x) for M in refs])
-    for xr in out:
-        assert bits(xr.cpu().numpy()) == bits(x)
+    for o in outs:
+        assert bits(o.cpu().numpy()) == bits(x)
+    h.free()
 
 
 def _ipc_worker(rank, world, port, kind, out_dir):
@@ -129,9 +146,10 @@ def _ipc_worker(rank, world, port, kind, out_dir):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         A = stencil27(12) if kind == "stencil" else powerlaw_csr(5000, 5000, seed=2, heavy_rows=[(3, 3000)])
+        # NCCL refuses two ranks on one GPU: the IPC handles go over gloo instead
         D = DistributedArgCsr(A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values, 128, 1,
-                              device=torch.device("cuda", 0), exchange="p2p")
-        assert D.exchange == "p2p" and D.peer.peers == [1 - rank]
+                              device=torch.device("cuda", 0), exchange="p2p", nccl=False)
+        assert D.exchange == "p2p"
         x0 = oracle.bench_input(A.num_cols)
         lam, x = D.power_iteration(torch.from_numpy(x0).cuda(), 12)
         lam2, x2 = D.power_iteration(torch.from_numpy(x0).cuda(), 12)  # a second run on the same buffers

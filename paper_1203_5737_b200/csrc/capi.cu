@@ -51,6 +51,7 @@ Knobs read_knobs() {
     v.heavy_u = chr("ARGCSR_HEAVY_U", 0);
     v.heavy_b = chr("ARGCSR_HEAVY_B", 0);
     v.heavy_runs = flag("ARGCSR_HEAVY_RUNS", 0) == 1;
+    v.heavy_blocked = flag("ARGCSR_HEAVY_BLOCKED", 1) != 0;
     v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
     v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
     if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
@@ -485,13 +486,14 @@ argcsr_status argcsr_dev_spmv_norm2(const argcsr_dev* m, const void* x, const do
         SpmvSerial serial(m, static_cast<cudaStream_t>(stream));
         argcsr_dev* mm = const_cast<argcsr_dev*>(m);
         const uint64_t S = argcsr_gpu::norm_slots(m);
-        if (!mm->norm_scratch) CUDA_OK(cudaMalloc(&mm->norm_scratch, std::max<uint64_t>(S, 1) * sizeof(double)));
+        if (!mm->norm_scratch)
+            CUDA_OK(cudaMalloc(&mm->norm_scratch, (S + argcsr_gpu::norm_scratch_len(S) + 1) * sizeof(double)));
         argcsr_gpu::SpmvExtra ex;
         ex.x_scale = x_scale;
         ex.scale_is_norm2 = (flags & ARGCSR_SCALE_IS_NORM2) != 0;
         ex.norm_part = mm->norm_scratch;
         argcsr_gpu::spmv_launch(m, x, y, 0, m->num_groups, serial.s, ex);
-        argcsr_gpu::norm_reduce(mm->norm_scratch, S, y_norm2, serial.s);
+        argcsr_gpu::norm_reduce(mm->norm_scratch, S, y_norm2, serial.s, mm->norm_scratch + S);
         serial.done();
     });
 }

@@ -141,6 +141,7 @@ struct Knobs {
     char heavy_u = 0;             // ARGCSR_HEAVY_U: '4' | '8' | '1'(6) element steps in flight
     char heavy_b = 0;             // ARGCSR_HEAVY_B: '5' = 5 CTAs/SM for the fp64 heavy kernel
     bool heavy_runs = false;      // ARGCSR_HEAVY_RUNS=1: vector x loads over consecutive columns
+    bool heavy_blocked = true;    // ARGCSR_HEAVY_BLOCKED=0: heavy groups walked lane by lane (no j-blocks)
     char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)

@@ -256,7 +256,8 @@ struct MgRank {
     cudaEvent_t ev_spmv = nullptr, ev_red = nullptr, ev_gath = nullptr;
     void* X[2] = {nullptr, nullptr};
     bool own_x = true;
-    double* part = nullptr;       // 3 regions of norm_slots(m) partials
+    double* part = nullptr;       // 3 regions of norm_slots(m) partials, then the reduce scratch
+    uint64_t part_len = 0;
     double* s2 = nullptr;         // [0] local ||y||^2, [1] all-reduced
     // halo plan
     std::vector<std::vector<uint32_t>> need_rows;  // rows this rank reads from every owner (global)
@@ -402,7 +403,8 @@ void alloc_rank_state(argcsr_mgpu* h, MgRank& R) {
     CUDA_OK(cudaEventCreateWithFlags(&R.ev_spmv, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&R.ev_red, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&R.ev_gath, cudaEventDisableTiming));
-    CUDA_OK(cudaMalloc(&R.part, std::max<uint64_t>(3 * norm_slots(R.m), 1) * sizeof(double)));
+    R.part_len = 3 * norm_slots(R.m);
+    CUDA_OK(cudaMalloc(&R.part, (R.part_len + norm_scratch_len(R.part_len) + 1) * sizeof(double)));
     CUDA_OK(cudaMalloc(&R.s2, 2 * sizeof(double)));
     CUDA_OK(cudaMemset(R.s2, 0, 2 * sizeof(double)));
     const size_t es = esize(h->dtype);
@@ -607,7 +609,7 @@ void step_nccl(argcsr_mgpu* h, bool last, Streams st) {
             if (!first && R.comm) CUDA_OK(cudaStreamWaitEvent(s, R.ev_gath, 0));
             spmv_launch(R.m, xin, y, 0, G, s, ex);
         }
-        if (h->normalize) norm_reduce(R.part, regions * S, R.s2, s);
+        if (h->normalize) norm_reduce(R.part, regions * S, R.s2, s, R.part + R.part_len);
         order.done();
         CUDA_OK(cudaEventRecord(R.ev_spmv, s));
         CUDA_OK(cudaStreamWaitEvent(R.cs, R.ev_spmv, 0));
@@ -668,7 +670,7 @@ void step_p2p(argcsr_mgpu* h, bool last, Streams st) {
         {
             SpmvOrder order(R.m, s);
             spmv_launch(R.m, R.X[b], static_cast<char*>(R.X[nb]) + R.r0 * es, 0, R.m->num_groups, s, ex);
-            if (h->normalize) norm_reduce(R.part, norm_slots(R.m), own, s);
+            if (h->normalize) norm_reduce(R.part, norm_slots(R.m), own, s, R.part + R.part_len);
             order.done();
         }
         if (!R.peers.empty()) {

@@ -51,6 +51,7 @@ struct SpmvArgs {
     const T* __restrict__ x;
     T* __restrict__ y;
     uint32_t heavy_ctas;
+    uint32_t norm_light0;     // first light-tile slot of norm_part (after the heavy CTAs' slots)
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
     uint32_t max_tile_groups;
     uint32_t max_tile_rows;
@@ -366,6 +367,141 @@ __device__ __forceinline__ uint32_t find_le(const uint32_t* arr, uint32_t n, uin
     return lo;
 }
 
+// ------------------------------------------------ blocked heavy groups
+// A long-chunk group's lane sums are long dependent chains (up to ~1,900
+// element steps per lane on R-MAT 2^24): walking them lane by lane with a few
+// steps in flight makes the group's time a latency chain, not a bandwidth
+// cost.  But only the ADDITIONS must follow the reference order (per lane, j
+// ascending, argcsr.cpp:193-203); the products are independent.  So one CTA
+// takes one heavy group and walks its block in j-blocks of J rows x W lanes
+// (B = J * W <= 2048 slots, one contiguous range of the stored arrays):
+//   * all 256 threads load the block flat -- 16-B column and 32-B value
+//     vectors, fully coalesced --, gather x and form the products into a
+//     shared-memory buffer (sentinel slots get a marker no product can take:
+//     a signalling-NaN bit pattern, since arithmetic only yields quiet NaNs);
+//   * the lane owners then add their lane's products in j order from shared
+//     memory, stopping at the marker, while the NEXT block's loads are
+//     already in flight (two buffers, one barrier per block).
+// Rows then sum their lanes in ascending order (argcsr.cpp:206-215): the
+// result is bit-identical to the lane-by-lane walk.
+constexpr uint32_t kHeavyBlockSlots = 2048;
+constexpr unsigned long long kSentinelBits = 0x7FF4A2C5E6D10B37ull;  // signalling NaN
+
+template <typename T>
+__device__ __forceinline__ uint32_t heavy_block_issue(const SpmvArgs<T>& a, uint64_t base, uint32_t nslots,
+                                                      int (&c)[2][4], T (&v)[2][4], uint64_t pol) {
+    uint32_t nv = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t f = 4u * (threadIdx.x + 256u * k);
+        if (f < nslots) {
+            ld_cols<4>(a.cols + base + f, c[k], pol);
+            ld_vals<4>(a.vals + base + f, v[k], pol);
+            nv = k + 1;
+        } else {
+#pragma unroll
+            for (int l = 0; l < 4; ++l) c[k][l] = -1, v[k][l] = T(0);
+        }
+    }
+    return nv;
+}
+
+template <typename T>
+__device__ __forceinline__ void heavy_block_products(const SpmvArgs<T>& a, const int (&c)[2][4],
+                                                     const T (&v)[2][4], double* buf, uint32_t nslots,
+                                                     uint64_t pol_x, double xs) {
+    double xv[2][4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) xv[k][l] = c[k][l] != -1 ? ld_x(a.x + c[k][l], pol_x) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t f = 4u * (threadIdx.x + 256u * k);
+        if (f < nslots) {
+            double p[4];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const double x = a.x_scale ? __dmul_rn(xv[k][l], xs) : xv[k][l];
+                p[l] = c[k][l] != -1 ? __dmul_rn(double(v[k][l]), x) : __longlong_as_double(kSentinelBits);
+            }
+            reinterpret_cast<double4*>(buf + f)[0] = make_double4(p[0], p[1], p[2], p[3]);
+        }
+    }
+}
+
+// LANES: lanes per thread (1 when the group's stride <= 256, else up to 8).
+template <typename T, int LANES, int MINB, bool PEER = false>
+__global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_blocked_kernel(const SpmvArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* buf = reinterpret_cast<double*>(smem);          // [2][kHeavyBlockSlots]
+    double* s_part = buf + 2 * kHeavyBlockSlots;            // [W] lane sums
+    const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
+    const double xs = x_scale_value(a);
+    const uint32_t g = a.heavy[blockIdx.x];
+    if (g < a.g_begin || g >= a.g_end) {
+        if (a.norm_part && threadIdx.x == 0) a.norm_part[blockIdx.x] = 0.0;
+        return;
+    }
+    const GroupDesc d = a.groups[g];
+    const uint32_t W = d.stride(), C = d.chunk;
+    const uint32_t J = kHeavyBlockSlots / W;
+    const uint32_t B = J * W;
+    const uint32_t nb = (C + J - 1) / J;
+    const uint64_t base = d.offset();
+
+    double acc[LANES];
+    bool live[LANES];
+#pragma unroll
+    for (int i = 0; i < LANES; ++i) acc[i] = 0.0, live[i] = true;
+
+    int c[2][4];
+    T v[2][4];
+    uint32_t rows_b = min(J, C);
+    heavy_block_issue(a, base, rows_b * W, c, v, pol_stream);
+    heavy_block_products(a, c, v, buf, rows_b * W, pol_x, xs);
+    __syncthreads();
+    for (uint32_t b = 0; b < nb; ++b) {
+        const uint32_t cur = b & 1;
+        const uint32_t rows_n = b + 1 < nb ? min(J, C - (b + 1) * J) : 0u;
+        if (rows_n) heavy_block_issue(a, base + uint64_t(b + 1) * B, rows_n * W, c, v, pol_stream);
+        // lane sums of block b (the next block's loads are in flight)
+        const double* cb = buf + cur * kHeavyBlockSlots;
+#pragma unroll
+        for (int i = 0; i < LANES; ++i) {
+            const uint32_t l = threadIdx.x + 256u * i;
+            if (l < W && live[i]) {
+                for (uint32_t j = 0; j < rows_b; ++j) {
+                    const double p = cb[j * W + l];
+                    if (__double_as_longlong(p) == (long long)kSentinelBits) {
+                        live[i] = false;
+                        break;
+                    }
+                    acc[i] = __dadd_rn(acc[i], p);
+                }
+            }
+        }
+        if (rows_n) heavy_block_products(a, c, v, buf + (cur ^ 1) * kHeavyBlockSlots, rows_n * W, pol_x, xs);
+        rows_b = rows_n;
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < LANES; ++i) {
+        const uint32_t l = threadIdx.x + 256u * i;
+        if (l < W) s_part[l] = acc[i];
+    }
+    __syncthreads();
+    const uint32_t f = d.first_row, rows = a.groups[g + 1].first_row - f;
+    double sq = 0.0;
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+        const uint32_t row = f + r;
+        const uint32_t b0 = r == 0 ? 0u : uint32_t(a.tm[row - 1]);
+        sq = __dadd_rn(sq, store_y<PEER>(a, row, row_sum(s_part, b0, uint32_t(a.tm[row]))));
+    }
+    if (a.norm_part) write_norm_partial(a.norm_part + blockIdx.x, sq);
+}
+
 // Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
 // order, one lane per thread.
 template <typename T, int UH, bool RUNS, int MINB, bool PEER = false>
@@ -435,7 +571,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     const uint32_t kt = a.tile0 + blockIdx.x;
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
     if (ge <= a.g_begin || gs >= a.g_end || gs == ge) {
-        if (a.norm_part && threadIdx.x == 0) a.norm_part[a.heavy_ctas + kt] = 0.0;
+        if (a.norm_part && threadIdx.x == 0) a.norm_part[a.norm_light0 + kt] = 0.0;
         return;
     }
     const uint32_t ng = ge - gs;
@@ -564,7 +700,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
         sq = __dadd_rn(sq, store_y<PEER>(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r]))));
     }
-    if (a.norm_part) write_norm_partial(a.norm_part + a.heavy_ctas + kt, sq);
+    if (a.norm_part) write_norm_partial(a.norm_part + a.norm_light0 + kt, sq);
 }
 
 size_t light_smem_bytes(const argcsr_dev* m, int V, bool map = false) {
@@ -677,6 +813,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     a.x = static_cast<const T*>(x);
     a.y = static_cast<T*>(y);
     a.heavy_ctas = m->heavy_ctas;
+    a.norm_light0 = uint32_t(norm_heavy_slots(m));
     a.g_begin = gb;
     a.g_end = ge;
     a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
@@ -710,7 +847,18 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
         const bool hr = knobs().heavy_runs;
         const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
         cudaStream_t hs = fork ? m->aux : s;
-        if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
+        if (heavy_blocked(m)) {
+            // one CTA per heavy group, j-blocks through shared memory (above)
+            const size_t bsmem = (2 * size_t(kHeavyBlockSlots) + m->tpg) * sizeof(double);
+            const bool wide = m->tpg > 256;
+            if (a.npeers) {
+                if (wide) launch(spmv_heavy_blocked_kernel<T, 8, 3, true>, m->num_heavy, bsmem, m, a, hs);
+                else launch(spmv_heavy_blocked_kernel<T, 1, 4, true>, m->num_heavy, bsmem, m, a, hs);
+            } else {
+                if (wide) launch(spmv_heavy_blocked_kernel<T, 8, 3>, m->num_heavy, bsmem, m, a, hs);
+                else launch(spmv_heavy_blocked_kernel<T, 1, 4>, m->num_heavy, bsmem, m, a, hs);
+            }
+        } else if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
             if (sizeof(T) == sizeof(float)) launch(spmv_heavy_kernel<T, 4, false, 6, true>, m->heavy_ctas, smem, m, a, hs);
             else launch(spmv_heavy_kernel<T, 8, false, 4, true>, m->heavy_ctas, smem, m, a, hs);
         } else if (hr && aligned) {
@@ -776,6 +924,10 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
 
 }  // namespace
 
+bool heavy_blocked(const argcsr_dev* m) {
+    return m->num_heavy > 0 && m->lanes_per_unit == 4 && m->tpg <= kHeavyBlockSlots && knobs().heavy_blocked;
+}
+
 void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0, uint32_t t1, cudaStream_t s) {
     if (t1 <= t0) return;
     if (m->dtype == ARGCSR_F64) launch_tiles_dtype<double>(m, x, y, t0, t1, s);
@@ -793,24 +945,47 @@ void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_beg
     else launch_dtype<float>(m, x, y, gb, ge, s, ex);
 }
 
-// Fixed-order sum of the per-CTA norm partials: thread t sums entries t,
-// t + 1024, ... in order, then a fixed pairwise tree over the 1024 sums.
-__global__ void __launch_bounds__(1024) k_norm_reduce(const double* __restrict__ p, uint64_t n, double* out) {
-    __shared__ double s[1024];
-    double v = 0.0;
-    for (uint64_t i = threadIdx.x; i < n; i += 1024) v = __dadd_rn(v, p[i]);
+// Fixed-order sum of the per-CTA norm partials, in two levels so that no
+// thread walks a long dependent chain: level 1 -- CTA c sums entries
+// [c * 4096, (c + 1) * 4096) (each thread 16 consecutive entries in order,
+// then a fixed pairwise tree over the 256 thread sums); level 2 -- one CTA
+// sums the level-1 results the same way.  Deterministic run to run.
+constexpr uint32_t kNormSeg = 4096;
+
+__device__ __forceinline__ double block_tree_sum_256(double v) {
+    __shared__ double s[256];
     s[threadIdx.x] = v;
     __syncthreads();
-    for (uint32_t w = 512; w > 0; w >>= 1) {
+    for (uint32_t w = 128; w > 0; w >>= 1) {
         if (threadIdx.x < w) s[threadIdx.x] = __dadd_rn(s[threadIdx.x], s[threadIdx.x + w]);
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = s[0];
+    return s[0];
 }
 
-void norm_reduce(const double* partials, uint64_t n, double* out, cudaStream_t s) {
-    k_norm_reduce<<<1, 1024, 0, s>>>(partials, n, out);
-    LAUNCH_OK("k_norm_reduce");
+__global__ void __launch_bounds__(256) k_norm_level(const double* __restrict__ p, uint64_t n, double* __restrict__ out) {
+    const uint64_t base = uint64_t(blockIdx.x) * kNormSeg + uint64_t(threadIdx.x) * 16;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+        if (base + k < n) v = __dadd_rn(v, p[base + k]);
+    const double t = block_tree_sum_256(v);
+    if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+
+void norm_reduce(const double* partials, uint64_t n, double* out, cudaStream_t s, double* scratch) {
+    const uint64_t nb = (n + kNormSeg - 1) / kNormSeg;
+    if (nb <= 1) {
+        k_norm_level<<<1, 256, 0, s>>>(partials, n, out);
+        LAUNCH_OK("k_norm_level");
+        return;
+    }
+    if (!scratch) fail(ARGCSR_E_INTERNAL, "norm_reduce: scratch needed above 4096 partials");
+    if (nb > kNormSeg) fail(ARGCSR_E_UNSUPPORTED, "norm_reduce: more than 2^24 partials");
+    k_norm_level<<<unsigned(nb), 256, 0, s>>>(partials, n, scratch);
+    LAUNCH_OK("k_norm_level");
+    k_norm_level<<<1, 256, 0, s>>>(scratch, nb, out);
+    LAUNCH_OK("k_norm_level");
 }
 
 // ------------------------------------------------ multi-GPU step signalling

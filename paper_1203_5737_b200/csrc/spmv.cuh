@@ -48,11 +48,18 @@ struct SpmvOrder {
     }
 };
 
-inline uint64_t norm_slots(const argcsr_dev* m) { return uint64_t(m->heavy_ctas) + m->num_tiles; }
+// Heavy groups run one CTA per group (the j-blocked kernel) when this holds,
+// else packed into m->heavy_ctas CTAs (the lane-walk kernel).
+bool heavy_blocked(const argcsr_dev* m);
+inline uint64_t norm_heavy_slots(const argcsr_dev* m) {
+    return heavy_blocked(m) ? uint64_t(m->num_heavy) : uint64_t(m->heavy_ctas);
+}
+inline uint64_t norm_slots(const argcsr_dev* m) { return norm_heavy_slots(m) + m->num_tiles; }
 
-// out[0] = sum of partials[0 .. n) in index order (one CTA, fixed tree):
-// deterministic.  `accumulate_into_out` adds *out first (several regions).
-void norm_reduce(const double* partials, uint64_t n, double* out, cudaStream_t s);
+// out[0] = the sum of partials[0 .. n) in a fixed order (two levels of fixed
+// trees; deterministic).  scratch: norm_scratch_len(n) doubles when n > 4096.
+void norm_reduce(const double* partials, uint64_t n, double* out, cudaStream_t s, double* scratch = nullptr);
+inline uint64_t norm_scratch_len(uint64_t n) { return (n + 4095) / 4096; }
 
 // Step signalling between the GPUs of a multi-GPU step (spmv.cu): store
 // `value` into flags[q] (system-scope release, after *partial is copied to

@@ -156,8 +156,8 @@ class DistributedArgCsr:
         if self.exchange == "p2p":
             return per + (1 if m.x_remap else 0) + (2 if self.world > 1 else 0) + 2  # + norm reduce(s), own flag
         if self.world > 1 and self.interior[1] > self.interior[0]:
-            return 3 * per + (2 if m.x_remap else 0) + 1  # interior + two boundary ranges + norm reduce
-        return per + (1 if m.x_remap else 0) + 1
+            return 3 * per + (2 if m.x_remap else 0) + 2  # interior + two boundary ranges + 2-level norm reduce
+        return per + (1 if m.x_remap else 0) + 2
 
     def step_description(self) -> str:
         if self.exchange == "p2p":

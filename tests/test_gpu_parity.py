@@ -180,13 +180,14 @@ def test_skew_and_uniform_families(argcsr, orc, ref):  # acceptance.cpp:171-198
 
 
 # --------------------------------------------------------- larger / edge cases
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16", "ARGCSR_LIGHT_DYN=0", "ARGCSR_LIGHT_DYN=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_U=16", "ARGCSR_LIGHT_DYN=0", "ARGCSR_LIGHT_DYN=1"])
 @pytest.mark.parametrize("tpg,dcs", [(128, 1), (128, 4), (64, 2), (32, 1), (100, 1), (30, 3), (127, 1), (256, 1)])
 def test_powerlaw_heavy_groups(argcsr, orc, tpg, dcs, heavy, monkeypatch):
     """Heavy-tailed rows: long-chunk (heavy) groups, multi-tile schedule,
     through two heavy-kernel variants."""
     if heavy != "default":
-        monkeypatch.setenv(*heavy.split("="))
+        for kv in heavy.split(","):
+            monkeypatch.setenv(*kv.split("="))
         argcsr._ext.reload_options()
     A = powerlaw_csr(40000, 30000, seed=tpg * 7 + dcs, heavy_rows=[(0, 25000), (777, 12000), (39999, 9000)])
     dev = _check_case(argcsr, orc, A, tpg, dcs, f"powerlaw ({tpg},{dcs})")
@@ -244,12 +245,13 @@ def test_unsorted_columns_copied_in_stored_order(argcsr, orc):
 
 # ---------------------------------------------------------------- other APIs
 @pytest.mark.parametrize("layout", LAYOUTS)
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_RUNS=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_BLOCKED=0", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_RUNS=1"])
 def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout, heavy, monkeypatch):
     import torch
 
     if heavy != "default":
-        monkeypatch.setenv(*heavy.split("="))
+        for kv in heavy.split(","):
+            monkeypatch.setenv(*kv.split("="))
         argcsr._ext.reload_options()
 
     A = powerlaw_csr(20000, 20000, seed=11, heavy_rows=[(100, 8000)])
@@ -344,7 +346,7 @@ def test_torch_device_path(argcsr, orc):
         argcsr.spmv_torch(dev, x[:-1])
 
 
-HEAVY_VARIANTS = ["default", "ARGCSR_HEAVY_RUNS=1", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_U=4", "ARGCSR_HEAVY_B=5"]
+HEAVY_VARIANTS = ["default", "ARGCSR_HEAVY_BLOCKED=0", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_RUNS=1", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_U=4", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_B=5"]
 
 
 @pytest.mark.parametrize("heavy", HEAVY_VARIANTS)
@@ -356,7 +358,8 @@ def test_dense_rows_vector_x_runs(argcsr, orc, dtype, layout, heavy, monkeypatch
     default scalar gathers, vector x loads over runs, 4/16 steps in flight);
     results stay bit-identical (fp32: one rounding of the fp64 sum)."""
     if heavy != "default":
-        monkeypatch.setenv(*heavy.split("="))
+        for kv in heavy.split(","):
+            monkeypatch.setenv(*kv.split("="))
         argcsr._ext.reload_options()
     rng = np.random.default_rng(3)
     n = 6000

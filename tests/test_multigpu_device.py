@@ -27,13 +27,14 @@ def test_fused_scale_is_bit_identical(argcsr, orc, x_remap):
     assert bits(y1.cpu().numpy()) == bits(ref)
 
 
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_RUNS=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_BLOCKED=0,ARGCSR_HEAVY_RUNS=1"])
 def test_fused_scale_heavy_groups(argcsr, orc, heavy, monkeypatch):
     """The fused scale through the long-chunk kernel variants."""
     from helpers import powerlaw_csr
 
     if heavy != "default":
-        monkeypatch.setenv(*heavy.split("="))
+        for kv in heavy.split(","):
+            monkeypatch.setenv(*kv.split("="))
         argcsr._ext.reload_options()
     A = powerlaw_csr(20000, 20000, seed=5, heavy_rows=[(3, 12000), (9000, 7000)])
     m = argcsr.argcsr_from_csr((A.num_rows, A.num_cols, A.row_pointers, A.columns, A.values), 128, 1)

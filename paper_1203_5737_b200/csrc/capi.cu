@@ -51,7 +51,8 @@ Knobs read_knobs() {
     v.heavy_u = chr("ARGCSR_HEAVY_U", 0);
     v.heavy_b = chr("ARGCSR_HEAVY_B", 0);
     v.heavy_runs = flag("ARGCSR_HEAVY_RUNS", 0) == 1;
-    v.heavy_blocked = flag("ARGCSR_HEAVY_BLOCKED", 1) != 0;
+    v.heavy_pipe = chr("ARGCSR_HEAVY_PIPE", 0);
+    v.heavy_blocked = flag("ARGCSR_HEAVY_BLOCKED", 0) != 0;
     v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
     v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
     if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
@@ -125,6 +126,7 @@ void free_handle(argcsr_dev* m) {
     if (m->ev_join) cudaEventDestroy(m->ev_join);
     if (m->ev_done) cudaEventDestroy(m->ev_done);
     cudaFree(m->norm_scratch);
+    cudaFree(m->scale_buf);
     if (m->holds_l2_persist) release_l2_persist(m->device);
     if (prev >= 0) cudaSetDevice(prev);
     delete m;

@@ -141,7 +141,8 @@ struct Knobs {
     char heavy_u = 0;             // ARGCSR_HEAVY_U: '4' | '8' | '1'(6) element steps in flight
     char heavy_b = 0;             // ARGCSR_HEAVY_B: '5' = 5 CTAs/SM for the fp64 heavy kernel
     bool heavy_runs = false;      // ARGCSR_HEAVY_RUNS=1: vector x loads over consecutive columns
-    bool heavy_blocked = true;    // ARGCSR_HEAVY_BLOCKED=0: heavy groups walked lane by lane (no j-blocks)
+    char heavy_pipe = 0;          // ARGCSR_HEAVY_PIPE: '4' | '8' | '6'(=16) steps, columns of the next batch in flight
+    bool heavy_blocked = false;   // ARGCSR_HEAVY_BLOCKED=1: one CTA per heavy group, j-blocks through shared memory
     char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)
@@ -260,8 +261,9 @@ struct argcsr_dev {
     std::mutex mu;
     cudaEvent_t ev_done = nullptr;
     bool spmv_issued = false;
-    bool holds_l2_persist = false;
-    double* norm_scratch = nullptr;       // per-CTA ||y||^2 partials (argcsr_dev_spmv_norm2), lazily allocated        // counted in the device's persisting-L2 users (capi.cu)
+    bool holds_l2_persist = false;        // counted in the device's persisting-L2 users (capi.cu)
+    double* norm_scratch = nullptr;       // per-CTA ||y||^2 partials (argcsr_dev_spmv_norm2), lazily allocated
+    double* scale_buf = nullptr;          // [1] 1/||y_prev|| of a scale_is_norm2 SpMV (spmv.cu)
 
     uint64_t light_slots = 0;             // stored slots of light groups (stored first)
 

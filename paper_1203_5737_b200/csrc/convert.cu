@@ -800,6 +800,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
         m->heavy_ctas = uint32_t(hptr.size() - 1);
         m->heavy_max_lanes = max_lanes;
         m->heavy_ptr = dev_alloc<uint32_t>(m, hptr.size());
+        m->scale_buf = dev_alloc<double>(m, 1);
         CUDA_OK(cudaMemcpyAsync(m->heavy_ptr, hptr.data(), hptr.size() * 4, cudaMemcpyHostToDevice, s));
         CUDA_OK(cudaStreamSynchronize(s));
     }

@@ -58,7 +58,6 @@ struct SpmvArgs {
     uint32_t tile0;  // light tiles [tile0, tile0 + gridDim.x) of this launch (spmv_launch_tiles)
     uint32_t max_tile_units;
     const double* x_scale;   // y = A (s * x), s = *x_scale (device) or 1.0: each gather is fl(s * x[c])
-    int x_scale_is_norm2;    // *x_scale holds ||y_prev||^2: s = fl(1 / fl(sqrt(*x_scale))) (power iteration)
     double* norm_part;       // fused ||y||^2: one partial per CTA (heavy CTAs first, then light tiles), or null
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
@@ -258,6 +257,52 @@ __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uin
     }
 }
 
+// Phase 1 of ONE lane (V = 1, the long-chunk path), software-pipelined: the
+// columns of batch b+1 are loaded while batch b's values and x gathers are in
+// flight, so a batch of U element steps costs one memory round trip instead
+// of two (columns, then gathers).  Same additions in the same order.
+__device__ __forceinline__ int ld_col1(const int32_t* p, uint64_t pol) {
+    int c;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(c) : "l"(p), "l"(pol));
+    return c;
+}
+template <typename T, int U>
+__device__ __forceinline__ double phase1_lane_pipe(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk,
+                                                   uint64_t stride, uint64_t pol_stream, uint64_t pol_x, double xs) {
+    double s = 0.0;
+    const int32_t* cp = a.cols + slot0;
+    const T* vp = a.vals + slot0;
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = uint32_t(u) < chunk ? ld_col1(cp + uint64_t(u) * stride, pol_stream) : -1;
+    for (uint32_t j0 = 0; j0 < chunk; j0 += U) {
+        T v[U][1];
+        double xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c[u] != -1) ld_vals<1>(vp + uint64_t(j0 + u) * stride, v[u], pol_stream);
+            else v[u][0] = T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = c[u] != -1 ? ld_x(a.x + c[u], pol_x) : 0.0;
+        int cn[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            cn[u] = j0 + U + u < chunk ? ld_col1(cp + uint64_t(j0 + U + u) * stride, pol_stream) : -1;
+        if (a.x_scale) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = __dmul_rn(xv[u], xs);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (c[u] != -1) s = __dadd_rn(s, __dmul_rn(double(v[u][0]), xv[u]));
+        if (c[U - 1] == -1) break;
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = cn[u];
+    }
+    return s;
+}
+
 // Phase 1 for a thread's two units when every light chunk of the matrix is
 // <= H: both units' element steps are issued in ONE batch (columns, values,
 // then all gathers) -- the register footprint of one unit with 2H steps, half
@@ -309,9 +354,14 @@ __device__ __forceinline__ void phase1_pair(const SpmvArgs<T>& a, const uint64_t
 
 template <typename T>
 __device__ __forceinline__ double x_scale_value(const SpmvArgs<T>& a) {
-    if (!a.x_scale) return 1.0;
-    const double v = *a.x_scale;
-    return a.x_scale_is_norm2 ? __drcp_rn(__dsqrt_rn(v)) : v;
+    return a.x_scale ? *a.x_scale : 1.0;
+}
+
+// sq += v only in the kernels that write ||y||^2 partials (NORM); elsewhere
+// the squares are dead code and compiled out.
+template <bool NORM>
+__device__ __forceinline__ void acc_sq(double& sq, double v) {
+    if constexpr (NORM) sq = __dadd_rn(sq, v);
 }
 
 // Fused ||y||^2: every thread accumulates the squares of the y values it
@@ -431,7 +481,7 @@ __device__ __forceinline__ void heavy_block_products(const SpmvArgs<T>& a, const
 }
 
 // LANES: lanes per thread (1 when the group's stride <= 256, else up to 8).
-template <typename T, int LANES, int MINB, bool PEER = false>
+template <typename T, int LANES, int MINB, bool PEER = false, bool NORM = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_blocked_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* buf = reinterpret_cast<double*>(smem);          // [2][kHeavyBlockSlots]
@@ -441,7 +491,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_blocked_kernel(
     const double xs = x_scale_value(a);
     const uint32_t g = a.heavy[blockIdx.x];
     if (g < a.g_begin || g >= a.g_end) {
-        if (a.norm_part && threadIdx.x == 0) a.norm_part[blockIdx.x] = 0.0;
+        if (NORM && threadIdx.x == 0) a.norm_part[blockIdx.x] = 0.0;
         return;
     }
     const GroupDesc d = a.groups[g];
@@ -497,14 +547,14 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_blocked_kernel(
     for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
         const uint32_t row = f + r;
         const uint32_t b0 = r == 0 ? 0u : uint32_t(a.tm[row - 1]);
-        sq = __dadd_rn(sq, store_y<PEER>(a, row, row_sum(s_part, b0, uint32_t(a.tm[row]))));
+        acc_sq<NORM>(sq, store_y<PEER>(a, row, row_sum(s_part, b0, uint32_t(a.tm[row]))));
     }
-    if (a.norm_part) write_norm_partial(a.norm_part + blockIdx.x, sq);
+    if constexpr (NORM) write_norm_partial(a.norm_part + blockIdx.x, sq);
 }
 
 // Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
 // order, one lane per thread.
-template <typename T, int UH, bool RUNS, int MINB, bool PEER = false>
+template <typename T, int UH, bool RUNS, int MINB, bool PEER = false, bool NORM = false, bool PIPE = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -534,10 +584,15 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
         const uint32_t g = s_g[i];
         if (g < a.g_begin || g >= a.g_end) continue;
         const GroupDesc d = a.groups[g];
-        double s[1];
-        phase1<T, 1, UH, false, RUNS>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream, pol_x,
-                                      xs);
-        s_part[l] = s[0];
+        if constexpr (PIPE) {
+            s_part[l] = phase1_lane_pipe<T, UH>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), pol_stream,
+                                                pol_x, xs);
+        } else {
+            double s[1];
+            phase1<T, 1, UH, false, RUNS>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream,
+                                          pol_x, xs);
+            s_part[l] = s[0];
+        }
     }
     __syncthreads();
     double sq = 0.0;
@@ -548,9 +603,9 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
         const uint32_t f = a.groups[g].first_row;
         const uint32_t row = f + (r - s_row0[i]);
         const uint32_t b = row == f ? 0u : uint32_t(a.tm[row - 1]);
-        sq = __dadd_rn(sq, store_y<PEER>(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row]))));
+        acc_sq<NORM>(sq, store_y<PEER>(a, row, row_sum(s_part + s_lane0[i], b, uint32_t(a.tm[row]))));
     }
-    if (a.norm_part) write_norm_partial(a.norm_part + blockIdx.x, sq);
+    if constexpr (NORM) write_norm_partial(a.norm_part + blockIdx.x, sq);
 }
 
 // Light tile kt: consecutive short-chunk groups, V-lane units, one unit per thread.
@@ -560,7 +615,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
 // PAIR (launched when every light chunk is <= U/2 and a tile has at most two
 // units per thread): each thread's two units go through phase1_pair.
 template <typename T, int V, int U, bool PRED, int MINB, bool MAP = true, bool PEER = false, bool PAIR = false,
-          bool DYNW = false>
+          bool DYNW = false, bool NORM = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -571,7 +626,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     const uint32_t kt = a.tile0 + blockIdx.x;
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
     if (ge <= a.g_begin || gs >= a.g_end || gs == ge) {
-        if (a.norm_part && threadIdx.x == 0) a.norm_part[a.norm_light0 + kt] = 0.0;
+        if (NORM && threadIdx.x == 0) a.norm_part[a.norm_light0 + kt] = 0.0;
         return;
     }
     const uint32_t ng = ge - gs;
@@ -692,15 +747,15 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     __syncthreads();
 
     double sq = 0.0;
-    if (pvalid) sq = store_y<PEER>(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe));
+    if (pvalid) acc_sq<NORM>(sq, store_y<PEER>(a, pr, row_sum(s_part + size_t(s_ub[pgi]) * V, pb, pe)));
     for (uint32_t r = pr + blockDim.x; r < row_end; r += blockDim.x) {
         const uint32_t gi = MAP ? s_rgrp[r - row0] : find_le(s_first, ng, r);
         const uint32_t g = gs + gi;
         if ((s_off[gi] & kHeavyBit) || g < a.g_begin || g >= a.g_end) continue;
         const uint32_t b = r == s_first[gi] ? 0u : uint32_t(a.tm[r - 1]);
-        sq = __dadd_rn(sq, store_y<PEER>(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r]))));
+        acc_sq<NORM>(sq, store_y<PEER>(a, r, row_sum(s_part + size_t(s_ub[gi]) * V, b, uint32_t(a.tm[r]))));
     }
-    if (a.norm_part) write_norm_partial(a.norm_part + a.norm_light0 + kt, sq);
+    if constexpr (NORM) write_norm_partial(a.norm_part + a.norm_light0 + kt, sq);
 }
 
 size_t light_smem_bytes(const argcsr_dev* m, int V, bool map = false) {
@@ -737,7 +792,7 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 
-template <typename T, int V, int U, bool PRED, int MINB, bool PEER = false>
+template <typename T, int V, int U, bool PRED, int MINB, bool PEER, bool NORM>
 void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // small groups (units + rows per group, on average): fill the maps, else search
     const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
@@ -746,40 +801,102 @@ void launch_light(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // every light chunk <= U/2 and at most two units per thread: pair them
     const bool pair = knobs().pair != 0 && m->max_light_chunk <= uint32_t(U / 2) &&
                       m->max_tile_units <= 2 * uint64_t(kTileThreads);
+    const size_t sm_map = light_smem_bytes(m, V, true), sm_search = light_smem_bytes(m, V);
+    const unsigned grid = m->num_tiles;
     if (pair) {  // (twice the loads in flight per thread: 64 registers, 4 CTAs/SM)
-        if (map)
-            launch(spmv_light_kernel<T, V, U, PRED, 4, true, PEER, true>, m->num_tiles, light_smem_bytes(m, V, true), m,
-                   a, s);
-        else
-            launch(spmv_light_kernel<T, V, U, PRED, 4, false, PEER, true>, m->num_tiles, light_smem_bytes(m, V), m, a,
-                   s);
+        if (map) launch(spmv_light_kernel<T, V, U, PRED, 4, true, PEER, true, false, NORM>, grid, sm_map, m, a, s);
+        else launch(spmv_light_kernel<T, V, U, PRED, 4, false, PEER, true, false, NORM>, grid, sm_search, m, a, s);
     } else if (!PEER && (knobs().light_dyn >= 0 ? knobs().light_dyn == 1 : m->num_heavy > 0)) {
         // power-law matrices (heavy groups present, light chunks of every
         // size): warps take 32-unit chunks dynamically (C3 +2%; C2 -3%, so
         // not for stencils).  ARGCSR_LIGHT_DYN=0|1 forces it (experiments).
-        if (map)
-            launch(spmv_light_kernel<T, V, U, PRED, MINB, true, false, false, true>, m->num_tiles,
-                   light_smem_bytes(m, V, true), m, a, s);
-        else
-            launch(spmv_light_kernel<T, V, U, PRED, MINB, false, false, false, true>, m->num_tiles,
-                   light_smem_bytes(m, V), m, a, s);
+        if (map) launch(spmv_light_kernel<T, V, U, PRED, MINB, true, false, false, true, NORM>, grid, sm_map, m, a, s);
+        else launch(spmv_light_kernel<T, V, U, PRED, MINB, false, false, false, true, NORM>, grid, sm_search, m, a, s);
     } else if (map) {
-        launch(spmv_light_kernel<T, V, U, PRED, MINB, true, PEER>, m->num_tiles, light_smem_bytes(m, V, true), m, a,
-               s);
+        launch(spmv_light_kernel<T, V, U, PRED, MINB, true, PEER, false, false, NORM>, grid, sm_map, m, a, s);
     } else {
-        launch(spmv_light_kernel<T, V, U, PRED, MINB, false, PEER>, m->num_tiles, light_smem_bytes(m, V), m, a, s);
+        launch(spmv_light_kernel<T, V, U, PRED, MINB, false, PEER, false, false, NORM>, grid, sm_search, m, a, s);
     }
 }
 
-template <typename T, int V>
+// hardware-dispatched tiles, unpredicated value loads, 5 CTAs per SM
+// (measured best on C2-C4 with the lane-compact layout)
+template <typename T, bool PEER, bool NORM>
 void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
-    if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
-        launch_light<T, V, 4, false, 5, true>(m, a, s);
-        return;
+    switch (m->lanes_per_unit) {
+        case 4: launch_light<T, 4, 4, false, 5, PEER, NORM>(m, a, s); break;
+        case 2: launch_light<T, 2, 4, false, 5, PEER, NORM>(m, a, s); break;
+        default: launch_light<T, 1, 4, false, 5, PEER, NORM>(m, a, s); break;
     }
-    // hardware-dispatched tiles, unpredicated value loads, 5 CTAs per SM
-    // (measured best on C2-C4 with the lane-compact layout)
-    launch_light<T, V, 4, false, 5>(m, a, s);
+}
+
+// Long-chunk groups.  Default: one lane per thread, scalar x gathers; fp64 8
+// element steps in flight per lane at 4 CTAs/SM, fp32 4 steps at 6 CTAs/SM
+// with the next batch's columns loaded under the current gathers (measured
+// best on C3/C4; the pipelined walk does not help fp64).  The peer-epilogue and ||y||^2
+// kernels are the default kernel only.  Experiments (ARGCSR_HEAVY_*):
+// U = 4 | 8 | 16 steps, 5 CTAs/SM, vector loads of consecutive x entries
+// (needs x aligned to 4 entries; x' always is), and the blocked kernel (one
+// CTA per group, j-blocks through shared memory: C3 1.91 vs 1.70 ms, C4 0.78
+// vs 0.62 ms, so off by default).
+template <typename T, bool PEER, bool NORM>
+void launch_heavy(const argcsr_dev* m, const SpmvArgs<T>& a, const void* x, cudaStream_t hs) {
+    size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
+    constexpr bool f32 = sizeof(T) == sizeof(float);
+    if constexpr (PEER || NORM) {
+        if (f32) launch(spmv_heavy_kernel<T, 4, false, 6, PEER, NORM, true>, m->heavy_ctas, smem, m, a, hs);
+        else launch(spmv_heavy_kernel<T, 8, false, 4, PEER, NORM>, m->heavy_ctas, smem, m, a, hs);
+        return;
+    } else {
+        // experiments: pad the heavy CTAs' shared memory so fewer of them fit
+        // an SM and light tiles co-reside (ARGCSR_HEAVY_SMEM bytes)
+        smem = std::max<size_t>(smem, knobs().heavy_smem);
+        const char uh0 = knobs().heavy_u, hb0 = knobs().heavy_b;
+        const bool hr = knobs().heavy_runs;
+        const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
+        if (heavy_blocked(m)) {
+            const size_t bsmem = (2 * size_t(kHeavyBlockSlots) + m->tpg) * sizeof(double);
+            if (m->tpg > 256) launch(spmv_heavy_blocked_kernel<T, 8, 3>, m->num_heavy, bsmem, m, a, hs);
+            else launch(spmv_heavy_blocked_kernel<T, 1, 4>, m->num_heavy, bsmem, m, a, hs);
+        } else if (hr && aligned) {
+            if (uh0 == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
+            else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
+        } else if (knobs().heavy_pipe == '8') {
+            launch(spmv_heavy_kernel<T, 8, false, 4, false, false, true>, m->heavy_ctas, smem, m, a, hs);
+        } else if (knobs().heavy_pipe == '4') {
+            launch(spmv_heavy_kernel<T, 4, false, 6, false, false, true>, m->heavy_ctas, smem, m, a, hs);
+        } else if (knobs().heavy_pipe == '6') {
+            launch(spmv_heavy_kernel<T, 16, false, 3, false, false, true>, m->heavy_ctas, smem, m, a, hs);
+        } else if (uh0 == '1') {
+            launch(spmv_heavy_kernel<T, 16, false, 2>, m->heavy_ctas, smem, m, a, hs);
+        } else if (f32 && !uh0) {
+            // fp32: 4 steps, next columns in flight (C4 fp32 0.50 vs 0.59 ms)
+            launch(spmv_heavy_kernel<T, 4, false, 6, false, false, true>, m->heavy_ctas, smem, m, a, hs);
+        } else if (uh0 == '4') {
+            launch(spmv_heavy_kernel<T, 4, false, 6>, m->heavy_ctas, smem, m, a, hs);
+        } else if (hb0 == '5' || f32) {
+            launch(spmv_heavy_kernel<T, 8, false, 5>, m->heavy_ctas, smem, m, a, hs);
+        } else {
+            launch(spmv_heavy_kernel<T, 8, false, 4>, m->heavy_ctas, smem, m, a, hs);
+        }
+    }
+}
+
+template <typename T, bool PEER, bool NORM>
+void launch_all(const argcsr_dev* m, const SpmvArgs<T>& a, const void* x, cudaStream_t s) {
+    // Heavy groups run concurrently on the handle's auxiliary stream (forked
+    // from and joined back into `s`), launched first so their CTAs start first.
+    const bool fork = m->heavy_ctas > 0 && m->num_tiles > 0;
+    if (fork) {
+        CUDA_OK(cudaEventRecord(m->ev_fork, s));
+        CUDA_OK(cudaStreamWaitEvent(m->aux, m->ev_fork, 0));
+    }
+    if (m->heavy_ctas > 0) launch_heavy<T, PEER, NORM>(m, a, x, fork ? m->aux : s);
+    launch_v<T, PEER, NORM>(m, a, s);
+    if (fork) {
+        CUDA_OK(cudaEventRecord(m->ev_join, m->aux));
+        CUDA_OK(cudaStreamWaitEvent(s, m->ev_join, 0));
+    }
 }
 
 template <typename T>
@@ -791,7 +908,6 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     const uint64_t* peer_rows = ex.peer_rows;
     a.npeers = npeers;
     a.norm_part = ex.norm_part;
-    a.x_scale_is_norm2 = ex.scale_is_norm2 ? 1 : 0;
     for (uint32_t q = 0; q < npeers; ++q) {
         a.peer_y[q] = static_cast<T*>(peer_y[q]);
         a.peer_lo[q] = peer_rows ? uint32_t(std::min<uint64_t>(peer_rows[2 * q], m->num_rows)) : 0u;
@@ -825,63 +941,12 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     // stream is prioritised: C4 0.69 vs 0.73, C3 0.323 vs 0.325); ARGCSR_SPOL=1 for A/B
     a.stream_evict_first = knobs().stream_evict_first;
 
-    // Heavy groups run concurrently on the handle's auxiliary stream (forked
-    // from and joined back into `s`), launched first so their CTAs start first.
-    const bool fork = m->heavy_ctas > 0 && m->num_tiles > 0;
-    if (fork) {
-        CUDA_OK(cudaEventRecord(m->ev_fork, s));
-        CUDA_OK(cudaStreamWaitEvent(m->aux, m->ev_fork, 0));
-    }
-    if (m->heavy_ctas > 0) {
-        size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
-        // experiments: pad the heavy CTAs' shared memory so fewer of them fit
-        // an SM and light tiles co-reside (ARGCSR_HEAVY_SMEM bytes)
-        smem = std::max<size_t>(smem, knobs().heavy_smem);
-        // Default: scalar x gathers; fp64 8 element steps in flight per lane at
-        // 4 CTAs/SM, fp32 4 steps at 6 CTAs/SM (measured best on C3/C4,
-        // DESIGN.md §4).  Experiments: ARGCSR_HEAVY_U = 4 | 8 | 16 (steps),
-        // ARGCSR_HEAVY_B = min CTAs/SM for U=8 (4 | 5), ARGCSR_HEAVY_RUNS=1:
-        // vector loads of 2 / 4 x entries where a lane's stored columns run
-        // consecutively (needs x aligned to 4 entries; x' always is).
-        const char uh0 = knobs().heavy_u, hb0 = knobs().heavy_b;
-        const bool hr = knobs().heavy_runs;
-        const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
-        cudaStream_t hs = fork ? m->aux : s;
-        if (heavy_blocked(m)) {
-            // one CTA per heavy group, j-blocks through shared memory (above)
-            const size_t bsmem = (2 * size_t(kHeavyBlockSlots) + m->tpg) * sizeof(double);
-            const bool wide = m->tpg > 256;
-            if (a.npeers) {
-                if (wide) launch(spmv_heavy_blocked_kernel<T, 8, 3, true>, m->num_heavy, bsmem, m, a, hs);
-                else launch(spmv_heavy_blocked_kernel<T, 1, 4, true>, m->num_heavy, bsmem, m, a, hs);
-            } else {
-                if (wide) launch(spmv_heavy_blocked_kernel<T, 8, 3>, m->num_heavy, bsmem, m, a, hs);
-                else launch(spmv_heavy_blocked_kernel<T, 1, 4>, m->num_heavy, bsmem, m, a, hs);
-            }
-        } else if (a.npeers) {  // the multi-GPU peer epilogue: default kernel only
-            if (sizeof(T) == sizeof(float)) launch(spmv_heavy_kernel<T, 4, false, 6, true>, m->heavy_ctas, smem, m, a, hs);
-            else launch(spmv_heavy_kernel<T, 8, false, 4, true>, m->heavy_ctas, smem, m, a, hs);
-        } else if (hr && aligned) {
-            if (uh0 == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
-            else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
-        } else if (uh0 == '1') {
-            launch(spmv_heavy_kernel<T, 16, false, 2>, m->heavy_ctas, smem, m, a, hs);
-        } else if (uh0 ? uh0 == '4' : sizeof(T) == sizeof(float)) {
-            launch(spmv_heavy_kernel<T, 4, false, 6>, m->heavy_ctas, smem, m, a, hs);
-        } else if (hb0 == '5' || sizeof(T) == sizeof(float)) {
-            launch(spmv_heavy_kernel<T, 8, false, 5>, m->heavy_ctas, smem, m, a, hs);
-        } else {
-            launch(spmv_heavy_kernel<T, 8, false, 4>, m->heavy_ctas, smem, m, a, hs);
-        }
-    }
-    switch (m->lanes_per_unit) {
-        case 4: launch_v<T, 4>(m, a, s); break;
-        case 2: launch_v<T, 2>(m, a, s); break;
-        default: launch_v<T, 1>(m, a, s); break;
-    }
-    if (fork) {
-        CUDA_OK(cudaEventRecord(m->ev_join, m->aux));
-        CUDA_OK(cudaStreamWaitEvent(s, m->ev_join, 0));
+    if (a.npeers) {
+        if (a.norm_part) launch_all<T, true, true>(m, a, x, s);
+        else launch_all<T, true, false>(m, a, x, s);
+    } else {
+        if (a.norm_part) launch_all<T, false, true>(m, a, x, s);
+        else launch_all<T, false, false>(m, a, x, s);
     }
 }
 
@@ -934,12 +999,23 @@ void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0,
     else launch_tiles_dtype<float>(m, x, y, t0, t1, s);
 }
 
+// scale_is_norm2: s = fl(1 / fl(sqrt(||y_prev||^2))), once per SpMV into the
+// handle's scalar (the SpMV kernels then only read a plain scale).
+__global__ void k_norm2_to_scale(const double* n2, double* out) { *out = __drcp_rn(__dsqrt_rn(*n2)); }
+
 void spmv_launch(const argcsr_dev* m, const void* x, void* y, uint64_t group_begin, uint64_t group_end,
-                 cudaStream_t s, const SpmvExtra& ex) {
+                 cudaStream_t s, const SpmvExtra& ex_in) {
     const uint32_t gb = uint32_t(std::min<uint64_t>(group_begin, m->num_groups));
     const uint32_t ge = uint32_t(std::min<uint64_t>(group_end, m->num_groups));
     if (gb >= ge) return;
     Phase range("argcsr_spmv", s);  // NVTX only
+    SpmvExtra ex = ex_in;
+    if (ex.x_scale && ex.scale_is_norm2) {
+        k_norm2_to_scale<<<1, 1, 0, s>>>(ex.x_scale, m->scale_buf);
+        LAUNCH_OK("k_norm2_to_scale");
+        ex.x_scale = m->scale_buf;
+        ex.scale_is_norm2 = false;
+    }
     x = ex.reuse_x && m->x_remap ? m->xbuf : xremap_apply(m, x, s);
     if (m->dtype == ARGCSR_F64) launch_dtype<double>(m, x, y, gb, ge, s, ex);
     else launch_dtype<float>(m, x, y, gb, ge, s, ex);

@@ -141,6 +141,7 @@ struct Knobs {
     char heavy_u = 0;             // ARGCSR_HEAVY_U: '4' | '8' | '1'(6) element steps in flight
     char heavy_b = 0;             // ARGCSR_HEAVY_B: '5' = 5 CTAs/SM for the fp64 heavy kernel
     bool heavy_runs = false;      // ARGCSR_HEAVY_RUNS=1: vector x loads over consecutive columns
+    uint32_t heavy_chunk = 0;     // ARGCSR_HEAVY_CHUNK: light/heavy chunk boundary (0 = kHeavyChunk)
     char heavy_pipe = 0;          // ARGCSR_HEAVY_PIPE: '4' | '8' | '6'(=16) steps, columns of the next batch in flight
     bool heavy_blocked = false;   // ARGCSR_HEAVY_BLOCKED=1: one CTA per heavy group, j-blocks through shared memory
     char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
@@ -211,6 +212,7 @@ struct argcsr_dev {
     uint64_t num_rows = 0, num_cols = 0, nnz = 0, tpg = 0, dcs = 0;
     uint64_t num_groups = 0, total_slots = 0, max_chunk = 0;
     uint32_t max_light_chunk = 0;         // largest chunk_size among the short-chunk (light) groups
+    uint32_t heavy_chunk = 32;            // groups with chunk_size above this are heavy
     int layout = argcsr_gpu::kLayoutCompact;
     uint64_t stored_slots = 0;            // length of values/columns (== total_slots in the reference layout)
     bool tm16 = true;  // threads_mapping / assigned stored as u16 (tpg <= 65535)

@@ -266,12 +266,13 @@ struct StrideOf {
     }
 };
 
-// Long-chunk groups (chunk_size > kHeavyChunk) run on the heavy path.
+// Long-chunk groups (chunk_size > thr, default kHeavyChunk) run on the heavy path.
 template <typename TM>
 struct HeavyOf {
     const uint32_t* chunk;
     StrideOf<TM> stride;
-    __device__ bool operator()(uint64_t g) const { return chunk[g] > kHeavyChunk; }
+    uint32_t thr;
+    __device__ bool operator()(uint64_t g) const { return chunk[g] > thr; }
 };
 
 struct SlotsOf {  // chunk_size * threads_per_group (argcsr.cpp:151-152)
@@ -384,12 +385,13 @@ __global__ void k4_max_tile_groups(const uint32_t* __restrict__ tiles, uint32_t 
 }
 
 // out[0] = max chunk_size, out[1] = max chunk_size of the light (short-chunk) groups
-__global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, unsigned long long* __restrict__ out) {
+__global__ void k4_max_chunk(const uint32_t* __restrict__ chunk, uint32_t G, uint32_t thr,
+                             unsigned long long* __restrict__ out) {
     uint64_t m = 0, ml = 0;
     for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < G;
          g += uint64_t(gridDim.x) * blockDim.x) {
         m = max(m, uint64_t(chunk[g]));
-        if (chunk[g] <= kHeavyChunk) ml = max(ml, uint64_t(chunk[g]));
+        if (chunk[g] <= thr) ml = max(ml, uint64_t(chunk[g]));
     }
     m = warp_max_u64(m);
     ml = warp_max_u64(ml);
@@ -706,7 +708,10 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     // (V divides tpg, so a compact stride never exceeds threads_per_group)
     const uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
     const StrideOf<TM> stride_of{assigned, tpg, V, compact};
-    const HeavyOf<TM> heavy_of{chunk.p, stride_of};
+    // experiments: ARGCSR_HEAVY_CHUNK moves the light/heavy boundary (1..32;
+    // measured on C3: 16 -> 1.79 ms, 8 -> 2.39, 4 -> 2.66 vs 1.64 at 32)
+    m->heavy_chunk = knobs().heavy_chunk ? knobs().heavy_chunk : kHeavyChunk;
+    const HeavyOf<TM> heavy_of{chunk.p, stride_of, m->heavy_chunk};
     DevPtr<uint64_t> offset(uint64_t(G) + 1, s);
     exclusive_scan(SlotsOf{chunk.p, tpg}, G, offset.p, s);  // reference offsets
     uint64_t total_slots = 0;
@@ -737,7 +742,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     {
         DevPtr<unsigned long long> mx(2, s);
         CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
-        k4_max_chunk<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, G, mx.p);
+        k4_max_chunk<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, G, m->heavy_chunk, mx.p);
         LAUNCH_OK("k4_max_chunk");
         unsigned long long mc[2] = {0, 0};
         CUDA_OK(cudaMemcpyAsync(mc, mx.p, sizeof mc, cudaMemcpyDeviceToHost, s));

@@ -57,7 +57,51 @@ __global__ void __launch_bounds__(256, MINB) k_gather(const int32_t* cols, uint6
     }
     if (acc == 12345.678) out[0] = acc;
 }
+// Same with the values streamed too (v4.f64): the structure-free SpMV ceiling.
+__device__ __forceinline__ void ld_vals4(const double* p, double (&v)[4], uint64_t pol) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p), "l"(pol));
+}
+template <int NV, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_spmv_flat(const int32_t* cols, const double* vals, uint64_t n,
+                                                         const double* x, double* out) {
+    const uint64_t pc = pol_normal(), px = pol_last();
+    double acc = 0.0;
+    const uint64_t stride = uint64_t(gridDim.x) * 256 * 4 * NV;
+    for (uint64_t b = (uint64_t(blockIdx.x) * 256 * NV + threadIdx.x) * 4; b < n; b += stride) {
+        int c[NV][4];
+        double v[NV][4];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const uint64_t i = b + uint64_t(q) * 1024;
+            if (i + 3 < n) {
+                ld_cols4(cols + i, c[q], pc);
+                ld_vals4(vals + i, v[q], pc);
+            } else {
+#pragma unroll
+                for (int l = 0; l < 4; ++l) c[q][l] = 0, v[q][l] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+#pragma unroll
+            for (int l = 0; l < 4; ++l) acc += v[q][l] * ldx<0>(x + c[q][l], px);
+    }
+    if (acc == 12345.678) out[0] = acc;
+}
 }  // namespace
+
+extern "C" int probe_spmv_flat(int variant, const int32_t* cols, const double* vals, uint64_t n, const double* x,
+                               double* out, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (variant == 0) k_spmv_flat<2, 4><<<sms * 4, 256, 0, s>>>(cols, vals, n, x, out);
+    else if (variant == 1) k_spmv_flat<1, 8><<<sms * 8, 256, 0, s>>>(cols, vals, n, x, out);
+    else k_spmv_flat<4, 2><<<sms * 2, 256, 0, s>>>(cols, vals, n, x, out);
+    return int(cudaGetLastError());
+}
 
 template <typename K>
 static void go(K k, int ctas_per_sm, const int32_t* cols, uint64_t n, const double* x, double* out, cudaStream_t s) {

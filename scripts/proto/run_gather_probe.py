@@ -13,6 +13,7 @@ import workloads  # noqa: E402
 lib = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgather_probe.so"))
 P = ctypes.c_void_p
 lib.probe_gather.argtypes = [ctypes.c_int, P, ctypes.c_uint64, P, P, P]
+lib.probe_spmv_flat.argtypes = [ctypes.c_int, P, P, ctypes.c_uint64, P, P, P]
 
 
 def timeit(fn, n=20, warm=3):
@@ -46,6 +47,28 @@ streams = {
 c = A.columns[: (n // 2048) * 2048].view(-1, 2048)
 streams["c3_sorted2048"] = torch.sort(c, dim=1).values.flatten().contiguous()
 streams["c3_shuffled"] = A.columns[torch.randperm(n, device="cuda", generator=g)]
+deg = torch.bincount(A.columns.long(), minlength=N)
+order = torch.argsort(-deg, stable=True)
+newidx = torch.empty_like(order)
+newidx[order] = torch.arange(N, device="cuda")
+streams["c3_degree_rank"] = newidx[A.columns.long()].to(torch.int32)
+# octave ranks (the product's x remap): floor(log2 deg) descending, index order within an octave
+octv = torch.where(deg > 0, torch.floor(torch.log2(deg.clamp(min=1).double())), torch.full_like(deg, -1, dtype=torch.float64))
+order2 = torch.argsort(-octv, stable=True)
+newidx2 = torch.empty_like(order2)
+newidx2[order2] = torch.arange(N, device="cuda")
+streams["c3_octave_rank"] = newidx2[A.columns.long()].to(torch.int32)
+for name in ("c3_csr", "c3_shuffled", "c3_degree_rank", "c3_octave_rank"):
+    cols = streams[name].contiguous()
+    res = {"flat_spmv": name}
+    for v in (0, 1, 2):
+        ms = timeit(lambda: lib.probe_spmv_flat(v, cols.data_ptr(), A.values.data_ptr(), n, x.data_ptr(),
+                                                out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        res[f"v{v}_ms"] = round(ms, 4)
+        res[f"v{v}_frac"] = round((n * 12 + 2 * N * 8) / ms / 1e6 / 6538.3, 4)
+    print(json.dumps(res), flush=True)
+if os.environ.get("FLAT_ONLY"):
+    sys.exit(0)
 for name, cols in streams.items():
     cols = cols.contiguous()
     nn = cols.numel()

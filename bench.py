@@ -351,6 +351,16 @@ def run_b200(args):
     stream = torch.cuda.Stream(dev)
     D = None
     distributed_path = world > 1 or args.power_iteration or os.environ.get("ARGCSR_BENCH_DIST") == "1"
+    # one small conversion + SpMV first, so that lazy kernel-module loading and
+    # first-call setup are not charged to the conversion time below
+    _w = workloads.stencil3d27(12, dev)
+    _wm = argcsr.argcsr_from_torch(_w.num_rows, _w.num_cols, _w.row_pointers, _w.columns, _w.values.to(tdtype),
+                                   args.tpg, args.dcs, stream=stream, layout=args.layout, x_remap=args.x_remap)
+    _wy = torch.empty(_w.num_rows, dtype=tdtype, device=dev)
+    _wm.spmv_device(workloads.bench_input(_w.num_cols, dev, tdtype).data_ptr(), _wy.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    _wm.free()
+    del _w, _wm, _wy
     t_conv = time.perf_counter()
     with torch.cuda.stream(stream):
         if distributed_path:

@@ -789,6 +789,8 @@ void launch(K kern, unsigned grid, size_t smem, const argcsr_dev* m, const SpmvA
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
+    if (knobs().carveout >= 0)  // experiments: shared memory / L1 split (percent of the maximum carve-out)
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, knobs().carveout));
     CUDA_OK(cudaLaunchKernelEx(&cfg, kern, a));
 }
 

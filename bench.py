@@ -242,10 +242,16 @@ def run_reference(args):
     ref = oracle.ref()
     t = time.perf_counter()
     A = cfg["gen"]("cpu")
+    config = make_config(args, A, args.gpus, cfg)
+    slice_note = ""
+    if args.config == "C5":
+        # bounded sample: the reference would need ~50 GB of host memory for all
+        # 879 M nnz at (128, 1); time one GPU's share at 8 GPUs (rows [0, N/8))
+        A = A.slice_rows(0, A.num_rows // 8)
+        slice_note = f"; rows [0, {A.num_rows}) = one GPU's share of C5 at 8 GPUs (bounded host memory)"
     csr = oracle.Csr(A.num_rows, A.num_cols, A.row_pointers.numpy().view(np.uint64), A.columns.numpy(),
                      A.values.numpy())
     gen_s = time.perf_counter() - t
-    config = make_config(args, A, args.gpus, cfg)
     t = time.perf_counter()
     h = ref.argcsr_handle(csr, args.tpg, args.dcs)
     conv_s = time.perf_counter() - t
@@ -263,7 +269,7 @@ def run_reference(args):
     cores, model = cpu_info()
     sample = (f"{steps} x spmv_argcsr_parallel over the full {args.config} matrix "
               f"(tpg={args.tpg}, dcs={args.dcs}) after {args.warmup} warm-up, median of individually timed runs; "
-              f"workers={workers}")
+              f"workers={workers}{slice_note}")
     out = {
         "impl": "reference", "metric": "SpMV GFLOP/s", "value": round(gflops, 4), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": med * 1e3,
@@ -476,6 +482,8 @@ def run_b200(args):
         out["power_iteration"] = {"steps_total": args.warmup + args.steps, "lambda": pi_lambda,
                                   "exchange": D.exchange, "step": D.step_description()}
     rc = 0
+    if args.power_iteration and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_c5_share(args, A)
     if e2e_dist is not None:
         out["e2e"] = e2e_dist
     elif world == 1 and D is None:
@@ -670,6 +678,36 @@ def variants(args, A, x, tdtype, sv, stream, x_remap=False):
         res.append(r)
     torch.cuda.empty_cache()
     return res
+
+
+def cpu_baseline_c5_share(args, A):
+    """CPU baseline of the power-iteration config, bounded: the reference's
+    spmv_argcsr_parallel (oracle/_ref, all host threads) on one GPU's share of
+    the rows at 8 GPUs (rows [0, N/8)), the unit each GPU converts and
+    multiplies in the row-partitioned step; same metric (GFLOP/s)."""
+    import numpy as np
+
+    try:
+        import oracle
+    except Exception as e:
+        return {"value": None, "error": f"oracle unavailable: {e}"}
+    if not oracle.ref_available():
+        return {"value": None, "error": "oracle/_ref not built"}
+    ref = oracle.ref()
+    S = A.slice_rows(0, A.num_rows // 8)
+    csr = ref_csr(S)
+    h = ref.argcsr_handle(csr, args.tpg, args.dcs)
+    workers = os.cpu_count()
+    xh = oracle.bench_input(S.num_cols)
+    times, _ = ref.time_spmv_argcsr_parallel(h, xh, workers, 2, args.cpu_sample_steps, S.num_rows)
+    ref.free_argcsr(h)
+    med = float(np.median(times))
+    _, model = cpu_info()
+    return {"value": round(2.0 * S.nnz / med / 1e9, 4), "unit": "GFLOP/s", "cores": workers, "kind": "reference",
+            "sample": f"{args.cpu_sample_steps} x spmv_argcsr_parallel (oracle/_ref, {workers} threads) on rows "
+                      f"[0, {S.num_rows}) of {args.config} ({S.nnz} nnz: one GPU's share at 8 GPUs; the full matrix "
+                      f"would need ~50 GB of host memory in the reference layout), after 2 warm-up, median",
+            "ms_per_step": med * 1e3, "cpu_model": model}
 
 
 def cpu_baseline_and_parity(args, m, A, x, y, stream):

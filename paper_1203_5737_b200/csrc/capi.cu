@@ -47,13 +47,8 @@ Knobs read_knobs() {
     v.map = flag("ARGCSR_MAP", -1);
     v.pair = flag("ARGCSR_PAIR", 1);
     v.light_dyn = flag("ARGCSR_LIGHT_DYN", -1);
-    if (const char* e = std::getenv("ARGCSR_HEAVY_SMEM")) v.heavy_smem = size_t(std::atol(e));
-    v.heavy_u = chr("ARGCSR_HEAVY_U", 0);
-    v.heavy_b = chr("ARGCSR_HEAVY_B", 0);
-    v.heavy_runs = flag("ARGCSR_HEAVY_RUNS", 0) == 1;
     v.heavy_pipe = chr("ARGCSR_HEAVY_PIPE", 0);
     if (const char* e = std::getenv("ARGCSR_HEAVY_CHUNK")) v.heavy_chunk = uint32_t(std::min(32, std::max(0, std::atoi(e))));
-    v.heavy_blocked = flag("ARGCSR_HEAVY_BLOCKED", 0) != 0;
     v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
     v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
     if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);

@@ -137,13 +137,8 @@ struct Knobs {
     int map = -1;                 // ARGCSR_MAP: unit/row -> group maps in shared memory (1/0)
     int pair = 1;                 // ARGCSR_PAIR=0: never the paired-unit light kernel
     int light_dyn = -1;           // ARGCSR_LIGHT_DYN: warp-granular dynamic light units (1/0)
-    size_t heavy_smem = 0;        // ARGCSR_HEAVY_SMEM: pad heavy CTAs' shared memory (bytes)
-    char heavy_u = 0;             // ARGCSR_HEAVY_U: '4' | '8' | '1'(6) element steps in flight
-    char heavy_b = 0;             // ARGCSR_HEAVY_B: '5' = 5 CTAs/SM for the fp64 heavy kernel
-    bool heavy_runs = false;      // ARGCSR_HEAVY_RUNS=1: vector x loads over consecutive columns
     uint32_t heavy_chunk = 0;     // ARGCSR_HEAVY_CHUNK: light/heavy chunk boundary (0 = kHeavyChunk)
-    char heavy_pipe = 0;          // ARGCSR_HEAVY_PIPE: '4' | '8' | '6'(=16) steps, columns of the next batch in flight
-    bool heavy_blocked = false;   // ARGCSR_HEAVY_BLOCKED=1: one CTA per heavy group, j-blocks through shared memory
+    char heavy_pipe = 0;          // ARGCSR_HEAVY_PIPE: '1' pipelined / '0' plain lane walk (default: fp32 pipelined)
     char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)

@@ -132,66 +132,12 @@ __device__ __forceinline__ double ld_x(const float* p, uint64_t pol) {
     return double(v);
 }
 
-// x runs: 2 or 4 consecutive x entries in one 16-/32-byte load (one L1
-// wavefront instead of 2 or 4 for a warp whose lanes are far apart).
-__device__ __forceinline__ void ld_x2(const double* p, double (&v)[2], uint64_t pol) {
-    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
-}
-__device__ __forceinline__ void ld_x2(const float* p, double (&v)[2], uint64_t pol) {
-    float a, b;
-    asm("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(a), "=f"(b) : "l"(p), "l"(pol));
-    v[0] = a, v[1] = b;
-}
-__device__ __forceinline__ void ld_x4(const double* p, double (&v)[4], uint64_t pol) {
-    asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
-        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p), "l"(pol));
-}
-__device__ __forceinline__ void ld_x4(const float* p, double (&v)[4], uint64_t pol) {
-    float a, b, c, d;
-    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(p), "l"(pol));
-    v[0] = a, v[1] = b, v[2] = c, v[3] = d;
-}
-
-// x of U consecutive element steps of ONE lane (V = 1: the heavy path).  A
-// lane holds a contiguous run of its row's entries, so when the columns of 4
-// (2) steps are consecutive and the first is 4- (2-) element aligned, one
-// vector load replaces 4 (2) gathers.  Same values, so bit-identical.
-template <typename T, int U>
-__device__ __forceinline__ void gather_lane_runs(const T* x, const int (&c)[U][1], double (&xv)[U][1], uint64_t pol) {
-#pragma unroll
-    for (int q = 0; q < U / 4; ++q) {
-        const int c0 = c[4 * q][0];
-        const bool run4 = c0 >= 0 && (c0 & 3) == 0 && c[4 * q + 1][0] == c0 + 1 && c[4 * q + 2][0] == c0 + 2 &&
-                          c[4 * q + 3][0] == c0 + 3;
-        if (run4) {
-            double t[4];
-            ld_x4(x + c0, t, pol);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) xv[4 * q + k][0] = t[k];
-            continue;
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int a = c[4 * q + 2 * h][0], b = c[4 * q + 2 * h + 1][0];
-            if (a >= 0 && (a & 1) == 0 && b == a + 1) {
-                double t[2];
-                ld_x2(x + a, t, pol);
-                xv[4 * q + 2 * h][0] = t[0], xv[4 * q + 2 * h + 1][0] = t[1];
-            } else {
-                xv[4 * q + 2 * h][0] = a != -1 ? ld_x(x + a, pol) : 0.0;
-                xv[4 * q + 2 * h + 1][0] = b != -1 ? ld_x(x + b, pol) : 0.0;
-            }
-        }
-    }
-}
-
 // Phase 1 (argcsr.cpp:193-203) for V adjacent lanes starting at slot0: per
 // lane, sum += v * x[c] over j ascending until the first sentinel.  Columns
 // and values of U element steps are issued together (values of a fully
 // finished vector are skipped when PRED); the layout keeps sentinels
 // trailing, so "skip sentinel" == "stop at the first sentinel".
-template <typename T, int V, int U, bool PRED, bool HEAVY_RUNS = false>
+template <typename T, int V, int U, bool PRED>
 __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uint32_t chunk, uint64_t stride,
                                        double (&s)[V], uint64_t pol_stream, uint64_t pol_x, double xs,
                                        uint32_t jstart = 0) {
@@ -230,15 +176,10 @@ __device__ __forceinline__ void phase1(const SpmvArgs<T>& a, uint64_t slot0, uin
             }
         }
         double xv[U][V];
-        if constexpr (V == 1 && U % 4 == 0 && HEAVY_RUNS) {
-            gather_lane_runs<T, U>(a.x, c, xv, pol_x);
-        } else {
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int l = 0; l < V; ++l)
-                    xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
-        }
+            for (int l = 0; l < V; ++l) xv[u][l] = c[u][l] != -1 ? ld_x(a.x + c[u][l], pol_x) : 0.0;
         if (a.x_scale) {  // uniform: fused normalisation of the power iteration
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -417,144 +358,9 @@ __device__ __forceinline__ uint32_t find_le(const uint32_t* arr, uint32_t n, uin
     return lo;
 }
 
-// ------------------------------------------------ blocked heavy groups
-// A long-chunk group's lane sums are long dependent chains (up to ~1,900
-// element steps per lane on R-MAT 2^24): walking them lane by lane with a few
-// steps in flight makes the group's time a latency chain, not a bandwidth
-// cost.  But only the ADDITIONS must follow the reference order (per lane, j
-// ascending, argcsr.cpp:193-203); the products are independent.  So one CTA
-// takes one heavy group and walks its block in j-blocks of J rows x W lanes
-// (B = J * W <= 2048 slots, one contiguous range of the stored arrays):
-//   * all 256 threads load the block flat -- 16-B column and 32-B value
-//     vectors, fully coalesced --, gather x and form the products into a
-//     shared-memory buffer (sentinel slots get a marker no product can take:
-//     a signalling-NaN bit pattern, since arithmetic only yields quiet NaNs);
-//   * the lane owners then add their lane's products in j order from shared
-//     memory, stopping at the marker, while the NEXT block's loads are
-//     already in flight (two buffers, one barrier per block).
-// Rows then sum their lanes in ascending order (argcsr.cpp:206-215): the
-// result is bit-identical to the lane-by-lane walk.
-constexpr uint32_t kHeavyBlockSlots = 2048;
-constexpr unsigned long long kSentinelBits = 0x7FF4A2C5E6D10B37ull;  // signalling NaN
-
-template <typename T>
-__device__ __forceinline__ uint32_t heavy_block_issue(const SpmvArgs<T>& a, uint64_t base, uint32_t nslots,
-                                                      int (&c)[2][4], T (&v)[2][4], uint64_t pol) {
-    uint32_t nv = 0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t f = 4u * (threadIdx.x + 256u * k);
-        if (f < nslots) {
-            ld_cols<4>(a.cols + base + f, c[k], pol);
-            ld_vals<4>(a.vals + base + f, v[k], pol);
-            nv = k + 1;
-        } else {
-#pragma unroll
-            for (int l = 0; l < 4; ++l) c[k][l] = -1, v[k][l] = T(0);
-        }
-    }
-    return nv;
-}
-
-template <typename T>
-__device__ __forceinline__ void heavy_block_products(const SpmvArgs<T>& a, const int (&c)[2][4],
-                                                     const T (&v)[2][4], double* buf, uint32_t nslots,
-                                                     uint64_t pol_x, double xs) {
-    double xv[2][4];
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int l = 0; l < 4; ++l) xv[k][l] = c[k][l] != -1 ? ld_x(a.x + c[k][l], pol_x) : 0.0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const uint32_t f = 4u * (threadIdx.x + 256u * k);
-        if (f < nslots) {
-            double p[4];
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const double x = a.x_scale ? __dmul_rn(xv[k][l], xs) : xv[k][l];
-                p[l] = c[k][l] != -1 ? __dmul_rn(double(v[k][l]), x) : __longlong_as_double(kSentinelBits);
-            }
-            reinterpret_cast<double4*>(buf + f)[0] = make_double4(p[0], p[1], p[2], p[3]);
-        }
-    }
-}
-
-// LANES: lanes per thread (1 when the group's stride <= 256, else up to 8).
-template <typename T, int LANES, int MINB, bool PEER = false, bool NORM = false>
-__global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_blocked_kernel(const SpmvArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double* buf = reinterpret_cast<double*>(smem);          // [2][kHeavyBlockSlots]
-    double* s_part = buf + 2 * kHeavyBlockSlots;            // [W] lane sums
-    const uint64_t pol_stream = a.stream_evict_first ? policy_evict_first() : policy_evict_normal();
-    const uint64_t pol_x = a.x_evict_last ? policy_evict_last() : policy_evict_normal();
-    const double xs = x_scale_value(a);
-    const uint32_t g = a.heavy[blockIdx.x];
-    if (g < a.g_begin || g >= a.g_end) {
-        if (NORM && threadIdx.x == 0) a.norm_part[blockIdx.x] = 0.0;
-        return;
-    }
-    const GroupDesc d = a.groups[g];
-    const uint32_t W = d.stride(), C = d.chunk;
-    const uint32_t J = kHeavyBlockSlots / W;
-    const uint32_t B = J * W;
-    const uint32_t nb = (C + J - 1) / J;
-    const uint64_t base = d.offset();
-
-    double acc[LANES];
-    bool live[LANES];
-#pragma unroll
-    for (int i = 0; i < LANES; ++i) acc[i] = 0.0, live[i] = true;
-
-    int c[2][4];
-    T v[2][4];
-    uint32_t rows_b = min(J, C);
-    heavy_block_issue(a, base, rows_b * W, c, v, pol_stream);
-    heavy_block_products(a, c, v, buf, rows_b * W, pol_x, xs);
-    __syncthreads();
-    for (uint32_t b = 0; b < nb; ++b) {
-        const uint32_t cur = b & 1;
-        const uint32_t rows_n = b + 1 < nb ? min(J, C - (b + 1) * J) : 0u;
-        if (rows_n) heavy_block_issue(a, base + uint64_t(b + 1) * B, rows_n * W, c, v, pol_stream);
-        // lane sums of block b (the next block's loads are in flight)
-        const double* cb = buf + cur * kHeavyBlockSlots;
-#pragma unroll
-        for (int i = 0; i < LANES; ++i) {
-            const uint32_t l = threadIdx.x + 256u * i;
-            if (l < W && live[i]) {
-                for (uint32_t j = 0; j < rows_b; ++j) {
-                    const double p = cb[j * W + l];
-                    if (__double_as_longlong(p) == (long long)kSentinelBits) {
-                        live[i] = false;
-                        break;
-                    }
-                    acc[i] = __dadd_rn(acc[i], p);
-                }
-            }
-        }
-        if (rows_n) heavy_block_products(a, c, v, buf + (cur ^ 1) * kHeavyBlockSlots, rows_n * W, pol_x, xs);
-        rows_b = rows_n;
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < LANES; ++i) {
-        const uint32_t l = threadIdx.x + 256u * i;
-        if (l < W) s_part[l] = acc[i];
-    }
-    __syncthreads();
-    const uint32_t f = d.first_row, rows = a.groups[g + 1].first_row - f;
-    double sq = 0.0;
-    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-        const uint32_t row = f + r;
-        const uint32_t b0 = r == 0 ? 0u : uint32_t(a.tm[row - 1]);
-        acc_sq<NORM>(sq, store_y<PEER>(a, row, row_sum(s_part, b0, uint32_t(a.tm[row]))));
-    }
-    if constexpr (NORM) write_norm_partial(a.norm_part + blockIdx.x, sq);
-}
-
 // Heavy groups heavy[hb..he) packed into one CTA: lanes and rows flattened in
 // order, one lane per thread.
-template <typename T, int UH, bool RUNS, int MINB, bool PEER = false, bool NORM = false, bool PIPE = false>
+template <typename T, int UH, int MINB, bool PEER = false, bool NORM = false, bool PIPE = false>
 __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const SpmvArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* s_part = reinterpret_cast<double*>(smem);
@@ -589,8 +395,8 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
                                                 pol_x, xs);
         } else {
             double s[1];
-            phase1<T, 1, UH, false, RUNS>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream,
-                                          pol_x, xs);
+            phase1<T, 1, UH, false>(a, d.offset() + (l - s_lane0[i]), d.chunk, d.stride(), s, pol_stream, pol_x,
+                                    xs);
             s_part[l] = s[0];
         }
     }
@@ -832,60 +638,30 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     }
 }
 
-// Long-chunk groups.  Default: one lane per thread, scalar x gathers; fp64 8
-// element steps in flight per lane at 4 CTAs/SM, fp32 4 steps at 6 CTAs/SM
-// with the next batch's columns loaded under the current gathers (measured
-// best on C3/C4; the pipelined walk does not help fp64).  The peer-epilogue and ||y||^2
-// kernels are the default kernel only.  Experiments (ARGCSR_HEAVY_*):
-// U = 4 | 8 | 16 steps, 5 CTAs/SM, vector loads of consecutive x entries
-// (needs x aligned to 4 entries; x' always is), and the blocked kernel (one
-// CTA per group, j-blocks through shared memory: C3 1.91 vs 1.70 ms, C4 0.78
-// vs 0.62 ms, so off by default).
+// Long-chunk groups: one lane per thread, scalar x gathers, lanes of
+// consecutive LPT-ordered groups packed into 256-thread CTAs.  fp64: 8 element
+// steps in flight per lane at 4 CTAs/SM; fp32: 4 steps at 6 CTAs/SM with the
+// next batch's columns loaded under the current gathers (C4 fp32 0.59 ->
+// 0.50 ms; the pipelined walk does not help fp64).  ARGCSR_HEAVY_PIPE=0|1
+// swaps the two walks (A/B, tests).  Variants measured and removed from the
+// library are listed in DESIGN.md section 4.
 template <typename T, bool PEER, bool NORM>
-void launch_heavy(const argcsr_dev* m, const SpmvArgs<T>& a, const void* x, cudaStream_t hs) {
-    size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
+void launch_heavy(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t hs) {
+    const size_t smem = size_t(std::max<uint64_t>(m->heavy_max_lanes, 1)) * sizeof(double);
     constexpr bool f32 = sizeof(T) == sizeof(float);
-    if constexpr (PEER || NORM) {
-        if (f32) launch(spmv_heavy_kernel<T, 4, false, 6, PEER, NORM, true>, m->heavy_ctas, smem, m, a, hs);
-        else launch(spmv_heavy_kernel<T, 8, false, 4, PEER, NORM>, m->heavy_ctas, smem, m, a, hs);
-        return;
+    const char hp = knobs().heavy_pipe;
+    const bool pipe = hp ? hp == '1' : f32;
+    if constexpr (f32) {
+        if (pipe) launch(spmv_heavy_kernel<T, 4, 6, PEER, NORM, true>, m->heavy_ctas, smem, m, a, hs);
+        else launch(spmv_heavy_kernel<T, 4, 6, PEER, NORM, false>, m->heavy_ctas, smem, m, a, hs);
     } else {
-        // experiments: pad the heavy CTAs' shared memory so fewer of them fit
-        // an SM and light tiles co-reside (ARGCSR_HEAVY_SMEM bytes)
-        smem = std::max<size_t>(smem, knobs().heavy_smem);
-        const char uh0 = knobs().heavy_u, hb0 = knobs().heavy_b;
-        const bool hr = knobs().heavy_runs;
-        const bool aligned = reinterpret_cast<uintptr_t>(x) % (4 * sizeof(T)) == 0;
-        if (heavy_blocked(m)) {
-            const size_t bsmem = (2 * size_t(kHeavyBlockSlots) + m->tpg) * sizeof(double);
-            if (m->tpg > 256) launch(spmv_heavy_blocked_kernel<T, 8, 3>, m->num_heavy, bsmem, m, a, hs);
-            else launch(spmv_heavy_blocked_kernel<T, 1, 4>, m->num_heavy, bsmem, m, a, hs);
-        } else if (hr && aligned) {
-            if (uh0 == '1') launch(spmv_heavy_kernel<T, 16, true, 2>, m->heavy_ctas, smem, m, a, hs);
-            else launch(spmv_heavy_kernel<T, 8, true, 4>, m->heavy_ctas, smem, m, a, hs);
-        } else if (knobs().heavy_pipe == '8') {
-            launch(spmv_heavy_kernel<T, 8, false, 4, false, false, true>, m->heavy_ctas, smem, m, a, hs);
-        } else if (knobs().heavy_pipe == '4') {
-            launch(spmv_heavy_kernel<T, 4, false, 6, false, false, true>, m->heavy_ctas, smem, m, a, hs);
-        } else if (knobs().heavy_pipe == '6') {
-            launch(spmv_heavy_kernel<T, 16, false, 3, false, false, true>, m->heavy_ctas, smem, m, a, hs);
-        } else if (uh0 == '1') {
-            launch(spmv_heavy_kernel<T, 16, false, 2>, m->heavy_ctas, smem, m, a, hs);
-        } else if (f32 && !uh0) {
-            // fp32: 4 steps, next columns in flight (C4 fp32 0.50 vs 0.59 ms)
-            launch(spmv_heavy_kernel<T, 4, false, 6, false, false, true>, m->heavy_ctas, smem, m, a, hs);
-        } else if (uh0 == '4') {
-            launch(spmv_heavy_kernel<T, 4, false, 6>, m->heavy_ctas, smem, m, a, hs);
-        } else if (hb0 == '5' || f32) {
-            launch(spmv_heavy_kernel<T, 8, false, 5>, m->heavy_ctas, smem, m, a, hs);
-        } else {
-            launch(spmv_heavy_kernel<T, 8, false, 4>, m->heavy_ctas, smem, m, a, hs);
-        }
+        if (pipe) launch(spmv_heavy_kernel<T, 8, 4, PEER, NORM, true>, m->heavy_ctas, smem, m, a, hs);
+        else launch(spmv_heavy_kernel<T, 8, 4, PEER, NORM, false>, m->heavy_ctas, smem, m, a, hs);
     }
 }
 
 template <typename T, bool PEER, bool NORM>
-void launch_all(const argcsr_dev* m, const SpmvArgs<T>& a, const void* x, cudaStream_t s) {
+void launch_all(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     // Heavy groups run concurrently on the handle's auxiliary stream (forked
     // from and joined back into `s`), launched first so their CTAs start first.
     const bool fork = m->heavy_ctas > 0 && m->num_tiles > 0;
@@ -893,7 +669,7 @@ void launch_all(const argcsr_dev* m, const SpmvArgs<T>& a, const void* x, cudaSt
         CUDA_OK(cudaEventRecord(m->ev_fork, s));
         CUDA_OK(cudaStreamWaitEvent(m->aux, m->ev_fork, 0));
     }
-    if (m->heavy_ctas > 0) launch_heavy<T, PEER, NORM>(m, a, x, fork ? m->aux : s);
+    if (m->heavy_ctas > 0) launch_heavy<T, PEER, NORM>(m, a, fork ? m->aux : s);
     launch_v<T, PEER, NORM>(m, a, s);
     if (fork) {
         CUDA_OK(cudaEventRecord(m->ev_join, m->aux));
@@ -944,11 +720,11 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     a.stream_evict_first = knobs().stream_evict_first;
 
     if (a.npeers) {
-        if (a.norm_part) launch_all<T, true, true>(m, a, x, s);
-        else launch_all<T, true, false>(m, a, x, s);
+        if (a.norm_part) launch_all<T, true, true>(m, a, s);
+        else launch_all<T, true, false>(m, a, s);
     } else {
-        if (a.norm_part) launch_all<T, false, true>(m, a, x, s);
-        else launch_all<T, false, false>(m, a, x, s);
+        if (a.norm_part) launch_all<T, false, true>(m, a, s);
+        else launch_all<T, false, false>(m, a, s);
     }
 }
 
@@ -991,9 +767,6 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
 
 }  // namespace
 
-bool heavy_blocked(const argcsr_dev* m) {
-    return m->num_heavy > 0 && m->lanes_per_unit == 4 && m->tpg <= kHeavyBlockSlots && knobs().heavy_blocked;
-}
 
 void spmv_launch_tiles(const argcsr_dev* m, const void* x, void* y, uint32_t t0, uint32_t t1, cudaStream_t s) {
     if (t1 <= t0) return;

@@ -48,12 +48,8 @@ struct SpmvOrder {
     }
 };
 
-// Heavy groups run one CTA per group (the j-blocked kernel) when this holds,
-// else packed into m->heavy_ctas CTAs (the lane-walk kernel).
-bool heavy_blocked(const argcsr_dev* m);
-inline uint64_t norm_heavy_slots(const argcsr_dev* m) {
-    return heavy_blocked(m) ? uint64_t(m->num_heavy) : uint64_t(m->heavy_ctas);
-}
+// Heavy groups run packed into m->heavy_ctas CTAs (one norm partial each).
+inline uint64_t norm_heavy_slots(const argcsr_dev* m) { return uint64_t(m->heavy_ctas); }
 inline uint64_t norm_slots(const argcsr_dev* m) { return norm_heavy_slots(m) + m->num_tiles; }
 
 // out[0] = the sum of partials[0 .. n) in a fixed order (two levels of fixed

@@ -180,7 +180,7 @@ def test_skew_and_uniform_families(argcsr, orc, ref):  # acceptance.cpp:171-198
 
 
 # --------------------------------------------------------- larger / edge cases
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16", "ARGCSR_LIGHT_DYN=0", "ARGCSR_LIGHT_DYN=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_PIPE=1", "ARGCSR_LIGHT_DYN=0", "ARGCSR_LIGHT_DYN=1"])
 @pytest.mark.parametrize("tpg,dcs", [(128, 1), (128, 4), (64, 2), (32, 1), (100, 1), (30, 3), (127, 1), (256, 1)])
 def test_powerlaw_heavy_groups(argcsr, orc, tpg, dcs, heavy, monkeypatch):
     """Heavy-tailed rows: long-chunk (heavy) groups, multi-tile schedule,
@@ -245,7 +245,7 @@ def test_unsorted_columns_copied_in_stored_order(argcsr, orc):
 
 # ---------------------------------------------------------------- other APIs
 @pytest.mark.parametrize("layout", LAYOUTS)
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_BLOCKED=1", "ARGCSR_HEAVY_RUNS=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_PIPE=1", "ARGCSR_HEAVY_PIPE=0"])
 def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout, heavy, monkeypatch):
     import torch
 
@@ -346,7 +346,7 @@ def test_torch_device_path(argcsr, orc):
         argcsr.spmv_torch(dev, x[:-1])
 
 
-HEAVY_VARIANTS = ["default", "ARGCSR_HEAVY_BLOCKED=1", "ARGCSR_HEAVY_RUNS=1", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_U=4", "ARGCSR_HEAVY_B=5", "ARGCSR_HEAVY_PIPE=8", "ARGCSR_HEAVY_PIPE=6"]
+HEAVY_VARIANTS = ["default", "ARGCSR_HEAVY_PIPE=1", "ARGCSR_HEAVY_PIPE=0"]
 
 
 @pytest.mark.parametrize("heavy", HEAVY_VARIANTS)

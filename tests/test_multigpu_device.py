@@ -27,7 +27,7 @@ def test_fused_scale_is_bit_identical(argcsr, orc, x_remap):
     assert bits(y1.cpu().numpy()) == bits(ref)
 
 
-@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_U=16", "ARGCSR_HEAVY_RUNS=1"])
+@pytest.mark.parametrize("heavy", ["default", "ARGCSR_HEAVY_PIPE=1", "ARGCSR_HEAVY_PIPE=0"])
 def test_fused_scale_heavy_groups(argcsr, orc, heavy, monkeypatch):
     """The fused scale through the long-chunk kernel variants."""
     from helpers import powerlaw_csr

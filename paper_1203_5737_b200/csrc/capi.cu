@@ -54,6 +54,7 @@ Knobs read_knobs() {
     if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
     v.ulen = flag("ARGCSR_ULEN", -1);
     if (const char* e = std::getenv("ARGCSR_CARVEOUT")) v.carveout = std::atoi(e);
+    if (const char* e = std::getenv("ARGCSR_VEC")) v.vec = std::atoi(e);
     v.trace = flag("ARGCSR_TRACE", 0) == 1;
     return v;
 }

@@ -143,6 +143,7 @@ struct Knobs {
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)
     int ulen = -1;                // ARGCSR_ULEN: per-unit lengths (1/0)
+    int vec = 0;                  // ARGCSR_VEC: cap the light unit width V (1 | 2; 0 = library decides)
     int carveout = -1;            // ARGCSR_CARVEOUT: preferred shared-memory carve-out in percent (-1: driver)
     bool trace = false;           // ARGCSR_TRACE=1: per-phase host timings of the converter on stderr
 };

@@ -706,7 +706,10 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     // SpMV also fixes the lane-compact stride granularity.
     const bool compact = m->layout == kLayoutCompact;
     // (V divides tpg, so a compact stride never exceeds threads_per_group)
-    const uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
+    uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
+    // experiments: ARGCSR_VEC = 1 | 2 caps the unit width (one or two lanes per
+    // thread: a warp's x gathers then cover consecutive lanes)
+    if (knobs().vec > 0 && uint32_t(knobs().vec) < V) V = uint32_t(knobs().vec);
     const StrideOf<TM> stride_of{assigned, tpg, V, compact};
     // experiments: ARGCSR_HEAVY_CHUNK moves the light/heavy boundary (1..32;
     // measured on C3: 16 -> 1.79 ms, 8 -> 2.39, 4 -> 2.66 vs 1.64 at 32)

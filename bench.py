@@ -781,6 +781,12 @@ def other_configs(args, dev, stream, peak):
             cfg = workloads.CONFIGS[name]
             tdtype = torch.float64 if cfg["dtype"] == "float64" else torch.float32
             sv = 8 if tdtype == torch.float64 else 4
+            # warm-up conversion of this dtype first: the first use of a dtype's
+            # kernels (lazy module loading) is not part of the conversion time
+            _w = workloads.stencil3d27(12, dev)
+            argcsr.argcsr_from_torch(_w.num_rows, _w.num_cols, _w.row_pointers, _w.columns, _w.values.to(tdtype),
+                                     args.tpg, args.dcs, stream=stream).free()
+            del _w
             A = cfg["gen"](dev)
             vals = A.values.to(tdtype).contiguous()
             torch.cuda.synchronize()  # the CSR is produced on the default stream

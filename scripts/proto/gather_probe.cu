@@ -126,3 +126,56 @@ extern "C" int probe_gather(int variant, const int32_t* cols, uint64_t n, const 
     }
     return int(cudaGetLastError());
 }
+
+// Unit-walk probe on a uniform j-major layout (C2-like: groups of W lanes x C
+// steps, stored j-major): thread = unit of 4 lanes, walks its C steps with
+// 4-wide vector loads, gathers, sums per lane (no row sums).  IL = 0: unit u'
+// holds lanes 4u'..4u'+3 (the product layout); IL = 1: lanes u' + k*W/4
+// (interleaved storage: the 4 lanes of a vector are W/4 apart, so a warp's
+// gather instruction covers consecutive lanes).  The storage is the same
+// array; only which column/value belongs to which lane changes, so the probe
+// just reads cols/vals as laid out and the lane order is a property of the
+// input arrays prepared by the driver.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_unit_walk(const int32_t* cols, const double* vals, uint64_t ngroups,
+                                                         uint32_t W, uint32_t C, const double* x, double* out) {
+    const uint64_t pc = pol_normal(), px = pol_last();
+    const uint32_t upg = W / 4;
+    const uint64_t nunits = ngroups * upg;
+    double acc = 0.0;
+    for (uint64_t u = uint64_t(blockIdx.x) * 256 + threadIdx.x; u < nunits; u += uint64_t(gridDim.x) * 256) {
+        const uint64_t g = u / upg, up = u % upg;
+        const uint64_t base = g * uint64_t(W) * C + up * 4;
+        int c[4][4];
+        double v[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (uint32_t(j) < C) {
+                ld_cols4(cols + base + uint64_t(j) * W, c[j], pc);
+                ld_vals4(vals + base + uint64_t(j) * W, v[j], pc);
+            } else {
+#pragma unroll
+                for (int l = 0; l < 4; ++l) c[j][l] = -1, v[j][l] = 0.0;
+            }
+        }
+        double s[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int l = 0; l < 4; ++l)
+                if (c[j][l] >= 0) s[l] += v[j][l] * ldx<0>(x + c[j][l], px);
+        acc += s[0] + s[1] + s[2] + s[3];
+    }
+    if (acc == 12345.678) out[0] = acc;
+}
+
+extern "C" int probe_unit_walk(int minb, const int32_t* cols, const double* vals, uint64_t ngroups, uint32_t W,
+                               uint32_t C, const double* x, double* out, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (minb == 5) k_unit_walk<5><<<sms * 5, 256, 0, s>>>(cols, vals, ngroups, W, C, x, out);
+    else k_unit_walk<4><<<sms * 4, 256, 0, s>>>(cols, vals, ngroups, W, C, x, out);
+    return int(cudaGetLastError());
+}

@@ -210,6 +210,7 @@ struct argcsr_dev {
     uint64_t num_groups = 0, total_slots = 0, max_chunk = 0;
     uint32_t max_light_chunk = 0;         // largest chunk_size among the short-chunk (light) groups
     uint32_t heavy_chunk = 32;            // groups with chunk_size above this are heavy
+    bool powerlaw_schedule = false;       // one lane per unit, 2048-unit light tiles (convert.cu)
     int layout = argcsr_gpu::kLayoutCompact;
     uint64_t stored_slots = 0;            // length of values/columns (== total_slots in the reference layout)
     bool tm16 = true;  // threads_mapping / assigned stored as u16 (tpg <= 65535)

@@ -584,9 +584,9 @@ __global__ void __launch_bounds__(256) k5_from_reference(const GroupDesc* __rest
 
 // Units per light tile (default kDefaultTileUnits; a tile is one CTA of kTileThreads).
 // ARGCSR_TILE_THREADS (128 .. 2048) sets the units per tile (experiments).
-uint64_t tile_threads_setting() {
+uint64_t tile_threads_setting(uint64_t dflt) {
     const long v = knobs().tile_threads;
-    return (v >= 128 && v <= 2048 && v % 128 == 0) ? uint64_t(v) : uint64_t(kDefaultTileUnits);
+    return (v >= 128 && v <= 2048 && v % 128 == 0) ? uint64_t(v) : dflt;
 }
 
 unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
@@ -705,15 +705,31 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     // K4: offsets (+ total slots), descriptors.  The vector width V of the
     // SpMV also fixes the lane-compact stride granularity.
     const bool compact = m->layout == kLayoutCompact;
-    // (V divides tpg, so a compact stride never exceeds threads_per_group)
-    uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
-    // experiments: ARGCSR_VEC = 1 | 2 caps the unit width (one or two lanes per
-    // thread: a warp's x gathers then cover consecutive lanes)
-    if (knobs().vec > 0 && uint32_t(knobs().vec) < V) V = uint32_t(knobs().vec);
-    const StrideOf<TM> stride_of{assigned, tpg, V, compact};
     // experiments: ARGCSR_HEAVY_CHUNK moves the light/heavy boundary (1..32;
     // measured on C3: 16 -> 1.79 ms, 8 -> 2.39, 4 -> 2.66 vs 1.64 at 32)
     m->heavy_chunk = knobs().heavy_chunk ? knobs().heavy_chunk : kHeavyChunk;
+    {
+        DevPtr<unsigned long long> mx(2, s);
+        CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
+        k4_max_chunk<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, G, m->heavy_chunk, mx.p);
+        LAUNCH_OK("k4_max_chunk");
+        unsigned long long mc[2] = {0, 0};
+        CUDA_OK(cudaMemcpyAsync(mc, mx.p, sizeof mc, cudaMemcpyDeviceToHost, s));
+        CUDA_OK(cudaStreamSynchronize(s));
+        m->max_chunk = mc[0];
+        m->max_light_chunk = uint32_t(mc[1]);
+    }
+    // (V divides tpg, so a compact stride never exceeds threads_per_group)
+    uint32_t V = (tpg % 4 == 0) ? 4 : (tpg % 2 == 0) ? 2 : 1;
+    // Power-law matrices (heavy groups AND long light lanes, chunk >= 8: R-MAT)
+    // run the light tiles one lane per thread over 2048-unit tiles: C3 1.54
+    // vs 1.64 ms (repeated A/B, profiles/r02/r02_vecab.jsonl); matrices with
+    // short light lanes keep V = 4 (C2 0.38 vs 0.30, C4 0.72 vs 0.62 at V = 1).
+    m->powerlaw_schedule = compact && knobs().vec == 0 && m->max_chunk > m->heavy_chunk && m->max_light_chunk >= 8;
+    if (m->powerlaw_schedule) V = 1;
+    // experiments: ARGCSR_VEC = 1 | 2 caps the unit width
+    if (knobs().vec > 0 && uint32_t(knobs().vec) < V) V = uint32_t(knobs().vec);
+    const StrideOf<TM> stride_of{assigned, tpg, V, compact};
     const HeavyOf<TM> heavy_of{chunk.p, stride_of, m->heavy_chunk};
     DevPtr<uint64_t> offset(uint64_t(G) + 1, s);
     exclusive_scan(SlotsOf{chunk.p, tpg}, G, offset.p, s);  // reference offsets
@@ -742,17 +758,6 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
                                                                   compact ? off_heavy.p : nullptr, light_total,
                                                                   heavy_of, G, N32, m->groups);
     LAUNCH_OK("k4_fill_desc");
-    {
-        DevPtr<unsigned long long> mx(2, s);
-        CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));
-        k4_max_chunk<<<grid_for(G, 256), 256, 0, s>>>(chunk.p, G, m->heavy_chunk, mx.p);
-        LAUNCH_OK("k4_max_chunk");
-        unsigned long long mc[2] = {0, 0};
-        CUDA_OK(cudaMemcpyAsync(mc, mx.p, sizeof mc, cudaMemcpyDeviceToHost, s));
-        CUDA_OK(cudaStreamSynchronize(s));
-        m->max_chunk = mc[0];
-        m->max_light_chunk = uint32_t(mc[1]);
-    }
     m->total_slots = total_slots;
     m->stored_slots = stored_slots;
     m->light_slots = light_total;
@@ -815,7 +820,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     // Tile keys every `span` units so that a tile (span + at most one group's
     // units - 1) fits one CTA pass when a group has at most half a CTA of units.
     const uint64_t maxu = (tpg + V - 1) / V;
-    const uint64_t tt = tile_threads_setting();
+    const uint64_t tt = tile_threads_setting(m->powerlaw_schedule ? 2048 : kDefaultTileUnits);
     const uint64_t span = maxu <= tt / 2 ? tt - maxu + 1 : tt;
     m->tile_span = span;
     m->tile_threads = uint32_t(tt);

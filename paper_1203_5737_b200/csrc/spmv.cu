@@ -634,7 +634,8 @@ void launch_v(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     switch (m->lanes_per_unit) {
         case 4: launch_light<T, 4, 4, false, 5, PEER, NORM>(m, a, s); break;
         case 2: launch_light<T, 2, 4, false, 5, PEER, NORM>(m, a, s); break;
-        default: launch_light<T, 1, 4, false, 5, PEER, NORM>(m, a, s); break;
+        // one lane per unit: 40 registers, 6 CTAs/SM (C3 1.538 vs 1.552 ms at 5)
+        default: launch_light<T, 1, 4, false, 6, PEER, NORM>(m, a, s); break;
     }
 }
 

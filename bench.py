@@ -383,6 +383,17 @@ def run_b200(args):
                                          layout=args.layout, x_remap=args.x_remap)
     torch.cuda.synchronize()
     conv_ms = 1e3 * (time.perf_counter() - t_conv)  # host wall clock: conversion synchronises
+    conv_repeat_ms = None
+    if not distributed_path:
+        # the same conversion again: the first one also pays the driver's first
+        # mapping of ~1.4 GB of fresh device memory
+        t_conv = time.perf_counter()
+        with torch.cuda.stream(stream):
+            argcsr.argcsr_from_torch(A.num_rows, A.num_cols, A.row_pointers.contiguous(), A.columns.contiguous(),
+                                     A.values.to(tdtype).contiguous(), args.tpg, args.dcs, stream=stream,
+                                     layout=args.layout, x_remap=args.x_remap).free()
+        torch.cuda.synchronize()
+        conv_repeat_ms = round(1e3 * (time.perf_counter() - t_conv), 3)
 
     x = workloads.bench_input(A.num_cols, dev, tdtype)
     y = torch.empty(m.num_rows, dtype=tdtype, device=dev)
@@ -474,7 +485,11 @@ def run_b200(args):
                      "peak_source": peak_src, "alg_bytes_per_launch": ab,
                      "kernel": "spmv_light_kernel (+ spmv_heavy_kernel when heavy groups exist), one SpMV",
                      "read_ceiling_GBps": READ_CEILING_GBS},
-        "conversion_ms": round(conv_ms, 3), "generation_s": round(gen_s, 3), "format": info,
+        "conversion_ms": round(conv_ms, 3), "conversion_repeat_ms": conv_repeat_ms,
+        "conversion_note": ("per-GPU slice conversions plus the multi-GPU handle setup (NCCL communicator, halo plan)"
+                            if distributed_path else "host wall clock around argcsr_from_torch after a warm-up "
+                            "conversion; conversion_repeat_ms = the same conversion again"),
+        "generation_s": round(gen_s, 3), "format": info,
         "clocks": clocks, "gpu_launches": launches,
         "layout": args.layout,
     }

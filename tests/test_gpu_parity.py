@@ -194,6 +194,30 @@ def test_powerlaw_heavy_groups(argcsr, orc, tpg, dcs, heavy, monkeypatch):
     assert dev.heavy_groups > 0
 
 
+@pytest.mark.parametrize("layout_opt", ["auto", "ARGCSR_VEC=4"])
+def test_powerlaw_schedule_one_lane_units(argcsr, orc, layout_opt, monkeypatch):
+    """Power-law matrices (heavy groups AND light lanes of >= 8 steps) run the
+    light tiles one lane per unit over 2048-unit tiles (convert.cu
+    powerlaw_schedule): the stored lane stride is then the assigned lane count
+    itself, not rounded up to 4.  Bit-exact either way."""
+    if layout_opt != "auto":
+        monkeypatch.setenv(*layout_opt.split("="))
+        argcsr._ext.reload_options()
+    A = powerlaw_csr(60000, 60000, seed=31, heavy_rows=[(5, 30000), (40000, 20000)])
+    M = orc.argcsr_from_csr(A, 128, 1)
+    G = np.asarray(M.groups).reshape(-1, 4).astype(np.int64)
+    tm = np.asarray(M.threads_mapping).astype(np.int64)
+    last = np.concatenate([G[1:, 0], [A.num_rows]]) - 1
+    assigned, chunk = tm[last], G[:, 3]
+    assert chunk.max() > 32 and chunk[chunk <= 32].max() >= 8  # the schedule's precondition
+    _check_case(argcsr, orc, A, 128, 1, f"powerlaw schedule ({layout_opt})")
+    dev = to_dev(argcsr, A, 128, 1)  # lane-compact, x remap auto
+    exact = int((chunk * assigned).sum())
+    rounded = int((chunk * ((assigned + 3) // 4 * 4)).sum())
+    assert exact < rounded
+    assert dev.stored_slots == (exact if layout_opt == "auto" else rounded)
+
+
 @pytest.mark.parametrize("tpg", [1, 2, 1024, 1025, 4000, 16384])
 def test_extreme_threads_per_group(argcsr, orc, tpg):
     """tpg > 1024 takes the sequential group walk; 16384 is the device limit."""

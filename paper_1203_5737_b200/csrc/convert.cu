@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(256) k5_from_reference(const GroupDesc* __rest
 // ARGCSR_TILE_THREADS (128 .. 2048) sets the units per tile (experiments).
 uint64_t tile_threads_setting(uint64_t dflt) {
     const long v = knobs().tile_threads;
-    return (v >= 128 && v <= 8192 && v % 128 == 0) ? uint64_t(v) : dflt;
+    return (v >= 128 && v <= 8192 && v % 32 == 0) ? uint64_t(v) : dflt;
 }
 
 unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {

@@ -141,7 +141,7 @@ struct Knobs {
     char heavy_pipe = 0;          // ARGCSR_HEAVY_PIPE: '1' pipelined / '0' plain lane walk (default: fp32 pipelined)
     char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
-    int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile CTA size (0 = default)
+    int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile size in units (multiple of 32; 0 = 512, 2048 power-law)
     int ulen = -1;                // ARGCSR_ULEN: per-unit lengths (1/0)
     int vec = 0;                  // ARGCSR_VEC: cap the light unit width V (1 | 2; 0 = library decides)
     int carveout = -1;            // ARGCSR_CARVEOUT: preferred shared-memory carve-out in percent (-1: driver)

@@ -48,7 +48,7 @@ Knobs read_knobs() {
     v.pair = flag("ARGCSR_PAIR", 1);
     v.light_dyn = flag("ARGCSR_LIGHT_DYN", -1);
     v.heavy_pipe = chr("ARGCSR_HEAVY_PIPE", 0);
-    if (const char* e = std::getenv("ARGCSR_HEAVY_CHUNK")) v.heavy_chunk = uint32_t(std::min(32, std::max(0, std::atoi(e))));
+    if (const char* e = std::getenv("ARGCSR_HEAVY_CHUNK")) v.heavy_chunk = uint32_t(std::min(250, std::max(0, std::atoi(e))));
     v.aux_prio = chr("ARGCSR_AUX_PRIO", 'h');
     v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
     if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);

@@ -705,7 +705,7 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     // K4: offsets (+ total slots), descriptors.  The vector width V of the
     // SpMV also fixes the lane-compact stride granularity.
     const bool compact = m->layout == kLayoutCompact;
-    // experiments: ARGCSR_HEAVY_CHUNK moves the light/heavy boundary (1..32;
+    // experiments: ARGCSR_HEAVY_CHUNK moves the light/heavy boundary (1..250;
     // measured on C3: 16 -> 1.79 ms, 8 -> 2.39, 4 -> 2.66 vs 1.64 at 32)
     m->heavy_chunk = knobs().heavy_chunk ? knobs().heavy_chunk : kHeavyChunk;
     {

@@ -142,6 +142,7 @@ struct Knobs {
     char aux_prio = 'h';          // ARGCSR_AUX_PRIO: heavy stream priority h(ighest) | l(owest) | d(efault)
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile size in units (multiple of 32; 0 = 512, 2048 power-law)
+    int l2pf = -1;                // ARGCSR_L2PF: light-tile L2 prefetch off (0) / on (1) / on up to N KB per tile (N > 1)
     int ulen = -1;                // ARGCSR_ULEN: per-unit lengths (1/0)
     int vec = 0;                  // ARGCSR_VEC: cap the light unit width V (1 | 2; 0 = library decides)
     int carveout = -1;            // ARGCSR_CARVEOUT: preferred shared-memory carve-out in percent (-1: driver)

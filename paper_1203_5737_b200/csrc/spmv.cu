@@ -61,6 +61,7 @@ struct SpmvArgs {
     double* norm_part;       // fused ||y||^2: one partial per CTA (heavy CTAs first, then light tiles), or null
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
+    uint32_t l2_prefetch;    // light tiles of at most this many stored bytes bulk-prefetch them into L2 (0: off)
     uint32_t npeers;         // multi-GPU epilogue: y rows in [peer_lo[q], peer_hi[q]) are also stored
     T* peer_y[kMaxPeers];    // to peer_y[q][row] (other GPUs' x buffers via NVLink peer mappings, pre-offset)
     uint32_t peer_lo[kMaxPeers], peer_hi[kMaxPeers];
@@ -414,6 +415,40 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
     if constexpr (NORM) write_norm_partial(a.norm_part + blockIdx.x, sq);
 }
 
+// L2 prefetch of a light tile's matrix block: the tile's light groups are
+// stored back to back, so its values and columns are two contiguous ranges.
+// The last warp issues them as 16 KB cp.async.bulk.prefetch.L2 pieces at CTA
+// start, so the DRAM reads run under the metadata staging and the unit loads
+// find their lines in L2.  Only for tiles of at most a.l2_prefetch bytes (the
+// prefetched blocks of the resident tiles must survive in L2 until used; see
+// l2_prefetch_bytes), and skipped when an end group is heavy (stored apart).
+template <typename T>
+__device__ __forceinline__ void tile_prefetch_l2(const SpmvArgs<T>& a, uint32_t gs, uint32_t ge) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t b = 0, e = 0;
+    if (lane == 0) {
+        const GroupDesc d0 = a.groups[gs], d1 = a.groups[ge - 1];
+        if (!d0.heavy() && !d1.heavy()) {
+            b = d0.offset();
+            e = d1.offset() + uint64_t(d1.chunk) * d1.stride();
+        }
+    }
+    b = __shfl_sync(0xFFFFFFFFu, b, 0);
+    e = __shfl_sync(0xFFFFFFFFu, e, 0);
+    if (e <= b || (e - b) * (sizeof(T) + sizeof(int32_t)) > a.l2_prefetch) return;
+    auto issue = [&](const char* base, uint64_t esz) {
+        const uint64_t lo = (uint64_t(reinterpret_cast<uintptr_t>(base)) + b * esz) & ~uint64_t(15);
+        const uint64_t hi = (uint64_t(reinterpret_cast<uintptr_t>(base)) + e * esz + 15) & ~uint64_t(15);
+        constexpr uint64_t kPiece = 16384;
+        for (uint64_t p = lo + uint64_t(lane) * kPiece; p < hi; p += 32 * kPiece) {
+            const uint32_t n = uint32_t(min(kPiece, hi - p));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
+        }
+    };
+    issue(reinterpret_cast<const char*>(a.vals), sizeof(T));
+    issue(reinterpret_cast<const char*>(a.cols), sizeof(int32_t));
+}
+
 // Light tile kt: consecutive short-chunk groups, V-lane units, one unit per thread.
 // MAP: every unit and row of the tile gets its group index in shared memory
 // while the metadata loads (one thread per group, so only for small groups);
@@ -436,6 +471,7 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
         return;
     }
     const uint32_t ng = ge - gs;
+    if (a.l2_prefetch && threadIdx.x >= blockDim.x - 32) tile_prefetch_l2(a, gs, ge);
     const uint32_t cap = a.max_tile_groups;
     // smem: s_part[max_tile_units * V] | s_off[cap] | s_ub[cap+1] | s_first[cap+1] | s_chunk[cap]
     //       | s_ugrp[max_tile_units] | s_rgrp[max_tile_rows]  (unit / row -> group in tile)
@@ -678,6 +714,23 @@ void launch_all(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     }
 }
 
+// Light-tile L2 prefetch bound (bytes per tile; 0 = off).  On when x (or x')
+// fits the persisting access-policy window, so x is L2-resident and the
+// prefetched blocks only compete with each other; tiles above 256 KB are not
+// prefetched.  Measured (gpu_r02_l2pf*.sh, ms, same box): C2 (128,1) 0.323 ->
+// 0.308, C2 (128,4) 0.339 -> 0.303, C4 0.617 -> 0.605; C2 (128,32) (768 KB
+// tiles) 0.254 -> 0.368 if prefetched; C5 on one GPU (x = 262 MB, beyond the
+// window) 2.63 -> 3.55 and R-MAT 1.52 -> 1.71 if prefetched.
+// ARGCSR_L2PF=0|1|N forces it off / on (256 KB) / on up to N KB (experiments).
+uint32_t l2_prefetch_bytes(const argcsr_dev* m) {
+    constexpr uint32_t kMaxTileBytes = 256 * 1024;
+    const int k = knobs().l2pf;
+    if (k >= 0) return k == 0 ? 0u : k == 1 ? kMaxTileBytes : uint32_t(std::min(k, 1 << 20)) * 1024u;
+    const size_t xbytes = m->n_used * (m->dtype == ARGCSR_F64 ? sizeof(double) : sizeof(float));
+    const size_t win = std::min<size_t>(size_t(m->l2_window_max), m->l2_persist_max);
+    return knobs().l2_window && xbytes <= win ? kMaxTileBytes : 0u;
+}
+
 template <typename T>
 void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint32_t ge, cudaStream_t s,
                   const SpmvExtra& ex) {
@@ -719,6 +772,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     // values/columns: L2 evict_normal (evict_first measured slower once the heavy
     // stream is prioritised: C4 0.69 vs 0.73, C3 0.323 vs 0.325); ARGCSR_SPOL=1 for A/B
     a.stream_evict_first = knobs().stream_evict_first;
+    a.l2_prefetch = l2_prefetch_bytes(m);
 
     if (a.npeers) {
         if (a.norm_part) launch_all<T, true, true>(m, a, s);
@@ -756,6 +810,7 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
     a.x_scale = nullptr;
     a.x_evict_last = 1;
     a.stream_evict_first = 0;
+    a.l2_prefetch = l2_prefetch_bytes(m);
     a.tile0 = t0;
     const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
     const unsigned grid = t1 - t0;

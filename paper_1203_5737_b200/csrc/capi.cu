@@ -98,6 +98,7 @@ void free_handle(argcsr_dev* m) {
     cudaFree(m->assigned);
     cudaFree(m->unit_base);
     cudaFree(m->tiles);
+    cudaFree(m->tile_rng);
     cudaFree(m->ulen);
     cudaFree(m->heavy);
     cudaFree(m->heavy_ptr);

@@ -226,6 +226,7 @@ struct argcsr_dev {
     int lanes_per_unit = 1;               // V: 4 | 2 | 1 (tpg % V == 0)
     uint64_t* unit_base = nullptr;        // [num_groups + 1] exclusive scan of light units
     uint32_t* tiles = nullptr;            // [num_tiles + 1] first group of each light tile
+    uint64_t* tile_rng = nullptr;         // [2 * num_tiles] stored slot range of each light tile (L2 prefetch)
     uint32_t* heavy = nullptr;            // [num_heavy] heavy groups, chunk descending (LPT)
     uint32_t* heavy_ptr = nullptr;        // [heavy_ctas + 1] packing of `heavy` into CTAs
     uint32_t num_tiles = 0, num_heavy = 0, heavy_ctas = 0;

@@ -368,6 +368,27 @@ __global__ void k4_tiles(const uint64_t* __restrict__ unit_base, uint32_t G, uin
 }
 
 // Largest tile: groups (out[0]) and rows (out[1]).
+// Per light tile, the stored slot range [lo, hi) of its groups (contiguous:
+// light groups are stored back to back), for the SpMV's L2 prefetch; (0, 0)
+// when an end group is heavy (stored apart) or the tile is empty.
+__global__ void k4_tile_ranges(const uint32_t* __restrict__ tiles, uint32_t ntiles,
+                               const GroupDesc* __restrict__ desc, uint64_t* __restrict__ rng) {
+    for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < ntiles;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t gs = tiles[k], ge = tiles[k + 1];
+        uint64_t lo = 0, hi = 0;
+        if (ge > gs) {
+            const GroupDesc d0 = desc[gs], d1 = desc[ge - 1];
+            if (!d0.heavy() && !d1.heavy()) {
+                lo = d0.offset();
+                hi = d1.offset() + uint64_t(d1.chunk) * d1.stride();
+            }
+        }
+        rng[2 * k] = lo;
+        rng[2 * k + 1] = hi;
+    }
+}
+
 __global__ void k4_max_tile_groups(const uint32_t* __restrict__ tiles, uint32_t ntiles,
                                    const GroupDesc* __restrict__ desc, unsigned long long* __restrict__ out) {
     uint64_t m = 0, mr = 0;
@@ -831,6 +852,11 @@ void layout_and_schedule(argcsr_dev* m, uint32_t G, const uint32_t* first_row, c
     m->tiles = dev_alloc<uint32_t>(m, ntiles + 1);
     k4_tiles<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(m->unit_base, G, uint32_t(ntiles), span, m->tiles);
     LAUNCH_OK("k4_tiles");
+    m->tile_rng = dev_alloc<uint64_t>(m, 2 * std::max<uint64_t>(ntiles, 1));
+    if (ntiles) {
+        k4_tile_ranges<<<grid_for(ntiles, 256), 256, 0, s>>>(m->tiles, uint32_t(ntiles), m->groups, m->tile_rng);
+        LAUNCH_OK("k4_tile_ranges");
+    }
     {
         DevPtr<unsigned long long> mx(2, s);
         CUDA_OK(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), s));

@@ -46,6 +46,7 @@ struct SpmvArgs {
     const uint8_t* __restrict__ ulen;  // light unit lengths (null: read up to the group's chunk)
     uint64_t total_units;
     const uint32_t* __restrict__ tiles;
+    const uint64_t* __restrict__ tile_rng;  // [2 * tiles] stored slot range per light tile (0, 0: none)
     const uint32_t* __restrict__ heavy;
     const uint32_t* __restrict__ heavy_ptr;
     const T* __restrict__ x;
@@ -53,6 +54,7 @@ struct SpmvArgs {
     uint32_t heavy_ctas;
     uint32_t norm_light0;     // first light-tile slot of norm_part (after the heavy CTAs' slots)
     uint32_t g_begin, g_end;  // rows of groups outside [g_begin, g_end) are not written
+    uint32_t all_groups;      // [g_begin, g_end) covers every group
     uint32_t max_tile_groups;
     uint32_t max_tile_rows;
     uint32_t tile0;  // light tiles [tile0, tile0 + gridDim.x) of this launch (spmv_launch_tiles)
@@ -416,25 +418,17 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_heavy_kernel(const Sp
 }
 
 // L2 prefetch of a light tile's matrix block: the tile's light groups are
-// stored back to back, so its values and columns are two contiguous ranges.
-// The last warp issues them as 16 KB cp.async.bulk.prefetch.L2 pieces at CTA
-// start, so the DRAM reads run under the metadata staging and the unit loads
-// find their lines in L2.  Only for tiles of at most a.l2_prefetch bytes (the
-// prefetched blocks of the resident tiles must survive in L2 until used; see
-// l2_prefetch_bytes), and skipped when an end group is heavy (stored apart).
+// stored back to back, so its values and columns are two contiguous ranges
+// (tile_rng, from the converter: no dependent metadata load).  The last warp
+// issues them as 16 KB cp.async.bulk.prefetch.L2 pieces at CTA start, so the
+// DRAM reads run under the metadata staging and the unit loads find their
+// lines in L2.  Only for tiles of at most a.l2_prefetch bytes (the prefetched
+// blocks of the resident tiles must survive in L2 until used; see
+// l2_prefetch_bytes).
 template <typename T>
-__device__ __forceinline__ void tile_prefetch_l2(const SpmvArgs<T>& a, uint32_t gs, uint32_t ge) {
+__device__ __forceinline__ void tile_prefetch_l2(const SpmvArgs<T>& a, uint32_t kt) {
     const uint32_t lane = threadIdx.x & 31;
-    uint64_t b = 0, e = 0;
-    if (lane == 0) {
-        const GroupDesc d0 = a.groups[gs], d1 = a.groups[ge - 1];
-        if (!d0.heavy() && !d1.heavy()) {
-            b = d0.offset();
-            e = d1.offset() + uint64_t(d1.chunk) * d1.stride();
-        }
-    }
-    b = __shfl_sync(0xFFFFFFFFu, b, 0);
-    e = __shfl_sync(0xFFFFFFFFu, e, 0);
+    const uint64_t b = a.tile_rng[2 * uint64_t(kt)], e = a.tile_rng[2 * uint64_t(kt) + 1];
     if (e <= b || (e - b) * (sizeof(T) + sizeof(int32_t)) > a.l2_prefetch) return;
     auto issue = [&](const char* base, uint64_t esz) {
         const uint64_t lo = (uint64_t(reinterpret_cast<uintptr_t>(base)) + b * esz) & ~uint64_t(15);
@@ -465,13 +459,15 @@ __global__ void __launch_bounds__(kTileThreads, MINB) spmv_light_kernel(const Sp
     const double xs = x_scale_value(a);
 
     const uint32_t kt = a.tile0 + blockIdx.x;
+    // every tile is in range (the whole matrix): prefetch before anything else
+    if (a.l2_prefetch && a.all_groups && threadIdx.x >= blockDim.x - 32) tile_prefetch_l2(a, kt);
     const uint32_t gs = a.tiles[kt], ge = a.tiles[kt + 1];
     if (ge <= a.g_begin || gs >= a.g_end || gs == ge) {
         if (NORM && threadIdx.x == 0) a.norm_part[a.norm_light0 + kt] = 0.0;
         return;
     }
+    if (a.l2_prefetch && !a.all_groups && threadIdx.x >= blockDim.x - 32) tile_prefetch_l2(a, kt);
     const uint32_t ng = ge - gs;
-    if (a.l2_prefetch && threadIdx.x >= blockDim.x - 32) tile_prefetch_l2(a, gs, ge);
     const uint32_t cap = a.max_tile_groups;
     // smem: s_part[max_tile_units * V] | s_off[cap] | s_ub[cap+1] | s_first[cap+1] | s_chunk[cap]
     //       | s_ugrp[max_tile_units] | s_rgrp[max_tile_rows]  (unit / row -> group in tile)
@@ -756,6 +752,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     a.ulen = m->ulen;
     a.total_units = m->total_units;
     a.tiles = m->tiles;
+    a.tile_rng = m->tile_rng;
     a.heavy = m->heavy;
     a.heavy_ptr = m->heavy_ptr;
     a.x = static_cast<const T*>(x);
@@ -764,6 +761,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     a.norm_light0 = uint32_t(norm_heavy_slots(m));
     a.g_begin = gb;
     a.g_end = ge;
+    a.all_groups = gb == 0 && ge >= m->num_groups;
     a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
     a.max_tile_rows = m->max_tile_rows;
     a.tile0 = 0;
@@ -797,6 +795,7 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
     a.ulen = m->ulen;
     a.total_units = m->total_units;
     a.tiles = m->tiles;
+    a.tile_rng = m->tile_rng;
     a.heavy = m->heavy;
     a.heavy_ptr = m->heavy_ptr;
     a.x = static_cast<const T*>(x);
@@ -804,6 +803,7 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
     a.heavy_ctas = 0;
     a.g_begin = 0;
     a.g_end = uint32_t(m->num_groups);
+    a.all_groups = 1;
     a.max_tile_groups = std::max<uint32_t>(m->max_tile_groups, 1);
     a.max_tile_rows = m->max_tile_rows;
     a.max_tile_units = uint32_t(m->max_tile_units);

@@ -42,7 +42,7 @@ Knobs read_knobs() {
     };
     v.l2_window = flag("ARGCSR_L2_WINDOW", 1) != 0;
     v.l2_persist = flag("ARGCSR_L2_PERSIST", 1) != 0;
-    v.x_evict_last = flag("ARGCSR_XPOL", 1);
+    v.x_evict_last = flag("ARGCSR_XPOL", -1);
     v.stream_evict_first = flag("ARGCSR_SPOL", 0);
     v.map = flag("ARGCSR_MAP", -1);
     v.pair = flag("ARGCSR_PAIR", 1);

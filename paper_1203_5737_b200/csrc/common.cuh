@@ -132,7 +132,7 @@ constexpr int kDefaultTileUnits = 512;
 struct Knobs {
     bool l2_window = true;        // ARGCSR_L2_WINDOW=0: no persisting access-policy window for x
     bool l2_persist = true;       // ARGCSR_L2_PERSIST=0: do not raise the device's persisting-L2 limit
-    int x_evict_last = 1;         // ARGCSR_XPOL: x gathers L2 evict_last (1) / evict_normal (0)
+    int x_evict_last = -1;        // ARGCSR_XPOL: x gathers L2 evict_last (1) / evict_normal (0) (-1: library decides)
     int stream_evict_first = 0;   // ARGCSR_SPOL: values/columns L2 evict_first (1) / evict_normal (0)
     int map = -1;                 // ARGCSR_MAP: unit/row -> group maps in shared memory (1/0)
     int pair = 1;                 // ARGCSR_PAIR=0: never the paired-unit light kernel

@@ -710,21 +710,37 @@ void launch_all(const argcsr_dev* m, const SpmvArgs<T>& a, cudaStream_t s) {
     }
 }
 
-// Light-tile L2 prefetch bound (bytes per tile; 0 = off).  On when x (or x')
-// fits the persisting access-policy window, so x is L2-resident and the
-// prefetched blocks only compete with each other; tiles above 256 KB are not
-// prefetched.  Measured (gpu_r02_l2pf*.sh, ms, same box): C2 (128,1) 0.323 ->
-// 0.308, C2 (128,4) 0.339 -> 0.303, C4 0.617 -> 0.605; C2 (128,32) (768 KB
-// tiles) 0.254 -> 0.368 if prefetched; C5 on one GPU (x = 262 MB, beyond the
-// window) 2.63 -> 3.55 and R-MAT 1.52 -> 1.71 if prefetched.
-// ARGCSR_L2PF=0|1|N forces it off / on (256 KB) / on up to N KB (experiments).
+// L2 policy of a handle ("tile L2 prefetch"): x (x') fits the
+// persisting window -- x gathers evict_last, light tiles prefetched; x larger
+// than the window on a regular matrix (no long-chunk groups, no power-law
+// schedule: stencil-like, x reused within a band of rows) -- x gathers
+// evict_normal and tiles prefetched (evict_last x lines would crowd the
+// prefetched blocks out of L2); power-law matrices with a large x (R-MAT) --
+// evict_last, no prefetch (their hot x columns need the L2).
+// Measured (ms, one box each): C2 (128,1) 0.331 -> 0.293, C2 (128,4) 0.345 ->
+// 0.306, C1 0.0348 -> 0.0338, C4 0.619 -> 0.608 (x fits); C5 on one GPU 2.315
+// -> 2.108 (evict_normal + prefetch; prefetch with evict_last x: 2.63 ->
+// 3.55); R-MAT 1.52 -> 1.71 if prefetched; C2 (128,32) 0.254 -> 0.368 if its
+// 768 KB tiles were prefetched, hence the 256 KB bound.
+// ARGCSR_L2PF=0|1|N forces the prefetch off / on (256 KB) / on up to N KB and
+// ARGCSR_XPOL=0|1 the x policy (experiments).
+bool x_fits_window(const argcsr_dev* m) {
+    const size_t xbytes = m->n_used * (m->dtype == ARGCSR_F64 ? sizeof(double) : sizeof(float));
+    const size_t win = std::min<size_t>(size_t(m->l2_window_max), m->l2_persist_max);
+    return knobs().l2_window && xbytes <= win;
+}
+bool regular_matrix(const argcsr_dev* m) { return m->num_heavy == 0 && !m->powerlaw_schedule; }
+
 uint32_t l2_prefetch_bytes(const argcsr_dev* m) {
     constexpr uint32_t kMaxTileBytes = 256 * 1024;
     const int k = knobs().l2pf;
     if (k >= 0) return k == 0 ? 0u : k == 1 ? kMaxTileBytes : uint32_t(std::min(k, 1 << 20)) * 1024u;
-    const size_t xbytes = m->n_used * (m->dtype == ARGCSR_F64 ? sizeof(double) : sizeof(float));
-    const size_t win = std::min<size_t>(size_t(m->l2_window_max), m->l2_persist_max);
-    return knobs().l2_window && xbytes <= win ? kMaxTileBytes : 0u;
+    return x_fits_window(m) || regular_matrix(m) ? kMaxTileBytes : 0u;
+}
+int x_evict_last(const argcsr_dev* m) {
+    const int k = knobs().x_evict_last;
+    if (k >= 0) return k;
+    return x_fits_window(m) || !regular_matrix(m) ? 1 : 0;
 }
 
 template <typename T>
@@ -766,7 +782,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     a.max_tile_rows = m->max_tile_rows;
     a.tile0 = 0;
     a.max_tile_units = uint32_t(m->max_tile_units);
-    a.x_evict_last = knobs().x_evict_last;
+    a.x_evict_last = x_evict_last(m);
     // values/columns: L2 evict_normal (evict_first measured slower once the heavy
     // stream is prioritised: C4 0.69 vs 0.73, C3 0.323 vs 0.325); ARGCSR_SPOL=1 for A/B
     a.stream_evict_first = knobs().stream_evict_first;
@@ -808,7 +824,7 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
     a.max_tile_rows = m->max_tile_rows;
     a.max_tile_units = uint32_t(m->max_tile_units);
     a.x_scale = nullptr;
-    a.x_evict_last = 1;
+    a.x_evict_last = x_evict_last(m);
     a.stream_evict_first = 0;
     a.l2_prefetch = l2_prefetch_bytes(m);
     a.tile0 = t0;

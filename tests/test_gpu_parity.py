@@ -295,6 +295,38 @@ def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout, heavy, monkeypatc
         assert bits(y.cpu().numpy()) == bits(y_ref), f"groups [{gb},{ge})"
 
 
+@pytest.mark.parametrize("policy", ["ARGCSR_L2PF=0", "ARGCSR_L2PF=1", "ARGCSR_L2PF=1,ARGCSR_XPOL=0",
+                                    "ARGCSR_L2PF=2,ARGCSR_XPOL=1"])
+def test_l2_policy_variants(argcsr, orc, policy, monkeypatch):
+    """The light tiles' L2 prefetch (spmv.cu tile_prefetch_l2: forced off, on,
+    on with evict_normal x, on with a 2 KB tile bound) only moves lines into
+    L2: results stay bit-identical, including group sub-ranges (the prefetch
+    then follows the range check)."""
+    import torch
+
+    for kv in policy.split(","):
+        monkeypatch.setenv(*kv.split("="))
+    argcsr._ext.reload_options()
+    A = stencil27(40)
+    for tpg, dcs in ((128, 1), (128, 4), (32, 1)):
+        _check_case(argcsr, orc, A, tpg, dcs, f"stencil27(40) ({tpg},{dcs}) {policy}")
+    P = powerlaw_csr(30000, 30000, seed=4, heavy_rows=[(17, 12000)])
+    _check_case(argcsr, orc, P, 128, 1, f"powerlaw {policy}")
+    ref_m = orc.argcsr_from_csr(A, 128, 1)
+    dev = to_dev(argcsr, A, 128, 1)
+    x = np.cos(np.arange(A.num_cols, dtype=np.float64))
+    full = orc.spmv_argcsr(ref_m, x)
+    G = dev.num_groups
+    for gb, ge in ((0, G), (7, G // 2), (G // 3, G)):
+        y = torch.full((A.num_rows,), 7.0, dtype=torch.float64, device="cuda")
+        argcsr.spmv_argcsr_groups(dev, torch.from_numpy(x).cuda(), gb, ge, y)
+        y_ref = np.full(A.num_rows, 7.0)
+        r0 = int(ref_m.groups[gb, 0])
+        r1 = int(ref_m.groups[ge, 0]) if ge < G else A.num_rows
+        y_ref[r0:r1] = full[r0:r1]
+        assert bits(y.cpu().numpy()) == bits(y_ref), f"groups [{gb},{ge}) {policy}"
+
+
 def test_padding_stats_matches_reference(argcsr, orc, ref, corpus):
     for A in corpus[:60]:
         for (tpg, dcs), layout in ((t, l) for t in ((4, 1), (32, 4), (128, 1)) for l in LAYOUTS):

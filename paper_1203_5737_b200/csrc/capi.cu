@@ -53,6 +53,7 @@ Knobs read_knobs() {
     v.async_split = flag("ARGCSR_ASYNC_SPLIT", 1) != 0;
     if (const char* e = std::getenv("ARGCSR_TILE_THREADS")) v.tile_threads = std::atoi(e);
     v.ulen = flag("ARGCSR_ULEN", -1);
+    v.l2pf_what = chr("ARGCSR_L2PF_WHAT", 0);
     if (const char* e = std::getenv("ARGCSR_L2PF")) v.l2pf = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("ARGCSR_CARVEOUT")) v.carveout = std::atoi(e);
     if (const char* e = std::getenv("ARGCSR_VEC")) v.vec = std::atoi(e);

@@ -143,6 +143,7 @@ struct Knobs {
     bool async_split = true;      // ARGCSR_ASYNC_SPLIT=0: one copy stream per direction
     int tile_threads = 0;         // ARGCSR_TILE_THREADS: light-tile size in units (multiple of 32; 0 = 512, 2048 power-law)
     int l2pf = -1;                // ARGCSR_L2PF: light-tile L2 prefetch off (0) / on (1) / on up to N KB per tile (N > 1)
+    char l2pf_what = 0;           // ARGCSR_L2PF_WHAT: prefetch b(oth) / c(olumns) / v(alues) of a tile (0: library decides)
     int ulen = -1;                // ARGCSR_ULEN: per-unit lengths (1/0)
     int vec = 0;                  // ARGCSR_VEC: cap the light unit width V (1 | 2; 0 = library decides)
     int carveout = -1;            // ARGCSR_CARVEOUT: preferred shared-memory carve-out in percent (-1: driver)

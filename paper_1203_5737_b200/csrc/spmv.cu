@@ -64,6 +64,7 @@ struct SpmvArgs {
     int x_evict_last;        // x gathers: L2 evict_last (1) or evict_normal (0)
     int stream_evict_first;  // values/columns: L2 evict_first (1) or evict_normal (0)
     uint32_t l2_prefetch;    // light tiles of at most this many stored bytes bulk-prefetch them into L2 (0: off)
+    char l2_prefetch_what;   // 'b' values and columns, 'c' columns only, 'v' values only (experiments)
     uint32_t npeers;         // multi-GPU epilogue: y rows in [peer_lo[q], peer_hi[q]) are also stored
     T* peer_y[kMaxPeers];    // to peer_y[q][row] (other GPUs' x buffers via NVLink peer mappings, pre-offset)
     uint32_t peer_lo[kMaxPeers], peer_hi[kMaxPeers];
@@ -429,7 +430,7 @@ template <typename T>
 __device__ __forceinline__ void tile_prefetch_l2(const SpmvArgs<T>& a, uint32_t kt) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t b = a.tile_rng[2 * uint64_t(kt)], e = a.tile_rng[2 * uint64_t(kt) + 1];
-    if (e <= b || (e - b) * (sizeof(T) + sizeof(int32_t)) > a.l2_prefetch) return;
+    if (e <= b || (e - b) * (sizeof(T) + sizeof(int32_t)) > a.l2_prefetch) return;  // bound: the tile's bytes
     auto issue = [&](const char* base, uint64_t esz) {
         const uint64_t lo = (uint64_t(reinterpret_cast<uintptr_t>(base)) + b * esz) & ~uint64_t(15);
         const uint64_t hi = (uint64_t(reinterpret_cast<uintptr_t>(base)) + e * esz + 15) & ~uint64_t(15);
@@ -439,8 +440,8 @@ __device__ __forceinline__ void tile_prefetch_l2(const SpmvArgs<T>& a, uint32_t 
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(n) : "memory");
         }
     };
-    issue(reinterpret_cast<const char*>(a.vals), sizeof(T));
-    issue(reinterpret_cast<const char*>(a.cols), sizeof(int32_t));
+    if (a.l2_prefetch_what != 'c') issue(reinterpret_cast<const char*>(a.vals), sizeof(T));
+    if (a.l2_prefetch_what != 'v') issue(reinterpret_cast<const char*>(a.cols), sizeof(int32_t));
 }
 
 // Light tile kt: consecutive short-chunk groups, V-lane units, one unit per thread.
@@ -737,6 +738,16 @@ uint32_t l2_prefetch_bytes(const argcsr_dev* m) {
     if (k >= 0) return k == 0 ? 0u : k == 1 ? kMaxTileBytes : uint32_t(std::min(k, 1 << 20)) * 1024u;
     return x_fits_window(m) || regular_matrix(m) ? kMaxTileBytes : 0u;
 }
+// What a tile prefetches: only its columns on a regular matrix whose x fits
+// the window (the gathers wait on the columns; the values load in parallel
+// with the gathers and need no head start: C2 0.294 -> 0.285 ms, C2 (128,4)
+// 0.304 -> 0.297 against both arrays), both arrays otherwise (C5 2.11 vs 2.17,
+// C4 0.608 vs 0.615 with columns only).  ARGCSR_L2PF_WHAT=b|c|v forces it.
+char l2_prefetch_what(const argcsr_dev* m) {
+    const char k = knobs().l2pf_what;
+    if (k == 'b' || k == 'c' || k == 'v') return k;
+    return x_fits_window(m) && regular_matrix(m) ? 'c' : 'b';
+}
 int x_evict_last(const argcsr_dev* m) {
     const int k = knobs().x_evict_last;
     if (k >= 0) return k;
@@ -787,6 +798,7 @@ void launch_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t gb, uint
     // stream is prioritised: C4 0.69 vs 0.73, C3 0.323 vs 0.325); ARGCSR_SPOL=1 for A/B
     a.stream_evict_first = knobs().stream_evict_first;
     a.l2_prefetch = l2_prefetch_bytes(m);
+    a.l2_prefetch_what = l2_prefetch_what(m);
 
     if (a.npeers) {
         if (a.norm_part) launch_all<T, true, true>(m, a, s);
@@ -827,6 +839,7 @@ void launch_tiles_dtype(const argcsr_dev* m, const void* x, void* y, uint32_t t0
     a.x_evict_last = x_evict_last(m);
     a.stream_evict_first = 0;
     a.l2_prefetch = l2_prefetch_bytes(m);
+    a.l2_prefetch_what = l2_prefetch_what(m);
     a.tile0 = t0;
     const double per_group = m->num_groups ? double(m->total_units + m->num_rows) / double(m->num_groups) : 0.0;
     const unsigned grid = t1 - t0;

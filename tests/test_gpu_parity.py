@@ -295,13 +295,14 @@ def test_spmv_groups_writes_only_its_rows(argcsr, orc, layout, heavy, monkeypatc
         assert bits(y.cpu().numpy()) == bits(y_ref), f"groups [{gb},{ge})"
 
 
-@pytest.mark.parametrize("policy", ["ARGCSR_L2PF=0", "ARGCSR_L2PF=1", "ARGCSR_L2PF=1,ARGCSR_XPOL=0",
-                                    "ARGCSR_L2PF=2,ARGCSR_XPOL=1"])
+@pytest.mark.parametrize("policy", ["ARGCSR_L2PF=0", "ARGCSR_L2PF=1,ARGCSR_L2PF_WHAT=b",
+                                    "ARGCSR_L2PF=1,ARGCSR_L2PF_WHAT=c,ARGCSR_XPOL=0",
+                                    "ARGCSR_L2PF=2,ARGCSR_L2PF_WHAT=v,ARGCSR_XPOL=1"])
 def test_l2_policy_variants(argcsr, orc, policy, monkeypatch):
-    """The light tiles' L2 prefetch (spmv.cu tile_prefetch_l2: forced off, on,
-    on with evict_normal x, on with a 2 KB tile bound) only moves lines into
-    L2: results stay bit-identical, including group sub-ranges (the prefetch
-    then follows the range check)."""
+    """The light tiles' L2 prefetch (spmv.cu tile_prefetch_l2: forced off; on
+    for both arrays; columns only with evict_normal x; values only with a 2 KB
+    tile bound) only moves lines into L2: results stay bit-identical,
+    including group sub-ranges (the prefetch then follows the range check)."""
     import torch
 
     for kv in policy.split(","):

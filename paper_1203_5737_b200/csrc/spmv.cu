@@ -21,8 +21,12 @@
 // fp64 and round each row sum once.
 //
 // Cache policy: values/columns are streamed once (L1 no-allocate, L2
-// evict-first); x gathers are L2 evict-last and x is additionally covered by a
+// evict-normal); x gathers are L2 evict-last and x is additionally covered by a
 // persisting access-policy window sized from the device's persisting-L2 limit.
+// Light tiles bulk-prefetch their stored block into L2 at CTA start
+// (tile_prefetch_l2; which arrays, and the x policy of regular matrices whose x
+// exceeds the window, are per handle: l2_prefetch_bytes / l2_prefetch_what /
+// x_evict_last).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>

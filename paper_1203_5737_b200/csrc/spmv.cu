@@ -436,8 +436,11 @@ __device__ __forceinline__ void tile_prefetch_l2(const SpmvArgs<T>& a, uint32_t 
     const uint64_t b = a.tile_rng[2 * uint64_t(kt)], e = a.tile_rng[2 * uint64_t(kt) + 1];
     if (e <= b || (e - b) * (sizeof(T) + sizeof(int32_t)) > a.l2_prefetch) return;  // bound: the tile's bytes
     auto issue = [&](const char* base, uint64_t esz) {
+        // 16-B granules inside [base + b, base + e): the range start rounded down
+        // stays inside the (256-B aligned) allocation, the end is rounded down
+        // so no prefetch reaches past the array's last byte
         const uint64_t lo = (uint64_t(reinterpret_cast<uintptr_t>(base)) + b * esz) & ~uint64_t(15);
-        const uint64_t hi = (uint64_t(reinterpret_cast<uintptr_t>(base)) + e * esz + 15) & ~uint64_t(15);
+        const uint64_t hi = (uint64_t(reinterpret_cast<uintptr_t>(base)) + e * esz) & ~uint64_t(15);
         constexpr uint64_t kPiece = 16384;
         for (uint64_t p = lo + uint64_t(lane) * kPiece; p < hi; p += 32 * kPiece) {
             const uint32_t n = uint32_t(min(kPiece, hi - p));
